@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the batched FCG-NO hot path on B200 (BASELINE.json metric and configs).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
+
+A step is one fcgno_fcg_solve over the whole batch of configs[1] (config 2: 64x64 grid, batch 64,
+FCG(m=5), tol 1e-6, random-init SNO width 48 in fp32 with fp64 FCG vectors; the random-init NO
+does not converge, so every step runs maxit = 2000 iterations).  value =
+unknown-iterations/s = sum_b N*iters_b over all ranks / max-over-ranks device time.  Under
+torchrun each rank solves its own batch of independent systems (weak scaling, no data-path
+collective).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "batched FCG-NO unknown-iterations/s on 1 B200; % of HBM roofline per iteration"
+UNIT = "unknown-iterations/s"
+K_MODES = 20
+FP32_ALU_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SMs x FP32 lanes x FMA x max SM clock
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--maxit", type=int, default=None, help="override the config's maxit")
+    ap.add_argument("--no-split", action="store_true", help="skip the instrumented time-split solve")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args(argv)
+
+
+# ----------------------------------------------------------------------------- distributed plumbing
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def reduce_over_ranks(units: float, ms: float, backend_device=None):
+    """(sum of units, max of ms) over all ranks; identity when not distributed."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return units, ms
+    dev = backend_device or "cpu"
+    u = torch.tensor([units], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(u, op=dist.ReduceOp.SUM)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(u.item()), float(t.item())
+
+
+def shard_systems(batch: int, rank: int):
+    """Weak scaling: rank r solves systems [r*B, (r+1)*B) of the seeded stream."""
+    return list(range(rank * batch, (rank + 1) * batch))
+
+
+# ----------------------------------------------------------------------------- workload model
+def layer_flops(B, n, w, cin):
+    """Algorithmic FLOPs of one SNO operator layer over the batch:
+    bypass 2*cin*w*N, x-synthesis 4K*w*N, x-analysis 4K*w*N, y-synthesis and y-analysis
+    8K^2*w*n each."""
+    N = n * n
+    return B * (2 * cin * w * N + 8 * K_MODES * w * N + 16 * K_MODES * K_MODES * w * n)
+
+
+def mean_window(m, iters):
+    import synthetic  # noqa: F401
+    tot = 0
+    for i in range(iters):
+        tot += min(i, max(1, i % (m + 1)))
+    return tot / max(iters, 1)
+
+
+def fcg_no_bytes_per_unknown(m_bar, w):
+    """Algorithmic HBM bytes per unknown per FCG-NO iteration (fused-minimal
+    FCG part with fp64 vectors, plus the NO's input/output and materialised fp32 activations
+    v1..v3 written and read once)."""
+    S = 8
+    fcg = (9 + 2 * m_bar) * S + 8
+    no = S + 8 + S + 6 * w * 4
+    return fcg + no
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1])); smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU baseline (oracle)
+def cpu_oracle_rate(cfg, budget_s=12.0, max_iters=400):
+    """The oracle as it stands: FCG-NO (fp64 NO, exact dots) on system 0 of the workload, on one
+    host thread, for as many iterations as fit ~budget_s.  Returns (unknown-iterations/s, sample)."""
+    import numpy as np
+    from threadpoolctl import threadpool_limits
+
+    import oracle as orc
+    import synthetic as sy
+    with threadpool_limits(limits=1):
+        k = sy.make_k(cfg, systems=[0])[0]
+        f = sy.make_f(cfg, systems=[0])[0]
+        params = orc.unpack_weights(sy.make_weights(cfg), cfg["width"])
+        A = lambda x: orc.apply_A(k, x)
+        P = lambda r: orc.no_forward(params, r, k)
+        t0 = time.perf_counter()
+        orc.fcg(A, f, np.zeros_like(f), cfg["m"], cfg["tol"], 3, precond=P)
+        per_it = (time.perf_counter() - t0) / 3
+        iters = int(max(5, min(max_iters, budget_s / max(per_it, 1e-6))))
+        t0 = time.perf_counter()
+        res = orc.fcg(A, f, np.zeros_like(f), cfg["m"], cfg["tol"], iters, precond=P)
+        dt = time.perf_counter() - t0
+    N = cfg["n"] ** 2
+    done = res["iters"]
+    return N * done / dt, f"system 0 of the workload, {done} FCG-NO iterations (fp64 NO, exact dots), {dt:.1f} s"
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synthetic as sy
+    from paper_2402_05598_b200 import fcgno as F
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = dict(sy.CONFIGS[args.config])
+    if args.maxit:
+        cfg["maxit"] = args.maxit
+    n, B, w, m = cfg["n"], cfg["batch"], cfg["width"], cfg["m"]
+    N = n * n
+    systems = shard_systems(B, rank)
+    k = sy.make_k(cfg, systems=systems)
+    f = sy.make_f(cfg, systems=systems)
+    blob = sy.make_weights(cfg)
+    dk = torch.from_numpy(k).cuda()
+    df = torch.from_numpy(f).cuda()
+    prob = F.Problem(dk)
+    no = F.NeuralOperator(w, blob, precision=F.FP32 if cfg["no_precision"] == "fp32" else F.FP64)
+    solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False,
+                      profile_mask=1 << F.PROF_NO_LAYER)
+    u = torch.zeros_like(df)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    for _ in range(args.warmup):
+        u.zero_()
+        solver.solve(df, u)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    F.profile_reset()
+    launches0 = F.kernel_launches()
+    times, units = [], 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        u.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        solver.solve(df, u)
+        e1.record()
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+        units += float(N) * float(solver.iters.sum().item())
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = F.kernel_launches() - launches0
+    clocks = sampler.stop()
+    prof = F.profile_read()
+    local_ms = sum(times)
+    tot_units, max_ms = reduce_over_ranks(units, local_ms, "cuda" if world > 1 else None)
+    value = tot_units / (max_ms / 1e3)
+    iters_step = float(solver.iters.float().mean().item())
+    ms_per_iter = (local_ms / args.steps) / max(iters_step, 1)
+
+    # dominant kernel: the SNO layer kernel (3 launches per iteration), timed in-graph
+    layer_ms, layer_n = prof["k_no_layer"]
+    avg_layer_ms = layer_ms / max(layer_n, 1)
+    flops_iter = layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)
+    avg_flops = flops_iter / 3
+    achieved = avg_flops / (avg_layer_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"config{args.config}", {}).get("k_no_layer")
+        except (ValueError, OSError):
+            traffic = None
+    roofline = {"kernel": "k_no_layer", "bound": "alu", "achieved": achieved, "peak": FP32_ALU_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP32_ALU_PEAK_TFLOPS, "traffic": traffic,
+                "flops_per_launch": avg_flops, "avg_launch_ms": avg_layer_ms, "launches_timed": layer_n,
+                "share_of_step": layer_ms / local_ms,
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (FFMA path; DESIGN.md §6)"}
+
+    # per-iteration HBM roofline (the metric's second half)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    m_bar = mean_window(m, cfg["maxit"])
+    bytes_iter = fcg_no_bytes_per_unknown(m_bar, w) * N * B
+    hbm_frac = (bytes_iter / (hbm * 1e9)) / (ms_per_iter * 1e-3)
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32 (NO) + f64 (FCG vectors, dots)",
+           "data": "synthetic (seeded; BASELINE configs[1] recipe, random-init NO weights)",
+           "config": {"workload": f"config{args.config}", "n": n, "batch": B, "m": m, "tol": cfg["tol"],
+                      "maxit": cfg["maxit"], "no_width": w, "no_precision": cfg["no_precision"],
+                      "k_field": cfg["k"], "rhs": cfg["rhs"], "l2": "flushed (256 MiB write) before every step",
+                      "parallelism": f"batch replicas x{world} (weak)"},
+           "iterations_per_step": iters_step, "ms_per_iteration": ms_per_iter,
+           "hbm_roofline_per_iteration": {"algorithmic_bytes_per_iter": bytes_iter, "peak_gbs": hbm,
+                                          "frac": hbm_frac},
+           "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks}
+
+    if not args.no_split and rank == 0:
+        out["time_split_ms_per_iter"] = time_split(F, prob, no, cfg, df)
+    if rank == 0:
+        out["e2e"] = e2e_measure(F, no, cfg, k, f, args.steps)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, sample = cpu_oracle_rate(cfg)
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+
+
+def time_split(F, prob, no, cfg, df, iters=64):
+    """Instrumented solve (every kernel class timed in-graph) -> ms per iteration per phase."""
+    import torch
+    s = F.Solver(prob, cfg["m"], cfg["tol"], iters, no=no, history=False, profile_mask=(1 << F.PROF_NCLASS) - 1)
+    u = torch.zeros_like(df)
+    s.solve(df, u)
+    F.profile_reset()
+    u.zero_()
+    s.solve(df, u)
+    torch.cuda.synchronize()
+    prof = F.profile_read()
+    it = iters
+    per = {name: ms / it for name, (ms, cnt) in prof.items() if cnt}
+    stencil = per.get("k_stencil_dots", 0.0)
+    no_ms = sum(per.get(x, 0.0) for x in ("k_no_layer", "k_mix", "k_no_out", "k_dft_rows+k_lift_mix"))
+    upd = sum(per.get(x, 0.0) for x in ("k_window_dots", "k_pform", "k_update", "k_finalize"))
+    return {"stencil": stencil, "no": no_ms, "fcg_update": upd, "per_kernel": per,
+            "note": "CUDA events around every launch inside the graph (instrumented run, 64 iterations)"}
+
+
+def e2e_measure(F, no, cfg, k, f, steps):
+    """Same metric through the host-buffer C-ABI entry point: H2D of k, f, u0 from pinned memory,
+    assemble, solve, D2H of u, iters, status, all inside the timed region."""
+    import numpy as np
+    import torch
+    n, B = cfg["n"], cfg["batch"]
+    hs = F.HostSolver(n, B, cfg["m"], cfg["tol"], cfg["maxit"], no=no)
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+    kh, fh = pin(k), pin(f)
+    uh = torch.zeros((B, n, n), dtype=torch.float64).pin_memory().numpy()
+    ih = torch.zeros(B, dtype=torch.int32).pin_memory().numpy()
+    sh = torch.zeros(B, dtype=torch.int32).pin_memory().numpy()
+    hs.solve(kh, fh, uh, ih, sh)   # warm-up
+    torch.cuda.synchronize()
+    tot_ms, units = 0.0, 0.0
+    for _ in range(steps):
+        uh[...] = 0.0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        hs.solve(kh, fh, uh, ih, sh)
+        e1.record()
+        e1.synchronize()
+        tot_ms += e0.elapsed_time(e1)
+        units += float(n * n) * float(ih.sum())
+    N = n * n
+    return {"value": units / (tot_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 3 * B * N * 8,
+            "d2h_bytes_per_step": B * N * 8 + 2 * 4 * B, "ms_per_step": tot_ms / steps,
+            "api": "fcgno_solve_host (pinned host buffers; includes assemble)"}
+
+
+# ----------------------------------------------------------------------------- reference arm (oracle)
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import synthetic as sy
+    cfg = dict(sy.CONFIGS[args.config])
+    if args.maxit:
+        cfg["maxit"] = args.maxit
+    rates, samples = [], []
+    for step in range(args.warmup + args.steps):
+        rate, sample = cpu_oracle_rate(cfg, budget_s=4.0, max_iters=100)
+        if step >= args.warmup:
+            rates.append(rate); samples.append(sample)
+    value = statistics.mean(rates)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"config{args.config}", "n": cfg["n"], "batch": cfg["batch"], "m": cfg["m"],
+                      "tol": cfg["tol"], "maxit": cfg["maxit"], "no_width": cfg["width"]},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": samples[-1]},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * fcgno.h — C ABI of the B200-native batched FCG-NO solver (libfcgno.so).
+ *
+ * The library solves B independent systems A_b u_b = f_b, the 5-point finite-difference
+ * discretisation of -div(k grad u) = f on (0,1)^2 with u = 0 on the boundary
+ * (§2.1 Eq. 1-2), by Flexible Conjugate Gradients FCG(m) (PAPER.md:96-112,
+ * Algorithm 1) preconditioned at every iteration by a spectral neural operator (SNO, Fourier
+ * basis; §2.4.2 and PAPER.md:530 App. A) or by the identity.
+ *
+ * Conventions shared by every call
+ *   - Grid: n interior nodes per dimension, h = 1/(n+1); a system is stored row-major as
+ *     [n][n] with row index i <-> x2 and column index j <-> x1; a batch is [B][n][n],
+ *     contiguous, system-major (element (b,i,j) at offset (b*n+i)*n+j).  fp64 throughout
+ *     unless stated.
+ *   - Pointers are DEVICE pointers unless marked [host].  The caller (e.g. PyTorch) owns
+ *     all device memory: inputs, outputs, packed weights and workspaces.  The library never
+ *     allocates device memory; it owns only the small host-side fcgno_problem descriptor.
+ *   - `stream` is a cudaStream_t passed as void*.  Calls enqueue work on it.  Calls that
+ *     must report data-dependent errors synchronise it (documented per call).
+ *   - Return value: FCGNO_OK (0) or an fcgno_error code; fcgno_last_error() returns a
+ *     thread-local message for the last non-OK return.  The library never aborts.
+ *   - Numerical failures of one system (breakdown, non-finite preconditioner output) are
+ *     reported per system in status[] and never abort the batch.
+ *   - Workspaces must be 256-byte aligned and at least the size the *_workspace_bytes
+ *     query returns, else FCGNO_EWORKSPACE.
+ */
+#ifndef FCGNO_H
+#define FCGNO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FCGNO_API __attribute__((visibility("default")))
+#else
+#define FCGNO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FCGNO_ABI_VERSION 1
+#define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
+#define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
+#define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
+#define FCGNO_NO_NMAX 512  /* largest grid n accepted by the NO kernels */
+
+typedef enum {
+  FCGNO_OK = 0,
+  FCGNO_EINVAL = 1,       /* bad shape, option or NULL pointer */
+  FCGNO_ENONPOS_K = 2,    /* some k <= 0 or non-finite (SPEC.md:71 NonPositiveCoefficient) */
+  FCGNO_ECUDA = 3,        /* a CUDA runtime error; message in fcgno_last_error() */
+  FCGNO_EWORKSPACE = 4,   /* workspace too small or misaligned */
+  FCGNO_EUNSUPPORTED = 5  /* e.g. NO with n < 20 or n > FCGNO_NO_NMAX, or no sm_100 device */
+} fcgno_error;
+
+/* Per-system solve status (int32 array [B] written by fcgno_fcg_solve). */
+typedef enum {
+  FCGNO_SYS_RUNNING = 0,
+  FCGNO_SYS_CONVERGED = 1,  /* ||r_i||/||r_0|| <= tol at i = iters */
+  FCGNO_SYS_MAXIT = 2,      /* iters == maxit without convergence */
+  FCGNO_SYS_BREAKDOWN = 3,  /* (p_i, s_i) <= 0 or non-finite */
+  FCGNO_SYS_NONFINITE = 4   /* preconditioner output non-finite */
+} fcgno_sys_status;
+
+typedef enum { FCGNO_FP32 = 0, FCGNO_FP64 = 1 } fcgno_precision;
+typedef enum { FCGNO_SCHEDULE_PAPER = 0, FCGNO_SCHEDULE_SLIDING = 1 } fcgno_schedule;
+
+typedef struct {
+  int32_t n;      /* interior nodes per dimension, n >= 2 */
+  int32_t batch;  /* number of independent systems B >= 1 */
+} fcgno_grid;
+
+/* Spectral neural operator: 2 input channels [r/||r||, k], width w, 4 Fourier
+ * layers with FCGNO_K_MODES^2 modes {-10..9}^2, GELU after layers 1-3, 1 output channel.
+ * Canonical fp64 weight blob (the layout fcgno_no_pack reads, [host]):
+ *   E[w][2], bE[w],
+ *   for l = 1..4: W_l[w_out][w_in], b_l[w], R_l[w_in][w_out][20][20][2 (re,im)],
+ *   D[w], bD                                  total 3w + 4(w^2 + w + 800 w^2) + w + 1 doubles. */
+typedef struct {
+  int32_t width;      /* w >= 1 (32 / 48 / 85 in the paper's Table 5) */
+  int32_t precision;  /* FCGNO_FP32 (production) or FCGNO_FP64 (trajectory-parity mode) */
+  int32_t use_gelu;   /* 1; 0 = test-only linear mode */
+} fcgno_no_desc;
+
+typedef struct {
+  int32_t m;            /* truncation parameter m_max, 1 <= m <= FCGNO_MMAX */
+  int32_t maxit;        /* iteration cap >= 0 */
+  double tol;           /* stop at the first i with ||r_i||/||r_0|| <= tol */
+  int32_t schedule;     /* FCGNO_SCHEDULE_PAPER: m_i = min(i, max(1, i mod (m+1)));
+                           FCGNO_SCHEDULE_SLIDING: m_i = min(i, m) */
+  int32_t check_every;  /* iterations per convergence poll and per CUDA-graph replay (0 = default
+                           16); work on converged systems stops immediately regardless, this only
+                           bounds idle tail launches */
+  int32_t profile_mask; /* bit c set: time every launch of kernel class c (fcgno_prof_class) with
+                           CUDA events recorded inside the solve's graphs; 0 = no instrumentation */
+} fcgno_solve_opts;
+
+/* Kernel classes for in-graph CUDA-event profiling (diagnostics; bench.py). */
+typedef enum {
+  FCGNO_PROF_NO_LAYER = 0,   /* k_no_layer: SNO layers 1-3 (the dominant kernel) */
+  FCGNO_PROF_NO_MIX = 1,     /* k_mix: mode-diagonal channel mixing (layers 2-4) */
+  FCGNO_PROF_NO_OUT = 2,     /* k_no_out: layer 4 + projection + window dots */
+  FCGNO_PROF_NO_INPUT = 3,   /* k_dft_rows + k_lift_mix: DFT of r/||r|| and layer-1 mixing */
+  FCGNO_PROF_WINDOW = 4,     /* k_window_dots (identity preconditioner only) */
+  FCGNO_PROF_PFORM = 5,      /* k_pform: p = w - sum beta p */
+  FCGNO_PROF_STENCIL = 6,    /* k_stencil_dots: s = A p, (p,s), (p,r) */
+  FCGNO_PROF_UPDATE = 7,     /* k_update: u, r update, (r,r) */
+  FCGNO_PROF_FINALIZE = 8,   /* k_finalize */
+  FCGNO_PROF_NCLASS = 9
+} fcgno_prof_class;
+
+typedef struct fcgno_problem fcgno_problem;
+
+/* ---------------------------------------------------------------------------------------
+ * assemble(k) — PAPER.md:78-82 (Eq. 2).  Validates k (> 0 and finite, else FCGNO_ENONPOS_K),
+ * precomputes the DFT twiddle tables for n and the NO mode coefficients DFT_M(k) of every
+ * system.  The stencil itself is matrix-free: face coefficients are harmonic means
+ * H(a,b) = (2ab)/(a+b) of nodal k (BASELINE north_star), recomputed on chip.
+ *   k   [B][n][n] fp64 device; must stay alive and unchanged while the problem is used.
+ *   ws  device workspace of fcgno_problem_workspace_bytes(g) bytes; owned by the problem
+ *       until fcgno_problem_destroy.
+ * Synchronises `stream` once (to report FCGNO_ENONPOS_K).  *out receives a host handle. */
+FCGNO_API size_t fcgno_problem_workspace_bytes(fcgno_grid g);
+FCGNO_API int fcgno_assemble(fcgno_grid g, const double* k, void* ws, size_t ws_bytes, void* stream,
+                   fcgno_problem** out);
+FCGNO_API void fcgno_problem_destroy(fcgno_problem* p);
+
+/* apply_A — y = A x for every system ("s_i <- A p_i").
+ *   x, y [B][n][n] fp64 device, y != x.  Canonical op order (R5): d=(kW+kE)+(kS+kN);
+ *   t=d*x; t-=kW*xW; t-=kE*xE; t-=kS*xS; t-=kN*xN; y=t*(n+1)^2, no fused multiply-add. */
+FCGNO_API int fcgno_apply_A(const fcgno_problem* p, const double* x, double* y, void* stream);
+
+/* Batched inner products out[b] = (x_b, y_b), correctly rounded in all but astronomically
+ * rare ties (exact products, double-double accumulation; R6).
+ *   x, y [B][n][n] fp64; out [B] fp64 device; ws of fcgno_dot_workspace_bytes(g) bytes. */
+FCGNO_API size_t fcgno_dot_workspace_bytes(fcgno_grid g);
+FCGNO_API int fcgno_batched_dot(const fcgno_problem* p, const double* x, const double* y, double* out,
+                      void* ws, size_t ws_bytes, void* stream);
+
+/* NO weights: fold and convert the canonical fp64 blob [host] into the device layout the
+ * kernels read (lift folded into layer 1, layer 4 folded into the projection).
+ * `packed` is caller-owned device memory of fcgno_no_packed_bytes(d) bytes.  Synchronises
+ * `stream` before returning (the host staging buffer is then released). */
+FCGNO_API size_t fcgno_no_packed_bytes(fcgno_no_desc d);
+FCGNO_API int fcgno_no_pack(fcgno_no_desc d, const double* weights_host, void* packed, void* stream);
+
+/* apply_NO(weights, r, k) — w_b = ||r_b|| * NO([r_b/||r_b||, k_b]) for every system, w_b = 0
+ * when r_b = 0 ("w_i <- B(r_i)").
+ *   r, w [B][n][n] fp64 device (w != r); requires 20 <= n <= FCGNO_NO_NMAX.
+ *   ws of fcgno_apply_no_workspace_bytes(g, d) bytes. */
+FCGNO_API size_t fcgno_apply_no_workspace_bytes(fcgno_grid g, fcgno_no_desc d);
+FCGNO_API int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, const double* r,
+                   double* w, void* ws, size_t ws_bytes, void* stream);
+
+/* fcg_solve(k, f, m, tol, maxit) — Algorithm 1 on every system, with
+ * w_i = NO(r_i) (d_or_null != NULL) or w_i = r_i (identity preconditioner, d_or_null == NULL).
+ *   f        [B][n][n] fp64 device right-hand sides.
+ *   u        [B][n][n] fp64 device: in = initial guess u0, out = final iterate.
+ *   iters    [B] int32 device: first i with ||r_i||/||r_0|| <= tol (0 if r_0 = 0), else the
+ *            iteration at which the system stopped (maxit, or i of a breakdown).
+ *   status   [B] int32 device: fcgno_sys_status.
+ *   history  [B][maxit+1] fp64 device or NULL: history[b][i] = ||r_i||/||r_0|| for
+ *            i <= iters[b] (entries beyond are left untouched).
+ *   ws       fcgno_solve_workspace_bytes(g, d_or_null, o) bytes.
+ * Converged systems are frozen (no further writes).  Polls an on-device "any system running"
+ * counter every check_every iterations and therefore synchronises `stream` before returning. */
+FCGNO_API size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* d_or_null, fcgno_solve_opts o);
+FCGNO_API int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* d_or_null, const void* packed,
+                    const double* f, double* u, fcgno_solve_opts o, int32_t* iters,
+                    int32_t* status, double* history, void* ws, size_t ws_bytes, void* stream);
+
+/* End-to-end convenience entry point with HOST buffers ([host], pageable or pinned): copies
+ * k, f, u0 to the device, assembles, solves and copies u, iters, status (and history if
+ * non-NULL) back.  `dev_ws` is a device workspace of fcgno_solve_host_workspace_bytes bytes;
+ * `packed` as for fcgno_fcg_solve (already resident).  Synchronises `stream`. */
+FCGNO_API size_t fcgno_solve_host_workspace_bytes(fcgno_grid g, const fcgno_no_desc* d_or_null,
+                                        fcgno_solve_opts o);
+FCGNO_API int fcgno_solve_host(fcgno_grid g, const double* k_host, const double* f_host, double* u_host,
+                     const fcgno_no_desc* d_or_null, const void* packed, fcgno_solve_opts o,
+                     int32_t* iters_host, int32_t* status_host, double* history_host,
+                     void* dev_ws, size_t ws_bytes, void* stream);
+
+/* Accumulated profile of kernel class `cls` since the last reset: total device milliseconds and
+ * number of timed launches (host pointers).  Returns FCGNO_EINVAL for a bad class. */
+FCGNO_API int fcgno_profile_get(int cls, double* total_ms, int64_t* launches);
+FCGNO_API void fcgno_profile_reset(void);
+FCGNO_API const char* fcgno_profile_name(int cls);
+
+/* Number of kernel launches the library issued in this process (diagnostics, bench.py). */
+FCGNO_API uint64_t fcgno_kernel_launches(void);
+FCGNO_API const char* fcgno_last_error(void);
+FCGNO_API int fcgno_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCGNO_H */

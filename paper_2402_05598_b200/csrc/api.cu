@@ -1,0 +1,702 @@
+// api.cu — the extern "C" boundary of libfcgno.so (declared in include/fcgno.h).
+//
+// Host-side responsibilities only: argument validation, workspace carving (the caller owns all
+// device memory), weight folding/packing, and the solve driver, which captures one FCG
+// iteration into a CUDA graph and replays it, polling an on-device "systems still running"
+// counter every check_every iterations (Algorithm 1 runs entirely in kernels).
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/fcgno.h"
+#include "internal.h"
+
+using namespace fcgno;
+
+struct fcgno_problem {
+  int n, B;
+  const double* k;
+  float* F32;
+  double* F64;
+  float* khat32;
+  double* khat64;
+  bool no_ok;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(FCGNO_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t e_ = (call);                              \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #call);   \
+  } while (0)
+
+// Bump allocator over a caller workspace (256-byte aligned regions).  With base == nullptr it
+// only measures.
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(size_t count) {
+    off = (off + 255) & ~size_t(255);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += count * sizeof(T);
+    return p;
+  }
+  size_t bytes() const { return (off + 255) & ~size_t(255); }
+};
+
+bool aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 255u) == 0; }
+int ngroups_of(int n) { return (n + 7) / 8; }
+int nblk_of(int n) { return (n * n + kTile - 1) / kTile; }
+bool no_grid_ok(int n) { return n >= kModes && n <= FCGNO_NO_NMAX; }
+
+struct ProblemWs {
+  float* F32; double* F64; float* khat32; double* khat64; double* part; int* bad;
+};
+ProblemWs carve_problem(Carver& c, int n, int B) {
+  ProblemWs w{};
+  w.bad = c.take<int>(1);
+  w.F32 = c.take<float>((size_t)n * kModes * 2);
+  w.F64 = c.take<double>((size_t)n * kModes * 2);
+  if (no_grid_ok(n)) {
+    w.khat32 = c.take<float>((size_t)B * kModes2 * 2);
+    w.khat64 = c.take<double>((size_t)B * kModes2 * 2);
+    w.part = c.take<double>((size_t)B * ngroups_of(n) * kModes2 * 2);
+  }
+  return w;
+}
+
+template <typename T>
+struct NoWs {
+  T *rpart, *v0, *v1, *chat, *ghat;
+};
+template <typename T>
+NoWs<T> carve_no(Carver& c, int n, int B, int w) {
+  NoWs<T> r{};
+  const size_t N = (size_t)n * n;
+  r.rpart = c.take<T>((size_t)B * ngroups_of(n) * kModes2 * 2);
+  r.v0 = c.take<T>((size_t)B * w * N);
+  r.v1 = c.take<T>((size_t)B * w * N);
+  r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
+  r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
+  return r;
+}
+
+void carve_no_any(Carver& c, int n, int B, const fcgno_no_desc& d, NoWs<float>* f32, NoWs<double>* f64) {
+  if (d.precision == FCGNO_FP64) *f64 = carve_no<double>(c, n, B, d.width);
+  else *f32 = carve_no<float>(c, n, B, d.width);
+}
+
+int check_desc(const fcgno_no_desc& d) {
+  if (d.width < 1 || d.width > 1024) return fail(FCGNO_EINVAL, "NO width %d out of range", d.width);
+  if (d.precision != FCGNO_FP32 && d.precision != FCGNO_FP64) return fail(FCGNO_EINVAL, "bad NO precision");
+  return FCGNO_OK;
+}
+
+template <typename T>
+NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* packed, const NoWs<T>& w,
+                    const T* F, const T* khat) {
+  NoDev<T> no{};
+  no.n = p->n; no.B = p->B; no.N = p->n * p->n; no.w = d.width; no.use_gelu = d.use_gelu;
+  no.k = p->k; no.pk = static_cast<const T*>(packed); no.L = no_layout(d.width);
+  no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
+  no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
+  return no;
+}
+
+int check_no_smem(const fcgno_no_desc& d, int n) {
+  const size_t need = d.precision == FCGNO_FP64 ? no_max_smem<double>(n, d.width) : no_max_smem<float>(n, d.width);
+  if (need > 227 * 1024)
+    return fail(FCGNO_EUNSUPPORTED, "NO width %d at n=%d needs %zu B of shared memory per CTA", d.width, n, need);
+  return FCGNO_OK;
+}
+
+}  // namespace
+
+namespace fcgno {
+NoLayout no_layout(int w) {
+  NoLayout L{};
+  L.w = w;
+  size_t o = 0;
+  auto take = [&](size_t count) {
+    o = (o + 3) & ~size_t(3);
+    const size_t at = o;
+    o += count;
+    return at;
+  };
+  L.W1E = take((size_t)2 * w);
+  L.b1 = take(w);
+  L.A0 = take((size_t)kModes2 * w * 2);
+  L.A1 = take((size_t)kModes2 * w * 2);
+  L.A2 = take((size_t)w * 2);
+  for (int l = 0; l < 2; ++l) {
+    L.W[l] = take((size_t)w * w);
+    L.b[l] = take(w);
+    L.R[l] = take((size_t)kModes2 * w * w * 2);
+  }
+  L.Q = take((size_t)kModes2 * w * 2);
+  L.dw = take(w);
+  L.cst = take(1);
+  L.total = (o + 3) & ~size_t(3);
+  return L;
+}
+}  // namespace fcgno
+
+extern "C" {
+
+const char* fcgno_last_error(void) { return g_err.c_str(); }
+int fcgno_abi_version(void) { return FCGNO_ABI_VERSION; }
+uint64_t fcgno_kernel_launches(void) { return launch_counter(); }
+
+// ------------------------------------------------------------------ problem
+size_t fcgno_problem_workspace_bytes(fcgno_grid g) {
+  if (g.n < 2 || g.batch < 1) return 0;
+  Carver c(nullptr);
+  carve_problem(c, g.n, g.batch);
+  return c.bytes();
+}
+
+int fcgno_assemble(fcgno_grid g, const double* k, void* ws, size_t ws_bytes, void* stream, fcgno_problem** out) {
+  if (!out || !k || !ws) return fail(FCGNO_EINVAL, "assemble: NULL argument");
+  *out = nullptr;
+  if (g.n < 2 || g.batch < 1 || (long long)g.n * g.n > (1LL << 26)) return fail(FCGNO_EINVAL, "assemble: bad grid n=%d B=%d", g.n, g.batch);
+  if (!aligned(ws) || ws_bytes < fcgno_problem_workspace_bytes(g)) return fail(FCGNO_EWORKSPACE, "assemble: workspace too small or misaligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  ProblemWs w = carve_problem(c, g.n, g.batch);
+  CK(cudaMemsetAsync(w.bad, 0, sizeof(int), s));
+  CK(launch_check_k(k, (size_t)g.batch * g.n * g.n, w.bad, s));
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, w.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (bad) return fail(FCGNO_ENONPOS_K, "assemble: k has a non-positive or non-finite entry");
+  CK(launch_twiddles(w.F32, w.F64, g.n, s));
+  const bool no_ok = no_grid_ok(g.n);
+  if (no_ok) {
+    CK(launch_khat<double>(k, w.F64, w.part, w.khat64, g.n, g.batch, ngroups_of(g.n), s));
+    CK(launch_khat<float>(k, w.F32, reinterpret_cast<float*>(w.part), w.khat32, g.n, g.batch, ngroups_of(g.n), s));
+  }
+  fcgno_problem* p = new fcgno_problem{g.n, g.batch, k, w.F32, w.F64, w.khat32, w.khat64, no_ok};
+  *out = p;
+  return FCGNO_OK;
+}
+
+void fcgno_problem_destroy(fcgno_problem* p) { delete p; }
+
+int fcgno_apply_A(const fcgno_problem* p, const double* x, double* y, void* stream) {
+  if (!p || !x || !y) return fail(FCGNO_EINVAL, "apply_A: NULL argument");
+  if (x == y) return fail(FCGNO_EINVAL, "apply_A: y must not alias x");
+  CK(launch_apply_A(p->k, x, y, p->n, p->B, static_cast<cudaStream_t>(stream)));
+  return FCGNO_OK;
+}
+
+size_t fcgno_dot_workspace_bytes(fcgno_grid g) {
+  if (g.n < 2 || g.batch < 1) return 0;
+  Carver c(nullptr);
+  c.take<dd>((size_t)g.batch * nblk_of(g.n));
+  c.take<unsigned>(g.batch);
+  return c.bytes();
+}
+
+int fcgno_batched_dot(const fcgno_problem* p, const double* x, const double* y, double* out, void* ws, size_t ws_bytes,
+                      void* stream) {
+  if (!p || !x || !y || !out || !ws) return fail(FCGNO_EINVAL, "batched_dot: NULL argument");
+  fcgno_grid g{p->n, p->B};
+  if (!aligned(ws) || ws_bytes < fcgno_dot_workspace_bytes(g)) return fail(FCGNO_EWORKSPACE, "batched_dot: workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  dd* part = c.take<dd>((size_t)p->B * nblk_of(p->n));
+  unsigned* cnt = c.take<unsigned>(p->B);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * p->B, s));
+  CK(launch_dot(x, y, out, part, cnt, p->n, p->B, s));
+  return FCGNO_OK;
+}
+
+// ------------------------------------------------------------------ NO weights
+size_t fcgno_no_packed_bytes(fcgno_no_desc d) {
+  if (check_desc(d) != FCGNO_OK) return 0;
+  const size_t tsz = d.precision == FCGNO_FP64 ? sizeof(double) : sizeof(float);
+  return no_layout(d.width).total * tsz;
+}
+
+int fcgno_no_pack(fcgno_no_desc d, const double* blob, void* packed, void* stream) {
+  if (int e = check_desc(d)) return e;
+  if (!blob || !packed) return fail(FCGNO_EINVAL, "no_pack: NULL argument");
+  const int w = d.width, K2 = kModes2;
+  using cd = std::complex<double>;
+  // unpack the canonical blob (include/fcgno.h)
+  size_t pos = 0;
+  auto take = [&](size_t count) { const double* at = blob + pos; pos += count; return at; };
+  const double* E = take((size_t)w * 2);
+  const double* bE = take(w);
+  const double *W[4], *b[4], *R[4];
+  for (int l = 0; l < 4; ++l) {
+    W[l] = take((size_t)w * w);
+    b[l] = take(w);
+    R[l] = take((size_t)w * w * K2 * 2);
+  }
+  const double* D = take(w);
+  const double bD = *take(1);
+  for (size_t t = 0; t < pos; ++t)
+    if (!std::isfinite(blob[t])) return fail(FCGNO_EINVAL, "no_pack: non-finite weight at %zu", t);
+  auto Rc = [&](int l, int c, int o, int kk) {
+    const double* q = R[l] + (((size_t)c * w + o) * K2 + kk) * 2;
+    return cd(q[0], q[1]);
+  };
+  const NoLayout L = no_layout(w);
+  std::vector<double> P(L.total, 0.0);
+  // layer 1 with the lift folded in: W1 (E x + bE) + b1 = (W1 E) x + (W1 bE + b1)
+  for (int o = 0; o < w; ++o) {
+    double a0 = 0, a1 = 0, bb = b[0][o];
+    for (int c = 0; c < w; ++c) {
+      a0 += W[0][(size_t)o * w + c] * E[c * 2 + 0];
+      a1 += W[0][(size_t)o * w + c] * E[c * 2 + 1];
+      bb += W[0][(size_t)o * w + c] * bE[c];
+    }
+    P[L.W1E + o * 2 + 0] = a0;
+    P[L.W1E + o * 2 + 1] = a1;
+    P[L.b1 + o] = bb;
+  }
+  // spectral term of layer 1: sum_c R1[c][o] DFT(E[c,0] r^ + E[c,1] k + bE[c])
+  const int k0 = (kModes / 2) * kModes + kModes / 2;
+  for (int kk = 0; kk < K2; ++kk)
+    for (int o = 0; o < w; ++o) {
+      cd a0 = 0, a1 = 0;
+      for (int c = 0; c < w; ++c) {
+        a0 += Rc(0, c, o, kk) * E[c * 2 + 0];
+        a1 += Rc(0, c, o, kk) * E[c * 2 + 1];
+      }
+      P[L.A0 + ((size_t)kk * w + o) * 2 + 0] = a0.real(); P[L.A0 + ((size_t)kk * w + o) * 2 + 1] = a0.imag();
+      P[L.A1 + ((size_t)kk * w + o) * 2 + 0] = a1.real(); P[L.A1 + ((size_t)kk * w + o) * 2 + 1] = a1.imag();
+    }
+  for (int o = 0; o < w; ++o) {
+    cd a2 = 0;
+    for (int c = 0; c < w; ++c) a2 += Rc(0, c, o, k0) * bE[c];
+    P[L.A2 + o * 2 + 0] = a2.real(); P[L.A2 + o * 2 + 1] = a2.imag();
+  }
+  // layers 2, 3 as they are (R re-laid out mode-major)
+  for (int l = 1; l <= 2; ++l) {
+    for (size_t t = 0; t < (size_t)w * w; ++t) P[L.W[l - 1] + t] = W[l][t];
+    for (int o = 0; o < w; ++o) P[L.b[l - 1] + o] = b[l][o];
+    for (int kk = 0; kk < K2; ++kk)
+      for (int c = 0; c < w; ++c)
+        for (int o = 0; o < w; ++o) {
+          const cd v = Rc(l, c, o, kk);
+          const size_t at = L.R[l - 1] + (((size_t)kk * w + c) * w + o) * 2;
+          P[at] = v.real(); P[at + 1] = v.imag();
+        }
+  }
+  // layer 4 folded with the projection: out = (D W4) v3 + (D b4 + bD) + S(sum_c (R4 D)[c] c3[c])
+  double cst = bD;
+  for (int o = 0; o < w; ++o) cst += D[o] * b[3][o];
+  for (int c = 0; c < w; ++c) {
+    double a = 0;
+    for (int o = 0; o < w; ++o) a += D[o] * W[3][(size_t)o * w + c];
+    P[L.dw + c] = a;
+  }
+  for (int kk = 0; kk < K2; ++kk)
+    for (int c = 0; c < w; ++c) {
+      cd q = 0;
+      for (int o = 0; o < w; ++o) q += Rc(3, c, o, kk) * D[o];
+      P[L.Q + ((size_t)kk * w + c) * 2 + 0] = q.real();
+      P[L.Q + ((size_t)kk * w + c) * 2 + 1] = q.imag();
+    }
+  P[L.cst] = cst;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (d.precision == FCGNO_FP64) {
+    CK(cudaMemcpyAsync(packed, P.data(), P.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  } else {
+    std::vector<float> Pf(P.size());
+    for (size_t t = 0; t < P.size(); ++t) Pf[t] = (float)P[t];
+    CK(cudaMemcpyAsync(packed, Pf.data(), Pf.size() * sizeof(float), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return FCGNO_OK;
+}
+
+// ------------------------------------------------------------------ apply_NO
+size_t fcgno_apply_no_workspace_bytes(fcgno_grid g, fcgno_no_desc d) {
+  if (g.n < 2 || g.batch < 1 || check_desc(d) != FCGNO_OK) return 0;
+  Carver c(nullptr);
+  c.take<double>(g.batch);
+  c.take<dd>((size_t)g.batch * nblk_of(g.n));
+  c.take<unsigned>(g.batch);
+  NoWs<float> a; NoWs<double> b;
+  carve_no_any(c, g.n, g.batch, d, &a, &b);
+  return c.bytes();
+}
+
+int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, const double* r, double* w, void* ws,
+                   size_t ws_bytes, void* stream) {
+  if (!p || !packed || !r || !w || !ws) return fail(FCGNO_EINVAL, "apply_NO: NULL argument");
+  if (r == w) return fail(FCGNO_EINVAL, "apply_NO: w must not alias r");
+  if (int e = check_desc(d)) return e;
+  if (!p->no_ok) return fail(FCGNO_EUNSUPPORTED, "apply_NO: needs %d <= n <= %d (n=%d)", kModes, FCGNO_NO_NMAX, p->n);
+  if (int e = check_no_smem(d, p->n)) return e;
+  fcgno_grid g{p->n, p->B};
+  if (!aligned(ws) || ws_bytes < fcgno_apply_no_workspace_bytes(g, d)) return fail(FCGNO_EWORKSPACE, "apply_NO: workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  double* rr = c.take<double>(p->B);
+  dd* part = c.take<dd>((size_t)p->B * nblk_of(p->n));
+  unsigned* cnt = c.take<unsigned>(p->B);
+  NoWs<float> w32{}; NoWs<double> w64{};
+  carve_no_any(c, p->n, p->B, d, &w32, &w64);
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * p->B, s));
+  CK(launch_dot(r, r, rr, part, cnt, p->n, p->B, s));
+  if (d.precision == FCGNO_FP64) {
+    CK(prepare_no_kernels<double>());
+    NoDev<double> no = make_nodev<double>(p, d, packed, w64, p->F64, p->khat64);
+    CK(launch_no_forward<double>(no, r, rr, w, nullptr, nullptr, s, nullptr));
+  } else {
+    CK(prepare_no_kernels<float>());
+    NoDev<float> no = make_nodev<float>(p, d, packed, w32, p->F32, p->khat32);
+    CK(launch_no_forward<float>(no, r, rr, w, nullptr, nullptr, s, nullptr));
+  }
+  return FCGNO_OK;
+}
+
+// ------------------------------------------------------------------ fcg_solve
+namespace {
+struct SolveWs {
+  FcgDev d;
+  NoWs<float> n32;
+  NoWs<double> n64;
+  double* wvec;
+};
+
+SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgno_solve_opts& o) {
+  SolveWs s{};
+  const size_t N = (size_t)n * n;
+  const int nblk = nblk_of(n);
+  FcgDev& d = s.d;
+  d.r = c.take<double>(B * N);
+  s.wvec = nd ? c.take<double>(B * N) : nullptr;
+  d.ring_p = c.take<double>((size_t)(o.m + 1) * B * N);
+  d.ring_s = c.take<double>((size_t)(o.m + 1) * B * N);
+  d.gamma = c.take<double>((size_t)(o.m + 1) * B);
+  d.beta = c.take<double>((size_t)B * kMmax);
+  d.alpha = c.take<double>(B);
+  d.rr = c.take<double>(B);
+  d.rho0 = c.take<double>(B);
+  d.part_win = c.take<dd>((size_t)B * nblk * kMmax);
+  d.part_step = c.take<dd>((size_t)B * nblk * 2);
+  d.part_rr = c.take<dd>((size_t)B * nblk);
+  d.cnt = c.take<unsigned>((size_t)3 * B);
+  d.flags = c.take<int>(B);
+  d.iter = c.take<int>(2);
+  d.active = d.iter + 1;
+  if (nd) carve_no_any(c, n, B, *nd, &s.n32, &s.n64);
+  return s;
+}
+
+int check_opts(const fcgno_solve_opts& o) {
+  if (o.m < 1 || o.m > FCGNO_MMAX) return fail(FCGNO_EINVAL, "m=%d outside [1, %d]", o.m, FCGNO_MMAX);
+  if (o.maxit < 0) return fail(FCGNO_EINVAL, "maxit < 0");
+  if (o.schedule != FCGNO_SCHEDULE_PAPER && o.schedule != FCGNO_SCHEDULE_SLIDING) return fail(FCGNO_EINVAL, "bad schedule");
+  if (!(o.tol >= 0.0) && !std::isnan(o.tol)) return fail(FCGNO_EINVAL, "tol < 0");
+  return FCGNO_OK;
+}
+
+// In-graph CUDA-event profiler: one (start, end) event pair per instrumented launch of every
+// unrolled iteration of a chunk graph; read back after the chunk completes.
+struct Profiler : ProfHook {
+  int mask = 0;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;          // of the chunk being captured
+  std::vector<Rec> pending;       // open begin() per class
+  bool failed = false;
+  void begin(int cls, cudaStream_t s) override {
+    if (!(mask >> cls & 1)) return;
+    Rec r{cls, nullptr, nullptr};
+    if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) { failed = true; return; }
+    if (cudaEventRecord(r.a, s) != cudaSuccess) failed = true;
+    pending.push_back(r);
+  }
+  void end(int cls, cudaStream_t s) override {
+    if (!(mask >> cls & 1)) return;
+    for (size_t t = pending.size(); t-- > 0;)
+      if (pending[t].cls == cls) {
+        Rec r = pending[t];
+        pending.erase(pending.begin() + t);
+        if (cudaEventRecord(r.b, s) != cudaSuccess) failed = true;
+        recs.push_back(r);
+        return;
+      }
+  }
+};
+
+struct ProfTotals { double ms[PROF_NCLASS]; int64_t n[PROF_NCLASS]; };
+ProfTotals& prof_totals() { static ProfTotals t{}; return t; }
+
+// One FCG iteration (the graph body).  Returns the number of kernels enqueued or -1.
+int enqueue_iteration(const FcgDev& d, const fcgno_no_desc* nd, const void* packed, const fcgno_problem* p,
+                      const SolveWs& sw, cudaStream_t s, ProfHook* prof) {
+  auto pb = [&](int c) { if (prof) prof->begin(c, s); };
+  auto pe = [&](int c) { if (prof) prof->end(c, s); };
+  int count = 0;
+  if (nd) {
+    int nl = 0;
+    cudaError_t e;
+    if (nd->precision == FCGNO_FP64) {
+      NoDev<double> no = make_nodev<double>(p, *nd, packed, sw.n64, p->F64, p->khat64);
+      e = launch_no_forward<double>(no, d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
+    } else {
+      NoDev<float> no = make_nodev<float>(p, *nd, packed, sw.n32, p->F32, p->khat32);
+      e = launch_no_forward<float>(no, d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
+    }
+    if (e != cudaSuccess) return -1;
+    count += nl;
+  } else {
+    pb(PROF_WINDOW);
+    if (launch_window_dots(d, s) != cudaSuccess) return -1;
+    pe(PROF_WINDOW);
+    ++count;
+  }
+  pb(PROF_PFORM);
+  if (launch_pform(d, s) != cudaSuccess) return -1;
+  pe(PROF_PFORM);
+  pb(PROF_STENCIL);
+  if (launch_stencil_dots(d, s) != cudaSuccess) return -1;
+  pe(PROF_STENCIL);
+  pb(PROF_UPDATE);
+  if (launch_update(d, s) != cudaSuccess) return -1;
+  pe(PROF_UPDATE);
+  pb(PROF_FINALIZE);
+  if (launch_finalize(d, s) != cudaSuccess) return -1;
+  pe(PROF_FINALIZE);
+  return count + 4;
+}
+
+// A CUDA graph replaying `iters` unrolled FCG iterations (+ its profiling events).
+struct Chunk {
+  int iters = 0, kernels = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::vector<Profiler::Rec> recs;
+  void destroy() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto& r : recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    exec = nullptr; graph = nullptr; recs.clear();
+  }
+  // Accumulate the event timings of the last replay into the process-wide totals.
+  void harvest() {
+    for (auto& r : recs) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
+        prof_totals().ms[r.cls] += ms;
+        prof_totals().n[r.cls] += 1;
+      }
+    }
+  }
+};
+
+int build_chunk(Chunk& c, int iters, int mask, const FcgDev& d, const fcgno_no_desc* nd, const void* packed,
+                const fcgno_problem* p, const SolveWs& sw, cudaStream_t s) {
+  Profiler prof;
+  prof.mask = mask;
+  c.iters = iters;
+  cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return cuda_fail(e, "graph capture");
+  const uint64_t before = launch_counter();
+  int per_iter = 0;
+  for (int t = 0; t < iters && per_iter >= 0; ++t) per_iter = enqueue_iteration(d, nd, packed, p, sw, s, mask ? &prof : nullptr);
+  launch_counter() = before;  // captured, not launched
+  e = cudaStreamEndCapture(s, &c.graph);
+  c.recs = prof.recs;
+  for (auto& r : prof.pending) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+  if (per_iter < 0 || e != cudaSuccess || prof.failed)
+    return cuda_fail(e != cudaSuccess ? e : cudaGetLastError(), "iteration capture");
+  c.kernels = per_iter * iters;
+  e = cudaGraphInstantiate(&c.exec, c.graph, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
+  return FCGNO_OK;
+}
+}  // namespace
+
+size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd, fcgno_solve_opts o) {
+  if (g.n < 2 || g.batch < 1 || check_opts(o) != FCGNO_OK) return 0;
+  if (nd && check_desc(*nd) != FCGNO_OK) return 0;
+  Carver c(nullptr);
+  carve_solve(c, g.n, g.batch, nd, o);
+  return c.bytes();
+}
+
+int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* f, double* u,
+                    fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (!p || !f || !u || !iters || !status || !ws) return fail(FCGNO_EINVAL, "fcg_solve: NULL argument");
+  if (int e = check_opts(o)) return e;
+  if (nd) {
+    if (int e = check_desc(*nd)) return e;
+    if (!packed) return fail(FCGNO_EINVAL, "fcg_solve: NO descriptor without packed weights");
+    if (!p->no_ok) return fail(FCGNO_EUNSUPPORTED, "fcg_solve: the NO needs %d <= n <= %d (n=%d)", kModes, FCGNO_NO_NMAX, p->n);
+    if (int e = check_no_smem(*nd, p->n)) return e;
+  }
+  fcgno_grid g{p->n, p->B};
+  if (!aligned(ws) || ws_bytes < fcgno_solve_workspace_bytes(g, nd, o)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
+  if (nd) {
+    if (nd->precision == FCGNO_FP64) CK(prepare_no_kernels<double>());
+    else CK(prepare_no_kernels<float>());
+  }
+  cudaStream_t caller = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  SolveWs sw = carve_solve(c, p->n, p->B, nd, o);
+  FcgDev& d = sw.d;
+  d.n = p->n; d.B = p->B; d.N = p->n * p->n; d.nblk = nblk_of(p->n);
+  d.m = o.m; d.maxit = o.maxit; d.schedule = o.schedule; d.tol = o.tol;
+  d.scale = double(p->n + 1) * double(p->n + 1);
+  d.k = p->k; d.f = f; d.u = u; d.w = nd ? sw.wvec : d.r;
+  d.status = status; d.iters = iters; d.hist = history;
+
+  // Private stream (graph capture is not allowed on the legacy default stream), ordered after
+  // everything already enqueued on the caller's stream.
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  cudaEvent_t ev_in, ev_poll[2];
+  CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev_poll[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ev_poll[1], cudaEventDisableTiming));
+  CK(cudaEventRecord(ev_in, caller));
+  CK(cudaStreamWaitEvent(s, ev_in, 0));
+  int* h_active = nullptr;
+  CK(cudaHostAlloc(&h_active, 2 * sizeof(int), cudaHostAllocDefault));
+  int rc = FCGNO_OK;
+  Chunk full[2], tail;
+  do {
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(d.cnt, 0, sizeof(unsigned) * 3 * d.B, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+    if ((e = cudaMemsetAsync(d.iter, 0, 2 * sizeof(int), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+    if ((e = launch_init_residual(d, s)) != cudaSuccess) { rc = cuda_fail(e, "init_residual"); break; }
+    if (o.maxit == 0) break;
+    const int chunk = std::min(o.check_every > 0 ? o.check_every : 16, o.maxit);
+    const int mask = o.profile_mask & ((1 << PROF_NCLASS) - 1);
+    // two replicas of the full chunk when profiling, so a replay never overwrites events that
+    // have not been read yet (the host reads chunk k-1 while chunk k runs)
+    if ((rc = build_chunk(full[0], chunk, mask, d, nd, packed, p, sw, s)) != FCGNO_OK) break;
+    if (mask && (rc = build_chunk(full[1], chunk, mask, d, nd, packed, p, sw, s)) != FCGNO_OK) break;
+    if (o.maxit % chunk && (rc = build_chunk(tail, o.maxit % chunk, mask, d, nd, packed, p, sw, s)) != FCGNO_OK) break;
+    int launched = 0, k = 0;
+    Chunk* prev = nullptr;
+    while (launched < o.maxit) {
+      Chunk* c = (o.maxit - launched >= chunk) ? &full[mask ? (k & 1) : 0] : &tail;
+      if ((e = cudaGraphLaunch(c->exec, s)) != cudaSuccess) { rc = cuda_fail(e, "graph launch"); break; }
+      launch_counter() += (uint64_t)c->kernels;
+      launched += c->iters;
+      if ((e = cudaMemcpyAsync(h_active + (k & 1), d.active, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess) { rc = cuda_fail(e, "poll copy"); break; }
+      if ((e = cudaEventRecord(ev_poll[k & 1], s)) != cudaSuccess) { rc = cuda_fail(e, "poll event"); break; }
+      bool done = false;
+      if (k > 0) {
+        if ((e = cudaEventSynchronize(ev_poll[(k - 1) & 1])) != cudaSuccess) { rc = cuda_fail(e, "poll sync"); break; }
+        if (mask && prev) prev->harvest();
+        done = h_active[(k - 1) & 1] == 0;
+      }
+      prev = c;
+      ++k;
+      if (done) break;
+    }
+    if (rc == FCGNO_OK && (e = cudaStreamSynchronize(s)) == cudaSuccess && mask && prev) prev->harvest();
+  } while (false);
+  cudaError_t e_end = cudaStreamSynchronize(s);
+  if (rc == FCGNO_OK && e_end != cudaSuccess) rc = cuda_fail(e_end, "solve");
+  // order the caller's stream after the solve
+  if (cudaEventRecord(ev_in, s) == cudaSuccess) cudaStreamWaitEvent(caller, ev_in, 0);
+  full[0].destroy(); full[1].destroy(); tail.destroy();
+  cudaFreeHost(h_active);
+  cudaEventDestroy(ev_in);
+  cudaEventDestroy(ev_poll[0]);
+  cudaEventDestroy(ev_poll[1]);
+  cudaStreamDestroy(s);
+  return rc;
+}
+
+int fcgno_profile_get(int cls, double* total_ms, int64_t* launches) {
+  if (cls < 0 || cls >= PROF_NCLASS || !total_ms || !launches) return fail(FCGNO_EINVAL, "profile_get: bad class");
+  *total_ms = prof_totals().ms[cls];
+  *launches = prof_totals().n[cls];
+  return FCGNO_OK;
+}
+
+void fcgno_profile_reset(void) { prof_totals() = ProfTotals{}; }
+
+const char* fcgno_profile_name(int cls) {
+  static const char* names[PROF_NCLASS] = {"k_no_layer", "k_mix", "k_no_out", "k_dft_rows+k_lift_mix",
+                                           "k_window_dots", "k_pform", "k_stencil_dots", "k_update", "k_finalize"};
+  return (cls >= 0 && cls < PROF_NCLASS) ? names[cls] : "";
+}
+
+// ------------------------------------------------------------------ host-buffer end-to-end entry point
+size_t fcgno_solve_host_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd, fcgno_solve_opts o) {
+  const size_t sb = fcgno_solve_workspace_bytes(g, nd, o);
+  if (!sb) return 0;
+  Carver c(nullptr);
+  const size_t BN = (size_t)g.batch * g.n * g.n;
+  c.take<double>(BN); c.take<double>(BN); c.take<double>(BN);
+  c.take<int32_t>(g.batch); c.take<int32_t>(g.batch);
+  c.take<double>((size_t)g.batch * (o.maxit + 1));
+  c.take<char>(fcgno_problem_workspace_bytes(g));
+  c.take<char>(sb);
+  return c.bytes();
+}
+
+int fcgno_solve_host(fcgno_grid g, const double* k_host, const double* f_host, double* u_host,
+                     const fcgno_no_desc* nd, const void* packed, fcgno_solve_opts o, int32_t* iters_host,
+                     int32_t* status_host, double* history_host, void* dev_ws, size_t ws_bytes, void* stream) {
+  if (!k_host || !f_host || !u_host || !iters_host || !status_host || !dev_ws) return fail(FCGNO_EINVAL, "solve_host: NULL argument");
+  const size_t need = fcgno_solve_host_workspace_bytes(g, nd, o);
+  if (!need) return fail(FCGNO_EINVAL, "solve_host: bad grid or options");
+  if (!aligned(dev_ws) || ws_bytes < need) return fail(FCGNO_EWORKSPACE, "solve_host: workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(dev_ws);
+  const size_t BN = (size_t)g.batch * g.n * g.n;
+  double* k = c.take<double>(BN);
+  double* f = c.take<double>(BN);
+  double* u = c.take<double>(BN);
+  int32_t* it = c.take<int32_t>(g.batch);
+  int32_t* st = c.take<int32_t>(g.batch);
+  double* hist = c.take<double>((size_t)g.batch * (o.maxit + 1));
+  const size_t pb = fcgno_problem_workspace_bytes(g);
+  void* pws = c.take<char>(pb);
+  const size_t sb = fcgno_solve_workspace_bytes(g, nd, o);
+  void* sws = c.take<char>(sb);
+  CK(cudaMemcpyAsync(k, k_host, BN * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(f, f_host, BN * sizeof(double), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(u, u_host, BN * sizeof(double), cudaMemcpyHostToDevice, s));
+  fcgno_problem* p = nullptr;
+  if (int e = fcgno_assemble(g, k, pws, pb, stream, &p)) return e;
+  int rc = fcgno_fcg_solve(p, nd, packed, f, u, o, it, st, history_host ? hist : nullptr, sws, sb, stream);
+  fcgno_problem_destroy(p);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(u_host, u, BN * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(iters_host, it, g.batch * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(status_host, st, g.batch * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  if (history_host)
+    CK(cudaMemcpyAsync(history_host, hist, (size_t)g.batch * (o.maxit + 1) * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return FCGNO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// common.cuh — device primitives shared by the FCG-NO kernels (sm_100a).
+//
+//  * double-double arithmetic built from error-free transformations (TwoSum, TwoProduct via
+//    fma), used to make every inner product the correctly rounded value of the exact sum in
+//    all but astronomically rare ties (reading R6);
+//  * deterministic block reductions and the "last CTA of a system reduces the partials"
+//    protocol, so no scalar-only kernel launch is needed per reduction;
+//  * the canonical fp64 stencil op order (R1-R5) written with explicit _rn
+//    intrinsics so that nvcc cannot contract it into fma.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace fcgno {
+
+constexpr int kThreads = 256;          // block size of the element-wise / stencil kernels
+constexpr int kPerThread = 4;          // elements per thread
+constexpr int kTile = kThreads * kPerThread;  // elements of one system per CTA
+constexpr int kModes = 20;             // K
+constexpr int kModes2 = kModes * kModes;
+constexpr int kMmax = 64;              // FCGNO_MMAX
+constexpr int kDotChunk = 8;           // window dots reduced together
+
+enum : int { SYS_RUNNING = 0, SYS_CONVERGED = 1, SYS_MAXIT = 2, SYS_BREAKDOWN = 3, SYS_NONFINITE = 4 };
+enum : int { FLAG_NONFINITE = 1, FLAG_BREAKDOWN = 2 };
+
+// ------------------------------------------------------------------ double-double
+struct __align__(16) dd { double hi, lo; };
+
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+__device__ __forceinline__ void fast_two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  e = __dsub_rn(b, __dsub_rn(s, a));
+}
+// Accurate double-double addition (relative error <= 3u^2); commutative bit for bit.
+__device__ __forceinline__ dd dd_add(dd x, dd y) {
+  double sh, sl, th, tl;
+  two_sum(x.hi, y.hi, sh, sl);
+  two_sum(x.lo, y.lo, th, tl);
+  sl = __dadd_rn(sl, th);
+  fast_two_sum(sh, sl, sh, sl);
+  sl = __dadd_rn(sl, tl);
+  fast_two_sum(sh, sl, sh, sl);
+  return {sh, sl};
+}
+// Dot2 (Ogita-Rump-Oishi) accumulation of one exact product a*b into (s, c).
+__device__ __forceinline__ void dot2_acc(double a, double b, double& s, double& c) {
+  double p = __dmul_rn(a, b);
+  double e = __fma_rn(a, b, -p);
+  double q;
+  two_sum(s, p, s, q);
+  c = __dadd_rn(c, __dadd_rn(q, e));
+}
+__device__ __forceinline__ dd dot2_finish(double s, double c) {
+  dd r;
+  fast_two_sum(s, c, r.hi, r.lo);
+  return r;
+}
+__device__ __forceinline__ double dd_round(dd x) { return __dadd_rn(x.hi, x.lo); }
+
+__device__ __forceinline__ dd shfl_down_dd(dd x, int off) {
+  return {__shfl_down_sync(0xffffffffu, x.hi, off), __shfl_down_sync(0xffffffffu, x.lo, off)};
+}
+
+// Block-reduce NV double-doubles; result valid in thread 0.  `sm` holds >= 8*NV dd.
+template <int NV>
+__device__ __forceinline__ void block_reduce_dd(dd (&v)[NV], dd* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = dd_add(v[q], shfl_down_dd(v[q], off));
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int q = 0; q < NV; ++q) sm[warp * NV + q] = v[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int nw = blockDim.x >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      dd acc = sm[q];
+      for (int w = 1; w < nw; ++w) acc = dd_add(acc, sm[w * NV + q]);
+      v[q] = acc;
+    }
+  }
+}
+
+// Deterministic reduction of `count` dd partials (stride `stride` in dd units) by the whole
+// block; result returned to every thread.  Order depends only on count and blockDim.
+__device__ __forceinline__ dd block_reduce_partials(const dd* part, int count, int stride, dd* sm) {
+  dd acc = {0.0, 0.0};
+  for (int t = threadIdx.x; t < count; t += blockDim.x) {
+    const double2 pv = __ldcg(reinterpret_cast<const double2*>(part + (size_t)t * stride));
+    acc = dd_add(acc, dd{pv.x, pv.y});
+  }
+  dd v[1] = {acc};
+  block_reduce_dd<1>(v, sm);
+  __shared__ dd bcast;
+  if (threadIdx.x == 0) bcast = v[0];
+  __syncthreads();
+  dd out = bcast;
+  __syncthreads();
+  return out;
+}
+
+// Last-CTA protocol: called by every thread after thread 0 wrote this CTA's partials.
+// Returns true in exactly one CTA per system (the last to arrive); that CTA re-arms the counter.
+__device__ __forceinline__ bool arrive_last(unsigned* counter, int nblk) {
+  __shared__ int last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(counter, 1u);
+    last = (prev == (unsigned)(nblk - 1));
+    if (last) *counter = 0u;  // every CTA of this round has arrived; safe to re-arm
+  }
+  __syncthreads();
+  if (last) __threadfence();
+  return last != 0;
+}
+
+// ------------------------------------------------------------------ schedule
+__device__ __forceinline__ int m_schedule(int i, int m, int schedule) {
+  if (schedule == 1) return i < m ? i : m;               // sliding
+  int mod = i % (m + 1);
+  int t = mod > 1 ? mod : 1;
+  return i < t ? i : t;
+}
+
+// ------------------------------------------------------------------ stencil (fp64, canonical order)
+__device__ __forceinline__ double harmonic(double a, double b) {
+  return __ddiv_rn(2.0 * __dmul_rn(a, b), __dadd_rn(a, b));
+}
+
+// y(i,j) of one system; k and x point at the system's [n][n] arrays.
+__device__ __forceinline__ double stencil_at(const double* __restrict__ k, const double* __restrict__ x,
+                                             int n, int i, int j, double scale) {
+  const int e = i * n + j;
+  const double kc = __ldg(k + e);
+  const double xc = x[e];
+  double kW = kc, kE = kc, kS = kc, kN = kc, xW = 0.0, xE = 0.0, xS = 0.0, xN = 0.0;
+  if (j > 0)     { kW = harmonic(kc, __ldg(k + e - 1)); xW = x[e - 1]; }
+  if (j < n - 1) { kE = harmonic(kc, __ldg(k + e + 1)); xE = x[e + 1]; }
+  if (i > 0)     { kS = harmonic(kc, __ldg(k + e - n)); xS = x[e - n]; }
+  if (i < n - 1) { kN = harmonic(kc, __ldg(k + e + n)); xN = x[e + n]; }
+  const double d = __dadd_rn(__dadd_rn(kW, kE), __dadd_rn(kS, kN));
+  double t = __dmul_rn(d, xc);
+  t = __dsub_rn(t, __dmul_rn(kW, xW));
+  t = __dsub_rn(t, __dmul_rn(kE, xE));
+  t = __dsub_rn(t, __dmul_rn(kS, xS));
+  t = __dsub_rn(t, __dmul_rn(kN, xN));
+  return __dmul_rn(t, scale);
+}
+
+}  // namespace fcgno

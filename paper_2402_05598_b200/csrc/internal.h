@@ -1,0 +1,106 @@
+// internal.h — host/device structures shared by the kernels and the C-ABI layer.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace fcgno {
+
+// State of one batched FCG solve (all device pointers).  Passed by value to every kernel.
+struct FcgDev {
+  int n, B, N, nblk;          // grid, batch, n*n, CTAs per system (ceil(N / kTile))
+  int m, maxit, schedule;
+  double tol, scale;          // scale = (n+1)^2
+  const double* k;            // [B][N]
+  const double* f;            // [B][N]
+  double* u;                  // [B][N]  caller's iterate
+  double* r;                  // [B][N]  residual
+  const double* w;            // [B][N]  preconditioned residual (== r for identity)
+  double* ring_p;             // [m+1][B][N]
+  double* ring_s;             // [m+1][B][N]
+  double* gamma;              // [m+1][B]   (p_k, s_k)
+  double* beta;               // [B][kMmax]
+  double* alpha;              // [B]
+  double* rr;                 // [B]        (r_i, r_i)
+  double* rho0;               // [B]
+  dd* part_win;               // [B][nblk][kMmax]
+  dd* part_step;              // [B][nblk][2]
+  dd* part_rr;                // [B][nblk]
+  unsigned* cnt;              // [3][B] last-CTA counters
+  int* flags;                 // [B]
+  int* status;                // [B] caller
+  int* iters;                 // [B] caller
+  double* hist;               // [B][maxit+1] caller or nullptr
+  int* iter;                  // global iteration counter
+  int* active;                // systems still running after the last finalize
+};
+
+// Packed NO weights (element offsets into the packed array of T; complex = 2 T).
+struct NoLayout {
+  int w;
+  size_t W1E, b1, A0, A1, A2;          // layer 1 with the lift folded in
+  size_t W[2], b[2], R[2];             // layers 2 and 3: W [o][c], b [o], R [kappa][c][o] complex
+  size_t Q, dw, cst;                   // layer 4 folded with the projection
+  size_t total;                        // elements of T
+};
+NoLayout no_layout(int w);
+
+// Device view of the NO for one launch sequence.
+template <typename T>
+struct NoDev {
+  int n, B, N, w;
+  int use_gelu;
+  const double* k;            // [B][N] nodal k (fp64, the problem's)
+  const T* pk;                // packed weights
+  NoLayout L;
+  const T* F;                 // twiddles [n][kModes] complex: exp(-2 pi i kappa j / n)
+  const T* khat;              // [B][400] complex DFT_M(k)
+  T* rpart;                   // [B][ngroups][400] complex partial DFT_M(r/s)
+  int ngroups;                // row groups of the input DFT
+  T* v0;                      // [B][w][N]
+  T* v1;                      // [B][w][N]
+  T* chat;                    // [400][B][w] complex
+  T* ghat;                    // [B][w][400] complex
+};
+
+// In-graph profiling hook: begin/end record CUDA events around launches of a kernel class.
+enum ProfClass : int { PROF_NO_LAYER = 0, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM,
+                       PROF_STENCIL, PROF_UPDATE, PROF_FINALIZE, PROF_NCLASS };
+struct ProfHook {
+  virtual ~ProfHook() = default;
+  virtual void begin(int cls, cudaStream_t s) = 0;
+  virtual void end(int cls, cudaStream_t s) = 0;
+};
+
+// Launch helpers (defined in fcg_kernels.cu / no_kernels.cu).  All return cudaGetLastError().
+cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, cudaStream_t s);
+cudaError_t launch_dot(const double* x, const double* y, double* out, dd* part, unsigned* cnt, int n, int B,
+                       cudaStream_t s);
+cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t s);
+cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_pform(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_stencil_dots(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_update(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_finalize(const FcgDev& d, cudaStream_t s);
+
+cudaError_t launch_twiddles(float* F32, double* F64, int n, cudaStream_t s);
+template <typename T>
+cudaError_t launch_khat(const double* k, const T* F, T* part, T* khat, int n, int B, int ngroups,
+                        cudaStream_t s);
+// NO forward; when fcg != nullptr the output kernel also computes the FCG window dots and
+// freezes converged systems; otherwise w = NO(r) standalone (rr must hold (r,r)).
+template <typename T>
+cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double* rr, double* w,
+                              const FcgDev* fcg, const int* status, cudaStream_t s, int* nlaunch,
+                              ProfHook* prof = nullptr);
+template <typename T>
+cudaError_t prepare_no_kernels();
+template <typename T>
+size_t no_max_smem(int n, int w);   // largest dynamic smem any NO kernel needs for (n, w)
+
+uint64_t& launch_counter();
+
+}  // namespace fcgno

@@ -1,0 +1,560 @@
+// no_kernels.cu — spectral neural operator forward (§2.4.2, App. A).
+//
+// Per layer: analysis c = DFT_M(v) (M = {-10..9}^2), mode-diagonal complex channel mixing
+// g[o](kappa) = sum_c R[c][o](kappa) c[c](kappa), synthesis z = n^-2 Re iDFT_M(g), bypass W v + b,
+// GELU (R7-R11).  Kernel split:
+//   k_dft_rows    DFT_M of r/||r|| (row-group partials)
+//   k_lift_mix    layer-1 mixing with the lift folded in: g1 = A0 R^ + A1 K^ + n^2 delta A2
+//   k_no_layer    one CTA per (system, group of GO output channels) streams the system's rows:
+//                 y-synthesis of g for the rows -> bypass GEMV + x-synthesis + bias + GELU ->
+//                 store v -> x-analysis -> y-analysis accumulated in registers -> c[kappa][b][o]
+//   k_mix         mode-diagonal mixing for layers 2, 3 and (folded with the projection) 4
+//   k_no_out      out = dw.v3 + cst + S(g4), w = ||r|| out, fused FCG window dots (w, s_k)
+// Templated on T = float (production) or double (trajectory-parity mode).
+#include <cstdio>
+
+#include "internal.h"
+#include "fcg_device.cuh"
+
+namespace fcgno {
+
+template <typename T> struct Cplx;
+template <> struct Cplx<float> { using type = float2; };
+template <> struct Cplx<double> { using type = double2; };
+
+__device__ __forceinline__ float gelu_t(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ double gelu_t(double x) { return 0.5 * x * (1.0 + erf(x * 0.70710678118654752440)); }
+
+constexpr int kDftRows = 8;      // rows per CTA of k_dft_rows
+constexpr int kGhStride = kModes2 + 1;  // padded row of the per-channel mode array in smem
+constexpr int kMixBatch = 16;    // systems per CTA of k_mix
+constexpr int kMaxDynSmem = 227 * 1024;
+
+// ------------------------------------------------------------------ twiddles
+__global__ void k_twiddles(float2* F32, double2* F64, int n) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n * kModes) return;
+  const int j = t / kModes, kx = t - j * kModes;
+  const long long kap = kx - kModes / 2;
+  const long long q = ((kap * j) % n + n) % n;       // exact phase reduction
+  double sn, cs;
+  sincospi(2.0 * (double)q / (double)n, &sn, &cs);
+  F64[t] = make_double2(cs, -sn);                    // exp(-2 pi i kappa j / n)
+  F32[t] = make_float2((float)cs, (float)-sn);
+}
+
+cudaError_t launch_twiddles(float* F32, double* F64, int n, cudaStream_t s) {
+  const int cnt = n * kModes;
+  k_twiddles<<<(cnt + 255) / 256, 256, 0, s>>>(reinterpret_cast<float2*>(F32), reinterpret_cast<double2*>(F64), n);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ DFT_M of an input field
+// grid (ngroups, B).  x is fp64; for FROM_R the field is x * (1/||x||) with ||x|| = sqrt(rr[b]).
+template <typename T, bool FROM_R>
+__global__ void __launch_bounds__(256) k_dft_rows(const double* __restrict__ x, const double* __restrict__ rr,
+                                                  const typename Cplx<T>::type* __restrict__ F,
+                                                  typename Cplx<T>::type* __restrict__ part, int n, int ngroups,
+                                                  const int* __restrict__ status) {
+  using T2 = typename Cplx<T>::type;
+  const int b = blockIdx.y, g = blockIdx.x;
+  if (status && status[b] != SYS_RUNNING) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* X = reinterpret_cast<T*>(smraw);                               // [kDftRows][n]
+  T2* Tx = reinterpret_cast<T2*>(X + ((kDftRows * n + 3) & ~3));    // [kDftRows][20]
+  const int N = n * n, i0 = g * kDftRows, rows = min(kDftRows, n - i0);
+  double inv = 1.0;
+  if (FROM_R) {
+    const double s = sqrt(rr[b]);
+    inv = s > 0.0 ? 1.0 / s : 0.0;
+  }
+  const double* xb = x + (size_t)b * N + (size_t)i0 * n;
+  for (int t = threadIdx.x; t < rows * n; t += blockDim.x) X[t] = (T)(xb[t] * inv);
+  __syncthreads();
+  for (int e = threadIdx.x; e < rows * kModes; e += blockDim.x) {
+    const int r = e / kModes, k2 = e - r * kModes;
+    T ar = 0, ai = 0;
+    for (int j = 0; j < n; ++j) {
+      const T v = X[r * n + j];
+      const T2 f = __ldg(F + j * kModes + k2);
+      ar += v * f.x; ai += v * f.y;
+    }
+    Tx[e] = T2{ar, ai};
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
+    const int k1 = e / kModes, k2 = e - k1 * kModes;
+    T ar = 0, ai = 0;
+    for (int r = 0; r < rows; ++r) {
+      const T2 f = __ldg(F + (i0 + r) * kModes + k1);
+      const T2 t = Tx[r * kModes + k2];
+      ar += f.x * t.x - f.y * t.y;
+      ai += f.x * t.y + f.y * t.x;
+    }
+    part[((size_t)b * ngroups + g) * kModes2 + e] = T2{ar, ai};
+  }
+}
+
+template <typename T>
+__global__ void k_reduce_groups(const typename Cplx<T>::type* __restrict__ part, typename Cplx<T>::type* __restrict__ out,
+                                int ngroups) {
+  using T2 = typename Cplx<T>::type;
+  const int b = blockIdx.x;
+  for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
+    T ar = 0, ai = 0;
+    for (int g = 0; g < ngroups; ++g) {
+      const T2 v = part[((size_t)b * ngroups + g) * kModes2 + e];
+      ar += v.x; ai += v.y;
+    }
+    out[(size_t)b * kModes2 + e] = T2{ar, ai};
+  }
+}
+
+static size_t dft_smem(int n, size_t tsz) { return ((size_t)((kDftRows * n + 3) & ~3)) * tsz + kDftRows * kModes * 2 * tsz; }
+
+template <typename T>
+cudaError_t launch_khat(const double* k, const T* F, T* part, T* khat, int n, int B, int ngroups, cudaStream_t s) {
+  using T2 = typename Cplx<T>::type;
+  k_dft_rows<T, false><<<dim3(ngroups, B), 256, dft_smem(n, sizeof(T)), s>>>(
+      k, nullptr, reinterpret_cast<const T2*>(F), reinterpret_cast<T2*>(part), n, ngroups, nullptr);
+  k_reduce_groups<T><<<B, 256, 0, s>>>(reinterpret_cast<const T2*>(part), reinterpret_cast<T2*>(khat), ngroups);
+  launch_counter() += 2;
+  return cudaGetLastError();
+}
+template cudaError_t launch_khat<float>(const double*, const float*, float*, float*, int, int, int, cudaStream_t);
+template cudaError_t launch_khat<double>(const double*, const double*, double*, double*, int, int, int, cudaStream_t);
+
+// ------------------------------------------------------------------ layer-1 mixing with the lift folded in
+template <typename T>
+__global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* __restrict__ rpart, int ngroups,
+                                                  const typename Cplx<T>::type* __restrict__ khat,
+                                                  const typename Cplx<T>::type* __restrict__ A0,
+                                                  const typename Cplx<T>::type* __restrict__ A1,
+                                                  const typename Cplx<T>::type* __restrict__ A2,
+                                                  typename Cplx<T>::type* __restrict__ ghat, int w, T n2, T inv_n2,
+                                                  const int* __restrict__ status) {
+  using T2 = typename Cplx<T>::type;
+  const int b = blockIdx.x;
+  if (status && status[b] != SYS_RUNNING) return;
+  __shared__ T2 Rh[kModes2];
+  for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
+    T ar = 0, ai = 0;
+    for (int g = 0; g < ngroups; ++g) {
+      const T2 v = rpart[((size_t)b * ngroups + g) * kModes2 + e];
+      ar += v.x; ai += v.y;
+    }
+    Rh[e] = T2{ar, ai};
+  }
+  __syncthreads();
+  const int k0 = (kModes / 2) * kModes + kModes / 2;   // kappa = (0, 0)
+  for (int e = threadIdx.x; e < w * kModes2; e += blockDim.x) {
+    const int o = e / kModes2, kk = e - o * kModes2;
+    const T2 a0 = A0[(size_t)kk * w + o], a1 = A1[(size_t)kk * w + o];
+    const T2 rh = Rh[kk], kh = khat[(size_t)b * kModes2 + kk];
+    T gr = a0.x * rh.x - a0.y * rh.y + a1.x * kh.x - a1.y * kh.y;
+    T gi = a0.x * rh.y + a0.y * rh.x + a1.x * kh.y + a1.y * kh.x;
+    if (kk == k0) { gr += n2 * A2[o].x; gi += n2 * A2[o].y; }
+    ghat[((size_t)b * w + o) * kModes2 + kk] = T2{gr * inv_n2, gi * inv_n2};
+  }
+}
+
+// ------------------------------------------------------------------ mode-diagonal mixing
+// grid (400, ceil(B / kMixBatch)).  chat [400][B][cin], R [400][cin][cout], ghat [B][cout][400].
+template <typename T>
+__global__ void __launch_bounds__(256) k_mix(const typename Cplx<T>::type* __restrict__ chat,
+                                             const typename Cplx<T>::type* __restrict__ R,
+                                             typename Cplx<T>::type* __restrict__ ghat, int B, int cin, int cout,
+                                             T inv_n2, const int* __restrict__ status) {
+  using T2 = typename Cplx<T>::type;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T2* Rs = reinterpret_cast<T2*>(smraw);             // [cin][cout]
+  T2* Cs = Rs + (size_t)cin * cout;                  // [kMixBatch][cin]
+  const int kk = blockIdx.x, b0 = blockIdx.y * kMixBatch, nb = min(kMixBatch, B - b0);
+  const T2* Rk = R + (size_t)kk * cin * cout;
+  for (int t = threadIdx.x; t < cin * cout; t += blockDim.x) Rs[t] = Rk[t];
+  const T2* Ck = chat + ((size_t)kk * B + b0) * cin;
+  for (int t = threadIdx.x; t < nb * cin; t += blockDim.x) Cs[t] = Ck[t];
+  __syncthreads();
+  for (int e = threadIdx.x; e < nb * cout; e += blockDim.x) {
+    const int bb = e / cout, o = e - bb * cout;
+    if (status && status[b0 + bb] != SYS_RUNNING) continue;
+    T ar = 0, ai = 0;
+    for (int c = 0; c < cin; ++c) {
+      const T2 rv = Rs[c * cout + o], cv = Cs[bb * cin + c];
+      ar += rv.x * cv.x - rv.y * cv.y;
+      ai += rv.x * cv.y + rv.y * cv.x;
+    }
+    ghat[((size_t)(b0 + bb) * cout + o) * kModes2 + kk] = T2{ar * inv_n2, ai * inv_n2};
+  }
+}
+
+// ------------------------------------------------------------------ operator layer (layers 1-3)
+template <typename T>
+struct LayerArgs {
+  int n, N, w, cin, B, rows, use_gelu;
+  const double* r; const double* rr; const double* k;   // FIRST layer inputs
+  const T* vin;                                          // [B][cin][N] (layers 2, 3)
+  const T* W;                                            // [w][cin]
+  const T* bias;                                         // [w]
+  const typename Cplx<T>::type* ghat;                    // [B][w][400], scaled by n^-2
+  const typename Cplx<T>::type* F;                       // [n][20]
+  T* vout;                                               // [B][w][N]
+  typename Cplx<T>::type* chat;                          // [400][B][w]
+  const int* status;
+};
+
+template <typename T, int GO>
+struct LayerSmem {
+  // element offsets (in T) of each region; complex regions are 2 T per entry
+  size_t Wsm, bsm, gh, Vin, Vout, Gs, Tx, total;
+  __host__ __device__ LayerSmem(int n, int cin, int rows) {
+    const int CH = rows * n;
+    size_t o = 0;
+    auto al = [](size_t x) { return (x + 3) & ~size_t(3); };
+    Wsm = o; o = al(o + (size_t)cin * GO);
+    bsm = o; o = al(o + GO);
+    gh = o; o = al(o + (size_t)2 * GO * kGhStride);
+    Vin = o; o = al(o + (size_t)cin * CH);
+    Vout = o; o = al(o + (size_t)GO * CH);
+    Gs = o; o = al(o + (size_t)2 * rows * kModes * GO);
+    Tx = o; o = al(o + (size_t)2 * GO * (rows * kModes + 1));
+    total = o;
+  }
+};
+
+template <typename T> constexpr int layer_go() { return sizeof(T) == 4 ? 8 : 4; }
+
+template <typename T, bool FIRST, int GO>
+__global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
+  using T2 = typename Cplx<T>::type;
+  constexpr int NACC = (GO * kModes2 + 255) / 256;
+  const int b = blockIdx.y, og = blockIdx.x * GO;
+  if (a.status && a.status[b] != SYS_RUNNING) return;
+  const int n = a.n, N = a.N, cin = a.cin, w = a.w, RC = a.rows;
+  const int go = min(GO, w - og);
+  const LayerSmem<T, GO> L(n, cin, RC);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T* sm = reinterpret_cast<T*>(smraw);
+  T* Wsm = sm + L.Wsm;           // [cin][GO]
+  T* bsm = sm + L.bsm;           // [GO]
+  T2* gh = reinterpret_cast<T2*>(sm + L.gh);      // [GO][kGhStride]
+  T* Vin = sm + L.Vin;           // [cin][CH]
+  T* Vout = sm + L.Vout;         // [GO][CH]
+  T2* Gs = reinterpret_cast<T2*>(sm + L.Gs);      // [RC][20][GO]
+  T2* Tx = reinterpret_cast<T2*>(sm + L.Tx);      // [GO][RC*20+1]
+  const int TXS = RC * kModes + 1;
+
+  for (int t = threadIdx.x; t < cin * GO; t += blockDim.x) {
+    const int c = t / GO, o = t - c * GO;
+    Wsm[t] = o < go ? a.W[(size_t)(og + o) * cin + c] : T(0);
+  }
+  for (int o = threadIdx.x; o < GO; o += blockDim.x) bsm[o] = o < go ? a.bias[og + o] : T(0);
+  for (int t = threadIdx.x; t < GO * kModes2; t += blockDim.x) {
+    const int o = t / kModes2, kk = t - o * kModes2;
+    gh[o * kGhStride + kk] = o < go ? a.ghat[((size_t)b * w + og + o) * kModes2 + kk] : T2{T(0), T(0)};
+  }
+  double inv_s = 1.0;
+  if (FIRST) {
+    const double s = sqrt(a.rr[b]);
+    inv_s = s > 0.0 ? 1.0 / s : 0.0;
+  }
+  T accr[NACC], acci[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) { accr[q] = 0; acci[q] = 0; }
+  __syncthreads();
+
+  for (int i0 = 0; i0 < n; i0 += RC) {
+    const int rows = min(RC, n - i0), npix = rows * n;
+    const size_t base = (size_t)i0 * n;
+    // 1. stage the input rows of every input channel
+    if (FIRST) {
+      const double* rb = a.r + (size_t)b * N + base;
+      const double* kb = a.k + (size_t)b * N + base;
+      for (int t = threadIdx.x; t < npix; t += blockDim.x) {
+        Vin[t] = (T)(rb[t] * inv_s);
+        Vin[npix + t] = (T)kb[t];
+      }
+    } else {
+      for (int t = threadIdx.x; t < cin * npix; t += blockDim.x) {
+        const int c = t / npix, p = t - c * npix;
+        Vin[c * npix + p] = a.vin[((size_t)b * cin + c) * N + base + p];
+      }
+    }
+    // 2. y-synthesis of this layer's spectral term for the rows: Gs[r][k2][o]
+    for (int e = threadIdx.x; e < rows * kModes * GO; e += blockDim.x) {
+      const int o = e % GO, rk = e / GO, r = rk / kModes, k2 = rk - r * kModes;
+      T gr = 0, gi = 0;
+      const T2* F1 = a.F + (size_t)(i0 + r) * kModes;
+#pragma unroll 4
+      for (int k1 = 0; k1 < kModes; ++k1) {
+        const T2 g = gh[o * kGhStride + k1 * kModes + k2];
+        const T2 f = __ldg(F1 + k1);                 // conj(f) = exp(+2 pi i kappa1 i / n)
+        gr += g.x * f.x + g.y * f.y;
+        gi += g.y * f.x - g.x * f.y;
+      }
+      Gs[(r * kModes + k2) * GO + o] = T2{gr, gi};
+    }
+    __syncthreads();
+    // 3. bypass + x-synthesis + bias + GELU for every pixel of the rows
+    for (int p = threadIdx.x; p < npix; p += blockDim.x) {
+      const int r = p / n, j = p - r * n;
+      T acc[GO];
+#pragma unroll
+      for (int o = 0; o < GO; ++o) acc[o] = bsm[o];
+      for (int c = 0; c < cin; ++c) {
+        const T x = Vin[c * npix + p];
+#pragma unroll
+        for (int o = 0; o < GO; ++o) acc[o] += Wsm[c * GO + o] * x;
+      }
+      const T2* Fj = a.F + (size_t)j * kModes;
+      const T2* Gr = Gs + (size_t)r * kModes * GO;
+#pragma unroll 2
+      for (int k2 = 0; k2 < kModes; ++k2) {
+        const T2 f = __ldg(Fj + k2);                 // Re(G exp(+i th)) = G.x f.x + G.y f.y
+#pragma unroll
+        for (int o = 0; o < GO; ++o) {
+          const T2 g = Gr[k2 * GO + o];
+          acc[o] += g.x * f.x + g.y * f.y;
+        }
+      }
+#pragma unroll
+      for (int o = 0; o < GO; ++o) {
+        const T v = a.use_gelu ? gelu_t(acc[o]) : acc[o];
+        Vout[o * npix + p] = v;
+        if (o < go) a.vout[((size_t)b * w + og + o) * N + base + p] = v;
+      }
+    }
+    __syncthreads();
+    // 4. x-analysis of the new activations: Tx[o][r][k2]
+    for (int e = threadIdx.x; e < GO * rows * kModes; e += blockDim.x) {
+      const int k2 = e % kModes, orr = e / kModes, r = orr % rows, o = orr / rows;
+      const T* vrow = Vout + (size_t)o * npix + (size_t)r * n;
+      T tr = 0, ti = 0;
+      for (int j = 0; j < n; ++j) {
+        const T2 f = __ldg(a.F + (size_t)j * kModes + k2);
+        const T v = vrow[j];
+        tr += v * f.x; ti += v * f.y;
+      }
+      Tx[o * TXS + r * kModes + k2] = T2{tr, ti};
+    }
+    __syncthreads();
+    // 5. y-analysis accumulated over the rows in registers: acc(kappa, o)
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) {
+      const int e = threadIdx.x + q * 256;
+      if (e < GO * kModes2) {
+        const int o = e % GO, kk = e / GO, k1 = kk / kModes, k2 = kk - k1 * kModes;
+        for (int r = 0; r < rows; ++r) {
+          const T2 f = __ldg(a.F + (size_t)(i0 + r) * kModes + k1);
+          const T2 t = Tx[o * TXS + r * kModes + k2];
+          accr[q] += f.x * t.x - f.y * t.y;
+          acci[q] += f.x * t.y + f.y * t.x;
+        }
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) {
+    const int e = threadIdx.x + q * 256;
+    if (e < GO * kModes2) {
+      const int o = e % GO, kk = e / GO;
+      if (o < go) a.chat[((size_t)kk * a.B + b) * w + og + o] = T2{accr[q], acci[q]};
+    }
+  }
+}
+
+
+
+// ------------------------------------------------------------------ layer 4 + projection + FCG window dots
+template <typename T>
+struct OutArgs {
+  int n, N, w, use_dots;
+  const T* vin;                                   // [B][w][N]
+  const T* dw;                                    // [w]
+  const T* cst;                                   // [1]
+  const typename Cplx<T>::type* gh4;              // [B][400] scaled by n^-2
+  const typename Cplx<T>::type* F;
+  const double* rr;
+  double* wout;                                   // [B][N]
+  const int* status;
+};
+
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const FcgDev d) {
+  using T2 = typename Cplx<T>::type;
+  const int b = blockIdx.y, blk = blockIdx.x;
+  if (a.status && a.status[b] != SYS_RUNNING) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  T2* gh = reinterpret_cast<T2*>(smraw);          // [400]
+  T2* Gs = gh + kModes2;                          // [nr][20]
+  const int n = a.n, N = a.N, w = a.w;
+  const int e0 = blk * kTile;
+  const int rlo = e0 / n, rhi = min(n - 1, (e0 + kTile - 1) / n), nr = rhi - rlo + 1;
+  T* dws = reinterpret_cast<T*>(Gs + (size_t)nr * kModes);   // [w]
+  for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)b * kModes2 + t];
+  for (int t = threadIdx.x; t < w; t += blockDim.x) dws[t] = a.dw[t];
+  __syncthreads();
+  for (int e = threadIdx.x; e < nr * kModes; e += blockDim.x) {
+    const int r = e / kModes, k2 = e - r * kModes;
+    T gr = 0, gi = 0;
+    for (int k1 = 0; k1 < kModes; ++k1) {
+      const T2 g = gh[k1 * kModes + k2];
+      const T2 f = __ldg(a.F + (size_t)(rlo + r) * kModes + k1);
+      gr += g.x * f.x + g.y * f.y;
+      gi += g.y * f.x - g.x * f.y;
+    }
+    Gs[e] = T2{gr, gi};
+  }
+  __syncthreads();
+  const double s = sqrt(a.rr[b]);
+  const T cst = a.cst[0];
+  double wv[kPerThread];
+#pragma unroll
+  for (int q = 0; q < kPerThread; ++q) {
+    const int e = e0 + q * kThreads + threadIdx.x;
+    wv[q] = 0.0;
+    if (e < N) {
+      const int i = e / n, j = e - i * n;
+      T acc = cst;
+      const T* vb = a.vin + (size_t)b * w * N + e;
+      for (int c = 0; c < w; ++c) acc += dws[c] * vb[(size_t)c * N];
+      const T2* Gr = Gs + (size_t)(i - rlo) * kModes;
+      for (int k2 = 0; k2 < kModes; ++k2) {
+        const T2 f = __ldg(a.F + (size_t)j * kModes + k2);
+        acc += Gr[k2].x * f.x + Gr[k2].y * f.y;
+      }
+      wv[q] = s * (double)acc;
+      a.wout[(size_t)b * N + e] = wv[q];
+    }
+  }
+  if (a.use_dots) {
+    const int i = *d.iter;
+    const int mi = m_schedule(i, d.m, d.schedule);
+    if (mi > 0) window_dots_beta(d, b, blk, i, mi, wv);
+  }
+}
+
+// ------------------------------------------------------------------ launcher
+static cudaError_t set_smem(const void* fn) {
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+}
+
+// Raise the dynamic shared-memory limit of every NO kernel once (never during graph capture).
+template <typename T>
+cudaError_t prepare_no_kernels() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  constexpr int GO = layer_go<T>();
+  cudaError_t e;
+  if ((e = set_smem((const void*)k_no_layer<T, true, GO>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_no_layer<T, false, GO>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_mix<T>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_no_out<T>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_dft_rows<T, true>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_dft_rows<T, false>)) != cudaSuccess) return e;
+  done = true;
+  return cudaSuccess;
+}
+template cudaError_t prepare_no_kernels<float>();
+template cudaError_t prepare_no_kernels<double>();
+
+template <typename T>
+size_t no_max_smem(int n, int w) {
+  constexpr int GO = layer_go<T>();
+  const int rows = n >= 256 ? 1 : 256 / n;
+  size_t m = LayerSmem<T, GO>(n, w, rows).total * sizeof(T);
+  const size_t msmem = ((size_t)w * w + (size_t)kMixBatch * w) * 2 * sizeof(T);
+  return m > msmem ? m : msmem;
+}
+template size_t no_max_smem<float>(int, int);
+template size_t no_max_smem<double>(int, int);
+
+template <typename T>
+cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double* rr, double* wout,
+                              const FcgDev* fcg, const int* status, cudaStream_t s, int* nlaunch, ProfHook* prof) {
+  auto pb = [&](int c) { if (prof) prof->begin(c, s); };
+  auto pe = [&](int c) { if (prof) prof->end(c, s); };
+  using T2 = typename Cplx<T>::type;
+  constexpr int GO = layer_go<T>();
+  const int n = no.n, B = no.B, w = no.w, N = n * n;
+  const T n2 = (T)((double)n * n), inv_n2 = (T)(1.0 / ((double)n * n));
+  const T* pk = no.pk;
+  const T2* F = reinterpret_cast<const T2*>(no.F);
+  T2* ghat = reinterpret_cast<T2*>(no.ghat);
+  T2* chat = reinterpret_cast<T2*>(no.chat);
+  int launches = 0;
+
+  // 1. DFT_M of r/||r|| (row-group partials)
+  pb(PROF_NO_INPUT);
+  k_dft_rows<T, true><<<dim3(no.ngroups, B), 256, dft_smem(n, sizeof(T)), s>>>(
+      r, rr, F, reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status);
+  ++launches;
+  // 2. layer-1 mixing with the lift folded in
+  k_lift_mix<T><<<B, 256, 0, s>>>(reinterpret_cast<const T2*>(no.rpart), no.ngroups,
+                                  reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
+                                  reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2),
+                                  ghat, w, n2, inv_n2, status);
+  pe(PROF_NO_INPUT);
+  ++launches;
+  // 3. layers 1..3, each followed by the mixing of the next layer
+  const int rows = n >= 256 ? 1 : 256 / n;
+  const dim3 lgrid((w + GO - 1) / GO, B);
+  T* vbuf[2] = {no.v0, no.v1};
+  for (int l = 0; l < 3; ++l) {
+    LayerArgs<T> la{};
+    la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.use_gelu = no.use_gelu;
+    la.r = r; la.rr = rr; la.k = no.k;
+    la.ghat = ghat; la.F = F; la.chat = chat; la.status = status;
+    la.vout = vbuf[l & 1];
+    if (l == 0) {
+      la.cin = 2; la.W = pk + no.L.W1E; la.bias = pk + no.L.b1; la.vin = nullptr;
+    } else {
+      la.cin = w; la.W = pk + no.L.W[l - 1]; la.bias = pk + no.L.b[l - 1]; la.vin = vbuf[(l - 1) & 1];
+    }
+    const size_t smem = LayerSmem<T, GO>(n, la.cin, rows).total * sizeof(T);
+    pb(PROF_NO_LAYER);
+    if (l == 0) {
+      k_no_layer<T, true, GO><<<lgrid, 256, smem, s>>>(la);
+    } else {
+      k_no_layer<T, false, GO><<<lgrid, 256, smem, s>>>(la);
+    }
+    pe(PROF_NO_LAYER);
+    ++launches;
+    // mixing for the next layer (layers 2, 3) or layer 4 folded with the projection (cout = 1)
+    const int cout = (l < 2) ? w : 1;
+    const T2* Rm = reinterpret_cast<const T2*>(pk + (l < 2 ? no.L.R[l] : no.L.Q));
+    const size_t msmem = ((size_t)w * cout + (size_t)kMixBatch * w) * sizeof(T2);
+    pb(PROF_NO_MIX);
+    k_mix<T><<<dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), 256, msmem, s>>>(chat, Rm, ghat, B, w, cout, inv_n2,
+                                                                               status);
+    pe(PROF_NO_MIX);
+    ++launches;
+  }
+  // 4. layer 4 + projection (+ window dots when inside FCG)
+  OutArgs<T> oa{};
+  oa.n = n; oa.N = N; oa.w = w; oa.use_dots = fcg != nullptr;
+  oa.vin = vbuf[0];                       // layer 3 wrote vbuf[2 & 1] = vbuf[0]
+  oa.dw = pk + no.L.dw; oa.cst = pk + no.L.cst;
+  oa.gh4 = ghat; oa.F = F; oa.rr = rr; oa.wout = wout; oa.status = status;
+  const int nblk = (N + kTile - 1) / kTile;
+  const int nr_max = kTile / n + 2;
+  const size_t osmem = (size_t)(kModes2 + (size_t)nr_max * kModes) * sizeof(T2) + (size_t)w * sizeof(T);
+  FcgDev dummy{};
+  pb(PROF_NO_OUT);
+  k_no_out<T><<<dim3(nblk, B), kThreads, osmem, s>>>(oa, fcg ? *fcg : dummy);
+  pe(PROF_NO_OUT);
+  ++launches;
+  launch_counter() += launches;
+  if (nlaunch) *nlaunch = launches;
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_no_forward<float>(const NoDev<float>&, const double*, const double*, double*,
+                                              const FcgDev*, const int*, cudaStream_t, int*, ProfHook*);
+template cudaError_t launch_no_forward<double>(const NoDev<double>&, const double*, const double*, double*,
+                                               const FcgDev*, const int*, cudaStream_t, int*, ProfHook*);
+
+}  // namespace fcgno

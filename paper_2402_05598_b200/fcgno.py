@@ -1,0 +1,273 @@
+"""Thin ctypes binding of libfcgno.so (include/fcgno.h).
+
+Argument marshalling only: every step of the hot path runs in the library's CUDA kernels.
+PyTorch supplies device memory (tensors) and the current stream.  There is no CPU fallback:
+importing this module fails loudly when the shared library is missing, and every call raises
+``FcgnoError`` on a non-OK return.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfcgno.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2402_05598_b200.build` "
+                      "(or __graft_entry__.build()); there is no CPU fallback")
+_lib = ctypes.CDLL(LIB_PATH)
+
+FP32, FP64 = 0, 1
+SCHEDULE_PAPER, SCHEDULE_SLIDING = 0, 1
+RUNNING, CONVERGED, MAXIT, BREAKDOWN, NONFINITE = 0, 1, 2, 3, 4
+K_MODES = 20
+ERRORS = {1: "EINVAL", 2: "ENONPOS_K", 3: "ECUDA", 4: "EWORKSPACE", 5: "EUNSUPPORTED"}
+
+
+class FcgnoError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"fcgno {ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Grid(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("batch", ctypes.c_int32)]
+
+
+class NoDesc(ctypes.Structure):
+    _fields_ = [("width", ctypes.c_int32), ("precision", ctypes.c_int32), ("use_gelu", ctypes.c_int32)]
+
+
+class SolveOpts(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int32), ("maxit", ctypes.c_int32), ("tol", ctypes.c_double),
+                ("schedule", ctypes.c_int32), ("check_every", ctypes.c_int32),
+                ("profile_mask", ctypes.c_int32)]
+
+
+_vp, _sz, _i = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+_P = ctypes.POINTER
+EXPORTS = {
+    "fcgno_problem_workspace_bytes": (_sz, [Grid]),
+    "fcgno_assemble": (_i, [Grid, _vp, _vp, _sz, _vp, _P(_vp)]),
+    "fcgno_problem_destroy": (None, [_vp]),
+    "fcgno_apply_A": (_i, [_vp, _vp, _vp, _vp]),
+    "fcgno_dot_workspace_bytes": (_sz, [Grid]),
+    "fcgno_batched_dot": (_i, [_vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_no_packed_bytes": (_sz, [NoDesc]),
+    "fcgno_no_pack": (_i, [NoDesc, _vp, _vp, _vp]),
+    "fcgno_apply_no_workspace_bytes": (_sz, [Grid, NoDesc]),
+    "fcgno_apply_NO": (_i, [_vp, NoDesc, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_solve_workspace_bytes": (_sz, [Grid, _P(NoDesc), SolveOpts]),
+    "fcgno_fcg_solve": (_i, [_vp, _P(NoDesc), _vp, _vp, _vp, SolveOpts, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_solve_host_workspace_bytes": (_sz, [Grid, _P(NoDesc), SolveOpts]),
+    "fcgno_solve_host": (_i, [Grid, _vp, _vp, _vp, _P(NoDesc), _vp, SolveOpts, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_profile_get": (_i, [_i, _P(ctypes.c_double), _P(ctypes.c_int64)]),
+    "fcgno_profile_reset": (None, []),
+    "fcgno_profile_name": (ctypes.c_char_p, [_i]),
+    "fcgno_kernel_launches": (ctypes.c_uint64, []),
+    "fcgno_last_error": (ctypes.c_char_p, []),
+    "fcgno_abi_version": (_i, []),
+}
+for _name, (_res, _args) in EXPORTS.items():
+    _fn = getattr(_lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+def _check(code: int):
+    if code != 0:
+        raise FcgnoError(code, _lib.fcgno_last_error().decode())
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return ctypes.c_void_p(t.data_ptr())
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data_as(ctypes.c_void_p)
+    raise TypeError(type(t))
+
+
+def _stream(stream=None):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    # torch's caching allocator returns 512-byte aligned blocks
+    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def _require(t: torch.Tensor, shape, name):
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise TypeError(f"{name} must be a contiguous float64 CUDA tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+def kernel_launches() -> int:
+    return int(_lib.fcgno_kernel_launches())
+
+
+def abi_version() -> int:
+    return int(_lib.fcgno_abi_version())
+
+
+PROF_NCLASS = 9
+PROF_NO_LAYER, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM, PROF_STENCIL, PROF_UPDATE, \
+    PROF_FINALIZE = range(PROF_NCLASS)
+
+
+def profile_reset() -> None:
+    _lib.fcgno_profile_reset()
+
+
+def profile_read() -> dict:
+    """{class name: (total device ms, timed launches)} accumulated since the last reset."""
+    out = {}
+    for c in range(PROF_NCLASS):
+        ms, n = ctypes.c_double(), ctypes.c_int64()
+        _check(_lib.fcgno_profile_get(c, ctypes.byref(ms), ctypes.byref(n)))
+        out[_lib.fcgno_profile_name(c).decode()] = (ms.value, n.value)
+    return out
+
+
+class Problem:
+    """assemble(k): a batch of B independent n x n systems."""
+
+    def __init__(self, k: torch.Tensor, stream=None):
+        if k.dim() != 3 or k.shape[1] != k.shape[2]:
+            raise ValueError("k must be [B, n, n]")
+        _require(k, k.shape, "k")
+        self.B, self.n = int(k.shape[0]), int(k.shape[1])
+        self.grid = Grid(self.n, self.B)
+        self.k = k
+        self.device = k.device
+        self._ws = _workspace(_lib.fcgno_problem_workspace_bytes(self.grid), self.device)
+        h = ctypes.c_void_p()
+        _check(_lib.fcgno_assemble(self.grid, _ptr(k), _ptr(self._ws), self._ws.numel(), _stream(stream),
+                                   ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _lib.fcgno_problem_destroy(h)
+            self._h = None
+
+    @property
+    def shape(self):
+        return (self.B, self.n, self.n)
+
+    def apply_A(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        _require(x, self.shape, "x")
+        y = torch.empty_like(x) if out is None else out
+        _check(_lib.fcgno_apply_A(self._h, _ptr(x), _ptr(y), _stream(stream)))
+        return y
+
+    def dot(self, x: torch.Tensor, y: torch.Tensor, stream=None) -> torch.Tensor:
+        _require(x, self.shape, "x")
+        _require(y, self.shape, "y")
+        out = torch.empty(self.B, dtype=torch.float64, device=self.device)
+        ws = _workspace(_lib.fcgno_dot_workspace_bytes(self.grid), self.device)
+        _check(_lib.fcgno_batched_dot(self._h, _ptr(x), _ptr(y), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
+        return out
+
+
+class NeuralOperator:
+    """Packed SNO weights resident on the device."""
+
+    def __init__(self, width: int, blob: np.ndarray, precision: int = FP32, use_gelu: bool = True,
+                 device="cuda", stream=None):
+        self.desc = NoDesc(int(width), int(precision), int(bool(use_gelu)))
+        blob = np.ascontiguousarray(blob, dtype=np.float64)
+        nbytes = _lib.fcgno_no_packed_bytes(self.desc)
+        if nbytes == 0:
+            raise ValueError("bad NO descriptor")
+        self.packed = _workspace(nbytes, device)
+        _check(_lib.fcgno_no_pack(self.desc, _ptr(blob), _ptr(self.packed), _stream(stream)))
+        self.width, self.precision = int(width), int(precision)
+
+    def apply(self, problem: Problem, r: torch.Tensor, stream=None) -> torch.Tensor:
+        _require(r, problem.shape, "r")
+        w = torch.empty_like(r)
+        ws = _workspace(_lib.fcgno_apply_no_workspace_bytes(problem.grid, self.desc), problem.device)
+        _check(_lib.fcgno_apply_NO(problem._h, self.desc, _ptr(self.packed), _ptr(r), _ptr(w), _ptr(ws), ws.numel(),
+                                   _stream(stream)))
+        return w
+
+
+@dataclass
+class SolveResult:
+    u: torch.Tensor
+    iters: torch.Tensor
+    status: torch.Tensor
+    history: torch.Tensor | None
+
+
+class Solver:
+    """fcg_solve(k, f, m, tol, maxit): Algorithm 1 over the batch.
+
+    Holds the workspace so repeated solves allocate nothing."""
+
+    def __init__(self, problem: Problem, m: int, tol: float, maxit: int, no: NeuralOperator | None = None,
+                 schedule: int = SCHEDULE_PAPER, check_every: int = 16, history: bool = True,
+                 profile_mask: int = 0):
+        self.problem, self.no = problem, no
+        self.opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), int(profile_mask))
+        self._desc = ctypes.byref(no.desc) if no is not None else None
+        nbytes = _lib.fcgno_solve_workspace_bytes(problem.grid, self._desc, self.opts)
+        if nbytes == 0:
+            raise ValueError("bad solve options")
+        dev = problem.device
+        self.ws = _workspace(nbytes, dev)
+        self.iters = torch.empty(problem.B, dtype=torch.int32, device=dev)
+        self.status = torch.empty(problem.B, dtype=torch.int32, device=dev)
+        self.history = (torch.full((problem.B, maxit + 1), float("nan"), dtype=torch.float64, device=dev)
+                        if history else None)
+
+    def solve(self, f: torch.Tensor, u: torch.Tensor, stream=None) -> SolveResult:
+        """u: in = u0, out = final iterate (updated in place)."""
+        p = self.problem
+        _require(f, p.shape, "f")
+        _require(u, p.shape, "u")
+        _check(_lib.fcgno_fcg_solve(p._h, self._desc, _ptr(self.no.packed) if self.no else None, _ptr(f), _ptr(u),
+                                    self.opts, _ptr(self.iters), _ptr(self.status), _ptr(self.history),
+                                    _ptr(self.ws), self.ws.numel(), _stream(stream)))
+        return SolveResult(u, self.iters, self.status, self.history)
+
+
+def fcg_solve(problem: Problem, f: torch.Tensor, u0: torch.Tensor | None = None, *, m: int, tol: float, maxit: int,
+              no: NeuralOperator | None = None, schedule: int = SCHEDULE_PAPER, history: bool = True,
+              check_every: int = 16) -> SolveResult:
+    u = torch.zeros_like(f) if u0 is None else u0.clone()
+    return Solver(problem, m, tol, maxit, no, schedule, check_every, history).solve(f, u)
+
+
+class HostSolver:
+    """End-to-end entry point with HOST buffers (fcgno_solve_host): H2D copies, assemble, solve
+    and D2H copies inside one call."""
+
+    def __init__(self, n: int, batch: int, m: int, tol: float, maxit: int, no: NeuralOperator | None = None,
+                 schedule: int = SCHEDULE_PAPER, check_every: int = 16, device="cuda"):
+        self.grid = Grid(int(n), int(batch))
+        self.no = no
+        self.opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), 0)
+        self._desc = ctypes.byref(no.desc) if no is not None else None
+        self.ws = _workspace(_lib.fcgno_solve_host_workspace_bytes(self.grid, self._desc, self.opts), device)
+        self.n, self.B = int(n), int(batch)
+
+    def solve(self, k: np.ndarray, f: np.ndarray, u: np.ndarray, iters: np.ndarray, status: np.ndarray,
+              stream=None):
+        for name, a, dt in (("k", k, np.float64), ("f", f, np.float64), ("u", u, np.float64),
+                            ("iters", iters, np.int32), ("status", status, np.int32)):
+            if not (isinstance(a, np.ndarray) and a.dtype == dt and a.flags.c_contiguous):
+                raise TypeError(f"{name} must be a C-contiguous {dt} array")
+        _check(_lib.fcgno_solve_host(self.grid, _ptr(k), _ptr(f), _ptr(u), self._desc,
+                                     _ptr(self.no.packed) if self.no else None, self.opts, _ptr(iters),
+                                     _ptr(status), None, _ptr(self.ws), self.ws.numel(), _stream(stream)))

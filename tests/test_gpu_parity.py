@@ -1,0 +1,352 @@
+"""GPU parity: the CUDA path through the C-ABI against the fp64 oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north_star):
+  apply_A, reductions         fp64, <= 1e-12 relative (bitwise here: same op order, exact dots)
+  NO forward, fp32            <= 1e-4 relative L2 per system
+  NO forward, fp64 mode       <= 1e-12 relative L2 per system
+  FCG residual histories      <= 1e-8 relative per iteration (identity: bitwise)
+  iteration counts            equal within +-1 (identity: exact)
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+import synthetic as sy
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+# ----------------------------------------------------------------------------- apply_A
+@pytest.mark.parametrize("n,B,kind", [(2, 1, "lognormal"), (3, 2, "const"), (20, 3, "lognormal"),
+                                      (33, 2, "lognormal"), (45, 5, "rectangles"), (64, 4, "lognormal"),
+                                      (100, 2, "lognormal4")])
+def test_apply_A_bitwise(lib, n, B, kind):
+    if kind == "const":
+        k = np.full((B, n, n), 3.5)
+    elif kind == "rectangles":
+        k = sy.rectangles_k(n, B, seed=5)
+    elif kind == "lognormal4":
+        k = sy.lognormal_k(n, B, 0.05, 4.0, seed=6)
+    else:
+        k = sy.lognormal_k(n, B, 0.1, 1.0, seed=7)
+    x = sy.normal_field(n, B, seed=8)
+    p = lib.Problem(dev(k))
+    y = host(p.apply_A(dev(x)))
+    ref = orc.apply_A(k, x)
+    assert np.array_equal(y, ref), np.max(np.abs(y - ref))
+
+
+@pytest.mark.parametrize("cfg_id", [3, 4, 5])
+def test_apply_A_full_configs(lib, cfg_id):
+    cfg = sy.CONFIGS[cfg_id]
+    k = sy.make_k(cfg)
+    x = sy.make_f(cfg)
+    y = host(lib.Problem(dev(k)).apply_A(dev(x)))
+    ref = orc.apply_A(k, x)
+    assert np.max(np.abs(y - ref) / (np.abs(ref) + 1e-300)) <= 1e-12
+    assert np.array_equal(y, ref)
+
+
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_apply_A_sweep_sizes_closed_form(lib, n):
+    # k = 1: the closed-form eigenvector is reproduced pointwise at the sweep sizes (BJ:11).
+    p, q = 3, 7
+    x = np.arange(1, n + 1) / (n + 1)
+    v = np.sin(q * np.pi * x)[:, None] * np.sin(p * np.pi * x)[None, :]
+    lam = 4 * (n + 1) ** 2 * (np.sin(p * np.pi / (2 * (n + 1))) ** 2 + np.sin(q * np.pi / (2 * (n + 1))) ** 2)
+    prob = lib.Problem(dev(np.ones((1, n, n))))
+    y = host(prob.apply_A(dev(v[None])))[0]
+    scale = np.abs(lam * v).max()
+    assert np.max(np.abs(y - lam * v)) < 1e-6 * scale
+    # and equals the oracle bit for bit on a sampled band of rows
+    ref = orc.apply_A(np.ones((n, n)), v)
+    assert np.array_equal(y[:64], ref[:64]) and np.array_equal(y[-64:], ref[-64:])
+
+
+def test_assemble_rejects_bad_k(lib):
+    k = np.ones((2, 8, 8)); k[1, 3, 4] = 0.0
+    with pytest.raises(lib.FcgnoError) as e:
+        lib.Problem(dev(k))
+    assert e.value.code == 2
+    k[1, 3, 4] = np.nan
+    with pytest.raises(lib.FcgnoError):
+        lib.Problem(dev(k))
+
+
+# ----------------------------------------------------------------------------- reductions
+@pytest.mark.parametrize("n,B", [(5, 3), (32, 1), (64, 8), (129, 2), (512, 2)])
+def test_dot_correctly_rounded(lib, n, B):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((B, n, n)) * 10.0 ** rng.integers(-3, 3, (B, 1, 1))
+    y = rng.standard_normal((B, n, n))
+    p = lib.Problem(dev(np.ones((B, n, n))))
+    got = host(p.dot(dev(x), dev(y)))
+    for b in range(B):
+        assert got[b] == orc.dot(x[b], y[b])
+    # ill-conditioned: y made nearly orthogonal to x
+    y2 = y - (np.sum(x * y, axis=(1, 2)) / np.sum(x * x, axis=(1, 2)))[:, None, None] * x
+    got2 = host(p.dot(dev(x), dev(y2)))
+    for b in range(B):
+        ref = orc.dot(x[b], y2[b])
+        assert abs(got2[b] - ref) <= 1e-12 * float(np.sum(np.abs(x[b] * y2[b])))
+
+
+def test_dot_integer_exact(lib):
+    rng = np.random.default_rng(3)
+    x = rng.integers(-2 ** 20, 2 ** 20, (2, 64, 64)).astype(float)
+    y = rng.integers(-2 ** 20, 2 ** 20, (2, 64, 64)).astype(float)
+    got = host(lib.Problem(dev(np.ones((2, 64, 64)))).dot(dev(x), dev(y)))
+    for b in range(2):
+        assert got[b] == float(int(np.dot(x[b].ravel().astype(object), y[b].ravel().astype(object))))
+
+
+# ----------------------------------------------------------------------------- NO forward
+def _no_case(n, B, w, wseed, seed):
+    k = sy.lognormal_k(n, B, 0.1, 1.0, seed)
+    r = sy.normal_field(n, B, seed + 1)
+    blob = sy.no_weights(w, wseed)
+    return k, r, blob
+
+
+@pytest.mark.parametrize("n,B,w", [(20, 2, 4), (32, 1, 32), (37, 2, 8), (64, 3, 48)])
+def test_no_fp64_matches_oracle(lib, n, B, w):
+    k, r, blob = _no_case(n, B, w, 11, 12)
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob, precision=lib.FP64)
+    got = host(no.apply(prob, dev(r)))
+    params = orc.unpack_weights(blob, w)
+    for b in range(B):
+        ref = orc.no_forward(params, r[b], k[b])
+        assert rel_l2(got[b], ref) <= 1e-12
+
+
+@pytest.mark.parametrize("n,B,w", [(20, 2, 4), (32, 2, 32), (45, 3, 48), (64, 8, 48), (128, 2, 85)])
+def test_no_fp32_matches_oracle(lib, n, B, w):
+    k, r, blob = _no_case(n, B, w, 21, 22)
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob, precision=lib.FP32)
+    got = host(no.apply(prob, dev(r)))
+    params = orc.unpack_weights(blob, w)
+    for b in sorted({0, B - 1}):
+        ref = orc.no_forward(params, r[b], k[b])
+        assert rel_l2(got[b], ref) <= 1e-4
+
+
+@pytest.mark.parametrize("cfg_id", [2, 5])
+def test_no_fp32_full_config_sampled(lib, cfg_id):
+    cfg = sy.CONFIGS[cfg_id]
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(cfg["width"], blob, precision=lib.FP32)
+    got = host(no.apply(prob, dev(f)))
+    params = orc.unpack_weights(blob, cfg["width"])
+    for b in (0, cfg["batch"] - 1):
+        assert rel_l2(got[b], orc.no_forward(params, f[b], k[b])) <= 1e-4
+
+
+def test_no_properties(lib):
+    n, B, w = 32, 2, 16
+    k, r, blob = _no_case(n, B, w, 31, 32)
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob, precision=lib.FP64)
+    base = host(no.apply(prob, dev(r)))
+    scaled = host(no.apply(prob, dev(3.0 * r)))
+    assert np.max(np.abs(scaled - 3.0 * base)) <= 1e-12 * np.max(np.abs(base)) * 3
+    zero = host(no.apply(prob, dev(np.zeros_like(r))))
+    assert np.all(zero == 0.0)
+    z = lib.NeuralOperator(w, np.zeros(sy.no_blob_size(w)), precision=lib.FP32)
+    assert np.all(host(z.apply(prob, dev(r))) == 0.0)
+
+
+def test_no_structured_closed_form(lib):
+    n, w = 64, 4
+    k = sy.lognormal_k(n, 2, 0.1, 1.0, 41)
+    r = sy.normal_field(n, 2, 42)
+    blob = sy.structured_no_weights(w, n)
+    prob = lib.Problem(dev(k))
+    got = host(lib.NeuralOperator(w, blob, precision=lib.FP64).apply(prob, dev(r)))
+    params = orc.unpack_weights(blob, w)
+    for b in range(2):
+        assert rel_l2(got[b], orc.no_forward(params, r[b], k[b])) <= 1e-12
+
+
+def test_no_linear_mode(lib):
+    n, w = 24, 4
+    k, r, blob = _no_case(n, 1, w, 51, 52)
+    prob = lib.Problem(dev(k))
+    got = host(lib.NeuralOperator(w, blob, precision=lib.FP64, use_gelu=False).apply(prob, dev(r)))
+    ref = orc.no_forward(orc.unpack_weights(blob, w), r[0], k[0], use_gelu=False)
+    assert rel_l2(got[0], ref) <= 1e-12
+
+
+def test_no_rejects_small_grid(lib):
+    prob = lib.Problem(dev(np.ones((1, 16, 16))))
+    no = lib.NeuralOperator(4, sy.no_weights(4, 1))
+    with pytest.raises(lib.FcgnoError) as e:
+        no.apply(prob, dev(np.ones((1, 16, 16))))
+    assert e.value.code == 5
+
+
+# ----------------------------------------------------------------------------- FCG, identity
+def _oracle_fcg(k, f, m, tol, maxit, precond=None, schedule="paper"):
+    return orc.fcg(lambda x: orc.apply_A(k, x), f, np.zeros_like(f), m, tol, maxit, precond=precond,
+                   schedule=schedule)
+
+
+def _check_identity(lib, k, f, m, tol, maxit, systems, schedule=0):
+    prob = lib.Problem(dev(k))
+    res = lib.fcg_solve(prob, dev(f), m=m, tol=tol, maxit=maxit, schedule=schedule)
+    iters, status, hist, u = host(res.iters), host(res.status), host(res.history), host(res.u)
+    for b in systems:
+        ref = _oracle_fcg(k[b], f[b], m, tol, maxit, schedule="sliding" if schedule else "paper")
+        it = ref["iters"]
+        assert iters[b] == it and status[b] == ref["status"]
+        assert np.array_equal(hist[b, :it + 1], ref["hist"]), "identity histories must agree bit for bit"
+        assert np.array_equal(u[b], ref["u"])
+    return iters, status
+
+
+def test_identity_config1_bitwise(lib):
+    cfg = sy.CONFIGS[1]
+    _check_identity(lib, sy.make_k(cfg), sy.make_f(cfg), cfg["m"], cfg["tol"], cfg["maxit"], [0])
+
+
+def test_identity_config2_sampled(lib):
+    cfg = dict(sy.CONFIGS[2])
+    k, f = sy.make_k(cfg), sy.make_f(cfg)
+    iters, status = _check_identity(lib, k, f, cfg["m"], cfg["tol"], 5000, [0, cfg["batch"] - 1])
+    assert np.all(status == lib.CONVERGED)
+
+
+@pytest.mark.parametrize("n,B,m", [(20, 3, 5), (45, 2, 10), (7, 2, 1)])
+def test_identity_ragged(lib, n, B, m):
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 61)
+    f = sy.normal_field(n, B, 62)
+    _check_identity(lib, k, f, m, 1e-8, 3000, range(B))
+
+
+@pytest.mark.parametrize("n", [4, 8])
+def test_identity_sliding_full_window_finite_termination(lib, n):
+    k = sy.lognormal_k(n, 2, 0.1, 4.0, 71)
+    f = sy.normal_field(n, 2, 72)
+    iters, status = _check_identity(lib, k, f, min(n * n, 64), 1e-10, 5 * n * n, range(2), schedule=1)
+    assert np.all(iters <= n * n) and np.all(status == lib.CONVERGED)
+
+
+def test_fcg_edge_cases(lib):
+    n, B = 20, 3
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 81)
+    f = sy.normal_field(n, B, 82)
+    f[1] = 0.0                                   # r0 = 0: converged at 0 iterations
+    prob = lib.Problem(dev(k))
+    res = lib.fcg_solve(prob, dev(f), m=5, tol=1e-8, maxit=2000)
+    assert host(res.status)[1] == lib.CONVERGED and host(res.iters)[1] == 0
+    assert np.all(host(res.u)[1] == 0.0)
+    res0 = lib.fcg_solve(prob, dev(f), m=5, tol=1e-8, maxit=0)
+    assert list(host(res0.status)) == [lib.MAXIT, lib.CONVERGED, lib.MAXIT]
+    resm = lib.fcg_solve(prob, dev(f), m=5, tol=1e-8, maxit=7)
+    assert list(host(resm.iters)) == [7, 0, 7]
+    # zero NO weights: w = 0 -> p = 0 -> (p, s) = 0 -> breakdown at i = 0
+    z = lib.NeuralOperator(4, np.zeros(sy.no_blob_size(4)))
+    resz = lib.fcg_solve(prob, dev(f), m=5, tol=1e-8, maxit=10, no=z)
+    assert host(resz.status)[0] == lib.BREAKDOWN and host(resz.iters)[0] == 0
+    # overflowing fp32 NO: non-finite preconditioner output
+    big = lib.NeuralOperator(4, sy.no_weights(4, 3) * 1e30)
+    resb = lib.fcg_solve(prob, dev(f), m=5, tol=1e-8, maxit=10, no=big)
+    assert host(resb.status)[0] == lib.NONFINITE and host(resb.iters)[0] == 0
+
+
+# ----------------------------------------------------------------------------- FCG with the NO
+def _prefix_window_ok(h_gpu, h_ref, upto, rtol=1e-8):
+    a, b = h_gpu[:upto + 1], h_ref[:upto + 1]
+    return np.max(np.abs(a - b) / b) <= rtol
+
+
+def test_fcg_no_fp64_config1_prefix(lib):
+    # fp64 NO: histories agree to <= 1e-8 over the prefix window where the oracle's own
+    # 1-ulp sensitivity stays below 1e-9.
+    cfg = sy.CONFIGS[1]
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    w = cfg["width"]
+    params = orc.unpack_weights(blob, w)
+    maxit = 40
+    ref = _oracle_fcg(k[0], f[0], cfg["m"], cfg["tol"], maxit, precond=lambda r: orc.no_forward(params, r, k[0]))
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob, precision=lib.FP64)
+    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit, no=no)
+    h = host(res.history)[0]
+    assert host(res.status)[0] == lib.MAXIT == ref["status"]
+    assert _prefix_window_ok(h, ref["hist"], 15)
+    assert np.max(np.abs(h - ref["hist"]) / ref["hist"]) <= 1e-3
+
+
+def test_fcg_structured_no_fp64_counts(lib):
+    # Supplementary convergent workload: iteration counts within +-1.
+    n, B, w = 32, 2, 4
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 91)
+    f = sy.normal_field(n, B, 92)
+    blob = sy.structured_no_weights(w, n)
+    params = orc.unpack_weights(blob, w)
+    prob = lib.Problem(dev(k))
+    res = lib.fcg_solve(prob, dev(f), m=5, tol=1e-8, maxit=500,
+                        no=lib.NeuralOperator(w, blob, precision=lib.FP64))
+    for b in range(B):
+        ref = _oracle_fcg(k[b], f[b], 5, 1e-8, 500, precond=lambda r: orc.no_forward(params, r, k[b]))
+        assert abs(int(host(res.iters)[b]) - ref["iters"]) <= 1
+        assert host(res.status)[b] == lib.CONVERGED
+        assert _prefix_window_ok(host(res.history)[b], ref["hist"], 20)
+
+
+def test_fcg_no_fp32_config2_sampled(lib):
+    cfg = sy.CONFIGS[2]
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    w = cfg["width"]
+    params = orc.unpack_weights(blob, w)
+    maxit = 30
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob, precision=lib.FP32)
+    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit, no=no)
+    assert np.all(host(res.status) == lib.MAXIT) and np.all(host(res.iters) == maxit)
+    for b in (0, cfg["batch"] - 1):
+        ref = _oracle_fcg(k[b], f[b], cfg["m"], cfg["tol"], maxit,
+                          precond=lambda r: orc.no_forward(params, r, k[b]))
+        h = host(res.history)[b]
+        # fp32 NO vs fp64 NO moves histories by ~1e-5..1e-3
+        assert np.max(np.abs(h - ref["hist"]) / ref["hist"]) <= 1e-2
+
+
+def test_solve_host_matches_device(lib):
+    cfg = sy.CONFIGS[1]
+    k, f = sy.make_k(cfg), sy.make_f(cfg)
+    hs = lib.HostSolver(cfg["n"], cfg["batch"], cfg["m"], cfg["tol"], cfg["maxit"])
+    u = np.zeros_like(f)
+    iters = np.zeros(cfg["batch"], np.int32); status = np.zeros(cfg["batch"], np.int32)
+    hs.solve(np.ascontiguousarray(k), np.ascontiguousarray(f), u, iters, status)
+    res = lib.fcg_solve(lib.Problem(dev(k)), dev(f), m=cfg["m"], tol=cfg["tol"], maxit=cfg["maxit"])
+    assert np.array_equal(u, host(res.u)) and np.array_equal(iters, host(res.iters))
+
+
+def test_repeat_solves_deterministic(lib):
+    cfg = sy.CONFIGS[2]
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(cfg["width"], blob)
+    s = lib.Solver(prob, cfg["m"], cfg["tol"], 12, no=no)
+    u1 = torch.zeros_like(dev(f)); s.solve(dev(f), u1); h1 = s.history.clone()
+    u2 = torch.zeros_like(dev(f)); s.solve(dev(f), u2)
+    assert torch.equal(u1, u2) and torch.equal(h1, s.history)
