@@ -432,7 +432,7 @@ struct Profiler : ProfHook {
     if (!(mask >> cls & 1)) return;
     Rec r{cls, nullptr, nullptr};
     if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) { failed = true; return; }
-    if (cudaEventRecord(r.a, s) != cudaSuccess) failed = true;
+    if (cudaEventRecordWithFlags(r.a, s, cudaEventRecordExternal) != cudaSuccess) failed = true;
     pending.push_back(r);
   }
   void end(int cls, cudaStream_t s) override {
@@ -441,7 +441,7 @@ struct Profiler : ProfHook {
       if (pending[t].cls == cls) {
         Rec r = pending[t];
         pending.erase(pending.begin() + t);
-        if (cudaEventRecord(r.b, s) != cudaSuccess) failed = true;
+        if (cudaEventRecordWithFlags(r.b, s, cudaEventRecordExternal) != cudaSuccess) failed = true;
         recs.push_back(r);
         return;
       }
@@ -509,6 +509,8 @@ struct Chunk {
       if (cudaEventElapsedTime(&ms, r.a, r.b) == cudaSuccess) {
         prof_totals().ms[r.cls] += ms;
         prof_totals().n[r.cls] += 1;
+      } else {
+        (void)cudaGetLastError();  // never leave a stale error for the caller's runtime
       }
     }
   }
@@ -622,6 +624,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
   } while (false);
   cudaError_t e_end = cudaStreamSynchronize(s);
   if (rc == FCGNO_OK && e_end != cudaSuccess) rc = cuda_fail(e_end, "solve");
+  if (rc == FCGNO_OK) (void)cudaGetLastError();
   // order the caller's stream after the solve
   if (cudaEventRecord(ev_in, s) == cudaSuccess) cudaStreamWaitEvent(caller, ev_in, 0);
   full[0].destroy(); full[1].destroy(); tail.destroy();

@@ -438,8 +438,22 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
 }
 
 // ------------------------------------------------------------------ launcher
+// Largest dynamic shared memory a CTA may request on this device (opt-in limit).
+static int optin_smem() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      v = kMaxDynSmem;
+  }
+  return v;
+}
+
 static cudaError_t set_smem(const void* fn) {
-  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaFuncAttributes fa{};
+  cudaError_t e = cudaFuncGetAttributes(&fa, fn);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin_smem() - (int)fa.sharedSizeBytes);
 }
 
 // Raise the dynamic shared-memory limit of every NO kernel once (never during graph capture).

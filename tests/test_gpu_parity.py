@@ -277,6 +277,18 @@ def _prefix_window_ok(h_gpu, h_ref, upto, rtol=1e-8):
     return np.max(np.abs(a - b) / b) <= rtol
 
 
+def _self_sensitivity_window(k, f, m, tol, maxit, precond, thresh=1e-9):
+    """Prefix window of G3(a): the first iteration at which the oracle's own
+    history moves by more than `thresh` when every preconditioner output is perturbed by one
+    ulp.  Beyond it, no implementation can be held to 1e-8 (FCG amplifies rounding chaotically)."""
+    base = _oracle_fcg(k, f, m, tol, maxit, precond=precond)
+    pert = _oracle_fcg(k, f, m, tol, maxit, precond=lambda r: np.nextafter(precond(r), np.inf))
+    n = min(len(base["hist"]), len(pert["hist"]))
+    d = np.abs(pert["hist"][:n] - base["hist"][:n]) / base["hist"][:n]
+    bad = np.nonzero(d > thresh)[0]
+    return base, (int(bad[0]) - 1 if bad.size else n - 1)
+
+
 def test_fcg_no_fp64_config1_prefix(lib):
     # fp64 NO: histories agree to <= 1e-8 over the prefix window where the oracle's own
     # 1-ulp sensitivity stays below 1e-9 (DESIGN.md §4, SURVEY.md C.4 G3(a)).
@@ -285,13 +297,15 @@ def test_fcg_no_fp64_config1_prefix(lib):
     w = cfg["width"]
     params = orc.unpack_weights(blob, w)
     maxit = 40
-    ref = _oracle_fcg(k[0], f[0], cfg["m"], cfg["tol"], maxit, precond=lambda r: orc.no_forward(params, r, k[0]))
+    ref, window = _self_sensitivity_window(k[0], f[0], cfg["m"], cfg["tol"], maxit,
+                                           lambda r: orc.no_forward(params, r, k[0]))
     prob = lib.Problem(dev(k))
     no = lib.NeuralOperator(w, blob, precision=lib.FP64)
     res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit, no=no)
     h = host(res.history)[0]
     assert host(res.status)[0] == lib.MAXIT == ref["status"]
-    assert _prefix_window_ok(h, ref["hist"], 15)
+    assert window >= 8
+    assert _prefix_window_ok(h, ref["hist"], window)
     assert np.max(np.abs(h - ref["hist"]) / ref["hist"]) <= 1e-3
 
 
@@ -306,10 +320,12 @@ def test_fcg_structured_no_fp64_counts(lib):
     res = lib.fcg_solve(prob, dev(f), m=5, tol=1e-8, maxit=500,
                         no=lib.NeuralOperator(w, blob, precision=lib.FP64))
     for b in range(B):
-        ref = _oracle_fcg(k[b], f[b], 5, 1e-8, 500, precond=lambda r: orc.no_forward(params, r, k[b]))
+        ref, window = _self_sensitivity_window(k[b], f[b], 5, 1e-8, 500,
+                                               lambda r: orc.no_forward(params, r, k[b]))
         assert abs(int(host(res.iters)[b]) - ref["iters"]) <= 1
         assert host(res.status)[b] == lib.CONVERGED
-        assert _prefix_window_ok(host(res.history)[b], ref["hist"], 20)
+        assert window >= 8
+        assert _prefix_window_ok(host(res.history)[b], ref["hist"], window)
 
 
 def test_fcg_no_fp32_config2_sampled(lib):
