@@ -204,18 +204,23 @@ struct LayerArgs {
   const int* status;
 };
 
+constexpr int kFsmemMaxN = 128;   // stage the twiddle table in shared memory up to this n
+
 template <typename T, int GO>
 struct LayerSmem {
   // element offsets (in T) of each region; complex regions are 2 T per entry
-  size_t Wsm, bsm, gh, Vin, Vout, Gs, Tx, total;
-  __host__ __device__ LayerSmem(int n, int cin, int rows) {
+  size_t Wsm, bsm, gh, Fs, Vin, Vout, Gs, Tx, total;
+  int nbuf;
+  __host__ __device__ LayerSmem(int n, int cin, int rows, bool first) {
     const int CH = rows * n;
+    nbuf = first ? 1 : 2;                       // double-buffered input rows (cp.async)
     size_t o = 0;
     auto al = [](size_t x) { return (x + 3) & ~size_t(3); };
     Wsm = o; o = al(o + (size_t)cin * GO);
     bsm = o; o = al(o + GO);
     gh = o; o = al(o + (size_t)2 * GO * kGhStride);
-    Vin = o; o = al(o + (size_t)cin * CH);
+    Fs = o; o = al(o + (n <= kFsmemMaxN ? (size_t)2 * n * kModes : 0));
+    Vin = o; o = al(o + (size_t)nbuf * cin * CH);
     Vout = o; o = al(o + (size_t)GO * CH);
     Gs = o; o = al(o + (size_t)2 * rows * kModes * GO);
     Tx = o; o = al(o + (size_t)2 * GO * (rows * kModes + 1));
@@ -225,25 +230,71 @@ struct LayerSmem {
 
 template <typename T> constexpr int layer_go() { return sizeof(T) == 4 ? 8 : 4; }
 
+// Rows per chunk: up to 256 pixels, halved until the CTA's shared memory fits the opt-in limit.
+template <typename T>
+int layer_rows(int n, int cin, bool first, size_t limit) {
+  int rows = n >= 256 ? 1 : 256 / n;
+  while (rows > 1 && LayerSmem<T, layer_go<T>()>(n, cin, rows, first).total * sizeof(T) > limit) rows = (rows + 1) / 2;
+  return rows;
+}
+
+__device__ __forceinline__ void cp_async_bytes16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(gsrc));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_small(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(gsrc),
+               "n"(BYTES));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 template <typename T, bool FIRST, int GO>
 __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   using T2 = typename Cplx<T>::type;
   constexpr int NACC = (GO * kModes2 + 255) / 256;
+  constexpr int VEC = 16 / sizeof(T);
   const int b = blockIdx.y, og = blockIdx.x * GO;
   if (a.status && a.status[b] != SYS_RUNNING) return;
   const int n = a.n, N = a.N, cin = a.cin, w = a.w, RC = a.rows;
   const int go = min(GO, w - og);
-  const LayerSmem<T, GO> L(n, cin, RC);
+  const LayerSmem<T, GO> L(n, cin, RC, FIRST);
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
   T* Wsm = sm + L.Wsm;           // [cin][GO]
   T* bsm = sm + L.bsm;           // [GO]
   T2* gh = reinterpret_cast<T2*>(sm + L.gh);      // [GO][kGhStride]
-  T* Vin = sm + L.Vin;           // [cin][CH]
+  T* VinB = sm + L.Vin;          // [nbuf][cin][CH]
   T* Vout = sm + L.Vout;         // [GO][CH]
   T2* Gs = reinterpret_cast<T2*>(sm + L.Gs);      // [RC][20][GO]
   T2* Tx = reinterpret_cast<T2*>(sm + L.Tx);      // [GO][RC*20+1]
   const int TXS = RC * kModes + 1;
+  const int CH = RC * n;
+  const bool fsm = n <= kFsmemMaxN;
+  T2* Fsm = reinterpret_cast<T2*>(sm + L.Fs);
+  const T2* Ft = fsm ? Fsm : a.F;                 // twiddles exp(-2 pi i kappa j / n), [n][20]
+
+  // async staging of the input rows of chunk i0 into buffer `buf` (layers 2, 3)
+  auto stage = [&](int i0, int buf) {
+    const int rows = min(RC, n - i0), npix = rows * n;
+    T* dst = VinB + (size_t)buf * cin * CH;
+    const T* src = a.vin + (size_t)b * cin * N + (size_t)i0 * n;
+    if (n % VEC == 0) {
+      const int nv = npix / VEC;
+      for (int t = threadIdx.x; t < cin * nv; t += blockDim.x) {
+        const int c = t / nv, q = t - c * nv;
+        cp_async_bytes16(dst + (size_t)c * npix + q * VEC, src + (size_t)c * N + q * VEC);
+      }
+    } else {
+      for (int t = threadIdx.x; t < cin * npix; t += blockDim.x) {
+        const int c = t / npix, q = t - c * npix;
+        cp_async_small<sizeof(T)>(dst + (size_t)c * npix + q, src + (size_t)c * N + q);
+      }
+    }
+    cp_async_commit();
+  };
+  if (!FIRST) stage(0, 0);
 
   for (int t = threadIdx.x; t < cin * GO; t += blockDim.x) {
     const int c = t / GO, o = t - c * GO;
@@ -254,6 +305,8 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
     const int o = t / kModes2, kk = t - o * kModes2;
     gh[o * kGhStride + kk] = o < go ? a.ghat[((size_t)b * w + og + o) * kModes2 + kk] : T2{T(0), T(0)};
   }
+  if (fsm)
+    for (int t = threadIdx.x; t < n * kModes; t += blockDim.x) Fsm[t] = a.F[t];
   double inv_s = 1.0;
   if (FIRST) {
     const double s = sqrt(a.rr[b]);
@@ -264,10 +317,12 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   for (int q = 0; q < NACC; ++q) { accr[q] = 0; acci[q] = 0; }
   __syncthreads();
 
-  for (int i0 = 0; i0 < n; i0 += RC) {
+  int it = 0;
+  for (int i0 = 0; i0 < n; i0 += RC, ++it) {
     const int rows = min(RC, n - i0), npix = rows * n;
     const size_t base = (size_t)i0 * n;
-    // 1. stage the input rows of every input channel
+    T* Vin = VinB + (size_t)(FIRST ? 0 : (it & 1)) * cin * CH;
+    // 1. input rows of every input channel (layer 1: r/||r|| and k converted on the fly)
     if (FIRST) {
       const double* rb = a.r + (size_t)b * N + base;
       const double* kb = a.k + (size_t)b * N + base;
@@ -276,20 +331,18 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
         Vin[npix + t] = (T)kb[t];
       }
     } else {
-      for (int t = threadIdx.x; t < cin * npix; t += blockDim.x) {
-        const int c = t / npix, p = t - c * npix;
-        Vin[c * npix + p] = a.vin[((size_t)b * cin + c) * N + base + p];
-      }
+      if (i0 + RC < n) { stage(i0 + RC, (it + 1) & 1); cp_async_wait<1>(); }
+      else cp_async_wait<0>();
     }
     // 2. y-synthesis of this layer's spectral term for the rows: Gs[r][k2][o]
     for (int e = threadIdx.x; e < rows * kModes * GO; e += blockDim.x) {
       const int o = e % GO, rk = e / GO, r = rk / kModes, k2 = rk - r * kModes;
       T gr = 0, gi = 0;
-      const T2* F1 = a.F + (size_t)(i0 + r) * kModes;
+      const T2* F1 = Ft + (size_t)(i0 + r) * kModes;
 #pragma unroll 4
       for (int k1 = 0; k1 < kModes; ++k1) {
         const T2 g = gh[o * kGhStride + k1 * kModes + k2];
-        const T2 f = __ldg(F1 + k1);                 // conj(f) = exp(+2 pi i kappa1 i / n)
+        const T2 f = F1[k1];                         // conj(f) = exp(+2 pi i kappa1 i / n)
         gr += g.x * f.x + g.y * f.y;
         gi += g.y * f.x - g.x * f.y;
       }
@@ -302,16 +355,17 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
       T acc[GO];
 #pragma unroll
       for (int o = 0; o < GO; ++o) acc[o] = bsm[o];
+#pragma unroll 4
       for (int c = 0; c < cin; ++c) {
         const T x = Vin[c * npix + p];
 #pragma unroll
         for (int o = 0; o < GO; ++o) acc[o] += Wsm[c * GO + o] * x;
       }
-      const T2* Fj = a.F + (size_t)j * kModes;
+      const T2* Fj = Ft + (size_t)j * kModes;
       const T2* Gr = Gs + (size_t)r * kModes * GO;
-#pragma unroll 2
+#pragma unroll 4
       for (int k2 = 0; k2 < kModes; ++k2) {
-        const T2 f = __ldg(Fj + k2);                 // Re(G exp(+i th)) = G.x f.x + G.y f.y
+        const T2 f = Fj[k2];                         // Re(G exp(+i th)) = G.x f.x + G.y f.y
 #pragma unroll
         for (int o = 0; o < GO; ++o) {
           const T2 g = Gr[k2 * GO + o];
@@ -331,8 +385,9 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
       const int k2 = e % kModes, orr = e / kModes, r = orr % rows, o = orr / rows;
       const T* vrow = Vout + (size_t)o * npix + (size_t)r * n;
       T tr = 0, ti = 0;
+#pragma unroll 4
       for (int j = 0; j < n; ++j) {
-        const T2 f = __ldg(a.F + (size_t)j * kModes + k2);
+        const T2 f = Ft[(size_t)j * kModes + k2];
         const T v = vrow[j];
         tr += v * f.x; ti += v * f.y;
       }
@@ -346,7 +401,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
       if (e < GO * kModes2) {
         const int o = e % GO, kk = e / GO, k1 = kk / kModes, k2 = kk - k1 * kModes;
         for (int r = 0; r < rows; ++r) {
-          const T2 f = __ldg(a.F + (size_t)(i0 + r) * kModes + k1);
+          const T2 f = Ft[(size_t)(i0 + r) * kModes + k1];
           const T2 t = Tx[o * TXS + r * kModes + k2];
           accr[q] += f.x * t.x - f.y * t.y;
           acci[q] += f.x * t.y + f.y * t.x;
@@ -364,8 +419,6 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
     }
   }
 }
-
-
 
 // ------------------------------------------------------------------ layer 4 + projection + FCG window dots
 template <typename T>
@@ -478,8 +531,9 @@ template cudaError_t prepare_no_kernels<double>();
 template <typename T>
 size_t no_max_smem(int n, int w) {
   constexpr int GO = layer_go<T>();
-  const int rows = n >= 256 ? 1 : 256 / n;
-  size_t m = LayerSmem<T, GO>(n, w, rows).total * sizeof(T);
+  const size_t lim = (size_t)optin_smem() - 2048;
+  const int rows1 = layer_rows<T>(n, w, false, lim);
+  size_t m = LayerSmem<T, GO>(n, w, rows1, false).total * sizeof(T);
   const size_t msmem = ((size_t)w * w + (size_t)kMixBatch * w) * 2 * sizeof(T);
   return m > msmem ? m : msmem;
 }
@@ -514,11 +568,12 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   pe(PROF_NO_INPUT);
   ++launches;
   // 3. layers 1..3, each followed by the mixing of the next layer
-  const int rows = n >= 256 ? 1 : 256 / n;
+  const size_t lim = (size_t)optin_smem() - 2048;
   const dim3 lgrid((w + GO - 1) / GO, B);
   T* vbuf[2] = {no.v0, no.v1};
   for (int l = 0; l < 3; ++l) {
     LayerArgs<T> la{};
+    const int rows = layer_rows<T>(n, l == 0 ? 2 : w, l == 0, lim);
     la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.use_gelu = no.use_gelu;
     la.r = r; la.rr = rr; la.k = no.k;
     la.ghat = ghat; la.F = F; la.chat = chat; la.status = status;
@@ -528,7 +583,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     } else {
       la.cin = w; la.W = pk + no.L.W[l - 1]; la.bias = pk + no.L.b[l - 1]; la.vin = vbuf[(l - 1) & 1];
     }
-    const size_t smem = LayerSmem<T, GO>(n, la.cin, rows).total * sizeof(T);
+    const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, l == 0).total * sizeof(T);
     pb(PROF_NO_LAYER);
     if (l == 0) {
       k_no_layer<T, true, GO><<<lgrid, 256, smem, s>>>(la);
