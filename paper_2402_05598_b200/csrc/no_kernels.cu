@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_mix(const typename Cplx<T>::type* __res
 // ------------------------------------------------------------------ operator layer (layers 1-3)
 template <typename T>
 struct LayerArgs {
-  int n, N, w, cin, B, rows, use_gelu;
+  int n, N, w, cin, B, rows, nbuf, use_gelu;
   const double* r; const double* rr; const double* k;   // FIRST layer inputs
   const T* vin;                                          // [B][cin][N] (layers 2, 3)
   const T* W;                                            // [w][cin]
@@ -211,9 +211,9 @@ struct LayerSmem {
   // element offsets (in T) of each region; complex regions are 2 T per entry
   size_t Wsm, bsm, gh, Fs, Vin, Vout, Gs, Tx, total;
   int nbuf;
-  __host__ __device__ LayerSmem(int n, int cin, int rows, bool first) {
+  __host__ __device__ LayerSmem(int n, int cin, int rows, int nbuf_) {
     const int CH = rows * n;
-    nbuf = first ? 1 : 2;                       // double-buffered input rows (cp.async)
+    nbuf = nbuf_;                               // 2: double-buffered input rows (cp.async)
     size_t o = 0;
     auto al = [](size_t x) { return (x + 3) & ~size_t(3); };
     Wsm = o; o = al(o + (size_t)cin * GO);
@@ -230,12 +230,17 @@ struct LayerSmem {
 
 template <typename T> constexpr int layer_go() { return sizeof(T) == 4 ? 8 : 4; }
 
-// Rows per chunk: up to 256 pixels, halved until the CTA's shared memory fits the opt-in limit.
+// Rows per chunk (up to 256 pixels) and input buffering: halve the rows, then drop the second
+// buffer, until the CTA's shared memory fits the opt-in limit.
 template <typename T>
-int layer_rows(int n, int cin, bool first, size_t limit) {
+void layer_config(int n, int cin, bool first, size_t limit, int* rows_out, int* nbuf_out) {
+  int nbuf = first ? 1 : 2;
   int rows = n >= 256 ? 1 : 256 / n;
-  while (rows > 1 && LayerSmem<T, layer_go<T>()>(n, cin, rows, first).total * sizeof(T) > limit) rows = (rows + 1) / 2;
-  return rows;
+  auto bytes = [&]() { return LayerSmem<T, layer_go<T>()>(n, cin, rows, nbuf).total * sizeof(T); };
+  while (rows > 1 && bytes() > limit) rows = (rows + 1) / 2;
+  if (bytes() > limit) nbuf = 1;
+  *rows_out = rows;
+  *nbuf_out = nbuf;
 }
 
 __device__ __forceinline__ void cp_async_bytes16(void* sdst, const void* gsrc) {
@@ -259,7 +264,8 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   if (a.status && a.status[b] != SYS_RUNNING) return;
   const int n = a.n, N = a.N, cin = a.cin, w = a.w, RC = a.rows;
   const int go = min(GO, w - og);
-  const LayerSmem<T, GO> L(n, cin, RC, FIRST);
+  const int nbuf = a.nbuf;
+  const LayerSmem<T, GO> L(n, cin, RC, nbuf);
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
   T* Wsm = sm + L.Wsm;           // [cin][GO]
@@ -294,7 +300,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
     }
     cp_async_commit();
   };
-  if (!FIRST) stage(0, 0);
+  if (!FIRST && nbuf == 2) stage(0, 0);
 
   for (int t = threadIdx.x; t < cin * GO; t += blockDim.x) {
     const int c = t / GO, o = t - c * GO;
@@ -321,7 +327,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   for (int i0 = 0; i0 < n; i0 += RC, ++it) {
     const int rows = min(RC, n - i0), npix = rows * n;
     const size_t base = (size_t)i0 * n;
-    T* Vin = VinB + (size_t)(FIRST ? 0 : (it & 1)) * cin * CH;
+    T* Vin = VinB + (size_t)((FIRST || nbuf == 1) ? 0 : (it & 1)) * cin * CH;
     // 1. input rows of every input channel (layer 1: r/||r|| and k converted on the fly)
     if (FIRST) {
       const double* rb = a.r + (size_t)b * N + base;
@@ -330,9 +336,12 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
         Vin[t] = (T)(rb[t] * inv_s);
         Vin[npix + t] = (T)kb[t];
       }
-    } else {
+    } else if (nbuf == 2) {
       if (i0 + RC < n) { stage(i0 + RC, (it + 1) & 1); cp_async_wait<1>(); }
       else cp_async_wait<0>();
+    } else {
+      stage(i0, 0);
+      cp_async_wait<0>();
     }
     // 2. y-synthesis of this layer's spectral term for the rows: Gs[r][k2][o]
     for (int e = threadIdx.x; e < rows * kModes * GO; e += blockDim.x) {
@@ -532,8 +541,9 @@ template <typename T>
 size_t no_max_smem(int n, int w) {
   constexpr int GO = layer_go<T>();
   const size_t lim = (size_t)optin_smem() - 2048;
-  const int rows1 = layer_rows<T>(n, w, false, lim);
-  size_t m = LayerSmem<T, GO>(n, w, rows1, false).total * sizeof(T);
+  int rows1, nbuf1;
+  layer_config<T>(n, w, false, lim, &rows1, &nbuf1);
+  size_t m = LayerSmem<T, GO>(n, w, rows1, nbuf1).total * sizeof(T);
   const size_t msmem = ((size_t)w * w + (size_t)kMixBatch * w) * 2 * sizeof(T);
   return m > msmem ? m : msmem;
 }
@@ -573,8 +583,9 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   T* vbuf[2] = {no.v0, no.v1};
   for (int l = 0; l < 3; ++l) {
     LayerArgs<T> la{};
-    const int rows = layer_rows<T>(n, l == 0 ? 2 : w, l == 0, lim);
-    la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.use_gelu = no.use_gelu;
+    int rows, nbuf;
+    layer_config<T>(n, l == 0 ? 2 : w, l == 0, lim, &rows, &nbuf);
+    la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.nbuf = nbuf; la.use_gelu = no.use_gelu;
     la.r = r; la.rr = rr; la.k = no.k;
     la.ghat = ghat; la.F = F; la.chat = chat; la.status = status;
     la.vout = vbuf[l & 1];
@@ -583,7 +594,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     } else {
       la.cin = w; la.W = pk + no.L.W[l - 1]; la.bias = pk + no.L.b[l - 1]; la.vin = vbuf[(l - 1) & 1];
     }
-    const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, l == 0).total * sizeof(T);
+    const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, nbuf).total * sizeof(T);
     pb(PROF_NO_LAYER);
     if (l == 0) {
       k_no_layer<T, true, GO><<<lgrid, 256, smem, s>>>(la);
