@@ -99,7 +99,7 @@ typedef struct {
 
 /* Kernel classes for in-graph CUDA-event profiling (diagnostics; bench.py). */
 typedef enum {
-  FCGNO_PROF_NO_LAYER = 0,   /* k_no_layer: SNO layers 1-3 (the dominant kernel) */
+  FCGNO_PROF_NO_LAYER = 0,   /* k_no_layer / k_tc_layer: SNO layers 1-3 (the dominant kernel) */
   FCGNO_PROF_NO_MIX = 1,     /* k_mix: mode-diagonal channel mixing (layers 2-4) */
   FCGNO_PROF_NO_OUT = 2,     /* k_no_out: layer 4 + projection + window dots */
   FCGNO_PROF_NO_INPUT = 3,   /* k_dft_rows + k_lift_mix: DFT of r/||r|| and layer-1 mixing */
@@ -108,7 +108,8 @@ typedef enum {
   FCGNO_PROF_STENCIL = 6,    /* k_stencil_dots: s = A p, (p,s), (p,r) */
   FCGNO_PROF_UPDATE = 7,     /* k_update: u, r update, (r,r) */
   FCGNO_PROF_FINALIZE = 8,   /* k_finalize */
-  FCGNO_PROF_NCLASS = 9
+  FCGNO_PROF_NO_YDIR = 9,    /* k_yan + k_ysyn: y-direction DFTs of the tensor-core NO path */
+  FCGNO_PROF_NCLASS = 10
 } fcgno_prof_class;
 
 typedef struct fcgno_problem fcgno_problem;

@@ -9,6 +9,7 @@
 #include <complex>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -90,6 +91,7 @@ ProblemWs carve_problem(Carver& c, int n, int B) {
 template <typename T>
 struct NoWs {
   T *rpart, *v0, *v1, *chat, *ghat;
+  float *G, *Tx;
 };
 template <typename T>
 NoWs<T> carve_no(Carver& c, int n, int B, int w) {
@@ -100,6 +102,10 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
   r.v1 = c.take<T>((size_t)B * w * N);
   r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
   r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
+  if (sizeof(T) == sizeof(float)) {
+    r.G = c.take<float>((size_t)B * n * w * 2 * kModes);
+    r.Tx = c.take<float>((size_t)B * n * w * 2 * kModes);
+  }
   return r;
 }
 
@@ -114,6 +120,16 @@ int check_desc(const fcgno_no_desc& d) {
   return FCGNO_OK;
 }
 
+// FCGNO_TC=0 in the environment forces the FFMA layer kernel (A/B comparisons, fallbacks).
+bool tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FCGNO_TC");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <typename T>
 NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* packed, const NoWs<T>& w,
                     const T* F, const T* khat) {
@@ -122,6 +138,8 @@ NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* 
   no.k = p->k; no.pk = static_cast<const T*>(packed); no.L = no_layout(d.width);
   no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
   no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
+  no.G = w.G; no.Tx = w.Tx;
+  no.tc = (sizeof(T) == sizeof(float)) && tc_enabled() && tc_layer_supported(p->n, d.width);
   return no;
 }
 
@@ -372,6 +390,7 @@ int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, 
     CK(launch_no_forward<double>(no, r, rr, w, nullptr, nullptr, s, nullptr));
   } else {
     CK(prepare_no_kernels<float>());
+    CK(prepare_tc_kernels());
     NoDev<float> no = make_nodev<float>(p, d, packed, w32, p->F32, p->khat32);
     CK(launch_no_forward<float>(no, r, rr, w, nullptr, nullptr, s, nullptr));
   }
@@ -562,7 +581,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
   if (!aligned(ws) || ws_bytes < fcgno_solve_workspace_bytes(g, nd, o)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
   if (nd) {
     if (nd->precision == FCGNO_FP64) CK(prepare_no_kernels<double>());
-    else CK(prepare_no_kernels<float>());
+    else { CK(prepare_no_kernels<float>()); CK(prepare_tc_kernels()); }
   }
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
   Carver c(ws);
@@ -647,7 +666,8 @@ void fcgno_profile_reset(void) { prof_totals() = ProfTotals{}; }
 
 const char* fcgno_profile_name(int cls) {
   static const char* names[PROF_NCLASS] = {"k_no_layer", "k_mix", "k_no_out", "k_dft_rows+k_lift_mix",
-                                           "k_window_dots", "k_pform", "k_stencil_dots", "k_update", "k_finalize"};
+                                           "k_window_dots", "k_pform", "k_stencil_dots", "k_update", "k_finalize",
+                                           "k_yan+k_ysyn"};
   return (cls >= 0 && cls < PROF_NCLASS) ? names[cls] : "";
 }
 

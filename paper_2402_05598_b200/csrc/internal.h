@@ -63,11 +63,28 @@ struct NoDev {
   T* v1;                      // [B][w][N]
   T* chat;                    // [400][B][w] complex
   T* ghat;                    // [B][w][400] complex
+  float* G;                   // [B][n][w][40] y-synthesised spectral term (tensor-core path)
+  float* Tx;                  // [B][n][w][40] x-analysed activations (tensor-core path)
+  int tc;                     // 1: fp32 layers on tcgen05 (no_tc_kernels.cu)
 };
+
+// Tensor-core SNO layer (no_tc_kernels.cu).
+struct TcLayerArgsHost {
+  int n, w, cin, B, use_gelu, first;
+  const double *r, *rr, *k;
+  const float *vin, *W, *bias, *G, *F;
+  float *vout, *T;
+  const int* status;
+};
+bool tc_layer_supported(int n, int w);
+cudaError_t prepare_tc_kernels();
+cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s);
+cudaError_t launch_ysyn(const float* ghat, const float* F, float* G, int n, int w, int B, const int* status, cudaStream_t s);
+cudaError_t launch_yan(const float* T, const float* F, float* chat, int n, int w, int B, const int* status, cudaStream_t s);
 
 // In-graph profiling hook: begin/end record CUDA events around launches of a kernel class.
 enum ProfClass : int { PROF_NO_LAYER = 0, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM,
-                       PROF_STENCIL, PROF_UPDATE, PROF_FINALIZE, PROF_NCLASS };
+                       PROF_STENCIL, PROF_UPDATE, PROF_FINALIZE, PROF_NO_YDIR, PROF_NCLASS };
 struct ProfHook {
   virtual ~ProfHook() = default;
   virtual void begin(int cls, cudaStream_t s) = 0;

@@ -581,28 +581,55 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   const size_t lim = (size_t)optin_smem() - 2048;
   const dim3 lgrid((w + GO - 1) / GO, B);
   T* vbuf[2] = {no.v0, no.v1};
+  bool tc_path = false;
+  if constexpr (sizeof(T) == sizeof(float)) tc_path = no.tc != 0;
+  if (tc_path) {
+    pb(PROF_NO_YDIR);
+    launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.G, n, w, B, status, s);
+    pe(PROF_NO_YDIR);
+    launches += 1;
+  }
   for (int l = 0; l < 3; ++l) {
-    LayerArgs<T> la{};
-    int rows, nbuf;
-    layer_config<T>(n, l == 0 ? 2 : w, l == 0, lim, &rows, &nbuf);
-    la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.nbuf = nbuf; la.use_gelu = no.use_gelu;
-    la.r = r; la.rr = rr; la.k = no.k;
-    la.ghat = ghat; la.F = F; la.chat = chat; la.status = status;
-    la.vout = vbuf[l & 1];
-    if (l == 0) {
-      la.cin = 2; la.W = pk + no.L.W1E; la.bias = pk + no.L.b1; la.vin = nullptr;
+    if (tc_path) {
+      TcLayerArgsHost h{};
+      h.n = n; h.w = w; h.B = B; h.use_gelu = no.use_gelu; h.first = l == 0;
+      h.r = r; h.rr = rr; h.k = no.k;
+      h.cin = l == 0 ? 2 : w;
+      h.W = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.W1E : no.L.W[l - 1]));
+      h.bias = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.b1 : no.L.b[l - 1]));
+      h.vin = l == 0 ? nullptr : reinterpret_cast<const float*>(vbuf[(l - 1) & 1]);
+      h.vout = reinterpret_cast<float*>(vbuf[l & 1]);
+      h.G = no.G; h.T = no.Tx; h.F = reinterpret_cast<const float*>(no.F); h.status = status;
+      pb(PROF_NO_LAYER);
+      launch_tc_layer(h, s);
+      pe(PROF_NO_LAYER);
+      pb(PROF_NO_YDIR);
+      launch_yan(no.Tx, reinterpret_cast<const float*>(no.F), reinterpret_cast<float*>(chat), n, w, B, status, s);
+      pe(PROF_NO_YDIR);
+      launches += 2;
     } else {
-      la.cin = w; la.W = pk + no.L.W[l - 1]; la.bias = pk + no.L.b[l - 1]; la.vin = vbuf[(l - 1) & 1];
+      LayerArgs<T> la{};
+      int rows, nbuf;
+      layer_config<T>(n, l == 0 ? 2 : w, l == 0, lim, &rows, &nbuf);
+      la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.nbuf = nbuf; la.use_gelu = no.use_gelu;
+      la.r = r; la.rr = rr; la.k = no.k;
+      la.ghat = ghat; la.F = F; la.chat = chat; la.status = status;
+      la.vout = vbuf[l & 1];
+      if (l == 0) {
+        la.cin = 2; la.W = pk + no.L.W1E; la.bias = pk + no.L.b1; la.vin = nullptr;
+      } else {
+        la.cin = w; la.W = pk + no.L.W[l - 1]; la.bias = pk + no.L.b[l - 1]; la.vin = vbuf[(l - 1) & 1];
+      }
+      const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, nbuf).total * sizeof(T);
+      pb(PROF_NO_LAYER);
+      if (l == 0) {
+        k_no_layer<T, true, GO><<<lgrid, 256, smem, s>>>(la);
+      } else {
+        k_no_layer<T, false, GO><<<lgrid, 256, smem, s>>>(la);
+      }
+      pe(PROF_NO_LAYER);
+      ++launches;
     }
-    const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, nbuf).total * sizeof(T);
-    pb(PROF_NO_LAYER);
-    if (l == 0) {
-      k_no_layer<T, true, GO><<<lgrid, 256, smem, s>>>(la);
-    } else {
-      k_no_layer<T, false, GO><<<lgrid, 256, smem, s>>>(la);
-    }
-    pe(PROF_NO_LAYER);
-    ++launches;
     // mixing for the next layer (layers 2, 3) or layer 4 folded with the projection (cout = 1)
     const int cout = (l < 2) ? w : 1;
     const T2* Rm = reinterpret_cast<const T2*>(pk + (l < 2 ? no.L.R[l] : no.L.Q));
@@ -612,6 +639,12 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
                                                                                status);
     pe(PROF_NO_MIX);
     ++launches;
+    if (tc_path && l < 2) {
+      pb(PROF_NO_YDIR);
+      launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.G, n, w, B, status, s);
+      pe(PROF_NO_YDIR);
+      ++launches;
+    }
   }
   // 4. layer 4 + projection (+ window dots when inside FCG)
   OutArgs<T> oa{};

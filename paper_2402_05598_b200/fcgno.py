@@ -118,9 +118,9 @@ def abi_version() -> int:
     return int(_lib.fcgno_abi_version())
 
 
-PROF_NCLASS = 9
+PROF_NCLASS = 10
 PROF_NO_LAYER, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM, PROF_STENCIL, PROF_UPDATE, \
-    PROF_FINALIZE = range(PROF_NCLASS)
+    PROF_FINALIZE, PROF_NO_YDIR = range(PROF_NCLASS)
 
 
 def profile_reset() -> None:
@@ -156,8 +156,11 @@ class Problem:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
-            _lib.fcgno_problem_destroy(h)
+        if h is not None and h.value and _lib is not None:
+            try:
+                _lib.fcgno_problem_destroy(h)
+            except (AttributeError, TypeError):   # interpreter shutdown
+                pass
             self._h = None
 
     @property
