@@ -100,7 +100,7 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
   r.rpart = c.take<T>((size_t)B * ngroups_of(n) * kModes2 * 2);
   r.v0 = c.take<T>((size_t)B * w * N);
   r.v1 = c.take<T>((size_t)B * w * N);
-  r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
+  r.chat = c.take<T>((size_t)(sizeof(T) == sizeof(float) ? kMaxYParts : 1) * kModes2 * B * w * 2);
   r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
   if (sizeof(T) == sizeof(float)) {
     r.G = c.take<float>((size_t)B * n * w * 2 * kModes);

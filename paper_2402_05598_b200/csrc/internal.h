@@ -80,7 +80,10 @@ bool tc_layer_supported(int n, int w);
 cudaError_t prepare_tc_kernels();
 cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s);
 cudaError_t launch_ysyn(const float* ghat, const float* F, float* G, int n, int w, int B, const int* status, cudaStream_t s);
-cudaError_t launch_yan(const float* T, const float* F, float* chat, int n, int w, int B, const int* status, cudaStream_t s);
+cudaError_t launch_yan(const float* T, const float* F, float* chat, int n, int w, int B, int nparts, const int* status,
+                       cudaStream_t s);
+int yan_parts(int n, int w, int B);   // row groups of the y-analysis (each writes a partial c)
+constexpr int kMaxYParts = 8;
 
 // In-graph profiling hook: begin/end record CUDA events around launches of a kernel class.
 enum ProfClass : int { PROF_NO_LAYER = 0, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM,

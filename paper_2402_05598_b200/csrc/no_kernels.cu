@@ -27,7 +27,7 @@ __device__ __forceinline__ double gelu_t(double x) { return 0.5 * x * (1.0 + erf
 
 constexpr int kDftRows = 8;      // rows per CTA of k_dft_rows
 constexpr int kGhStride = kModes2 + 1;  // padded row of the per-channel mode array in smem
-constexpr int kMixBatch = 16;    // systems per CTA of k_mix
+constexpr int kMixBatch = 32;    // systems per CTA of k_mix
 constexpr int kMaxDynSmem = 227 * 1024;
 
 // ------------------------------------------------------------------ twiddles
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
                                                   typename Cplx<T>::type* __restrict__ ghat, int w, T n2, T inv_n2,
                                                   const int* __restrict__ status) {
   using T2 = typename Cplx<T>::type;
-  const int b = blockIdx.x;
+  const int b = blockIdx.x, ochunk = blockIdx.y;   // 8 output channels per CTA
   if (status && status[b] != SYS_RUNNING) return;
   __shared__ T2 Rh[kModes2];
   for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
@@ -148,8 +148,9 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
   }
   __syncthreads();
   const int k0 = (kModes / 2) * kModes + kModes / 2;   // kappa = (0, 0)
-  for (int e = threadIdx.x; e < w * kModes2; e += blockDim.x) {
-    const int o = e / kModes2, kk = e - o * kModes2;
+  const int olo = ochunk * 8, ohi = min(w, olo + 8);
+  for (int e = threadIdx.x; e < (ohi - olo) * kModes2; e += blockDim.x) {
+    const int o = olo + e / kModes2, kk = e % kModes2;
     const T2 a0 = A0[(size_t)kk * w + o], a1 = A1[(size_t)kk * w + o];
     const T2 rh = Rh[kk], kh = khat[(size_t)b * kModes2 + kk];
     T gr = a0.x * rh.x - a0.y * rh.y + a1.x * kh.x - a1.y * kh.y;
@@ -160,12 +161,14 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
 }
 
 // ------------------------------------------------------------------ mode-diagonal mixing
-// grid (400, ceil(B / kMixBatch)).  chat [400][B][cin], R [400][cin][cout], ghat [B][cout][400].
+// grid (400, ceil(B / kMixBatch)).  chat [nparts][400][B][cin] (partial analyses summed here in a
+// fixed order), R [400][cin][cout], ghat [B][cout][400].  Each thread owns 2 systems x 2 output
+// channels, so every shared-memory read feeds two complex multiply-adds.
 template <typename T>
 __global__ void __launch_bounds__(256) k_mix(const typename Cplx<T>::type* __restrict__ chat,
                                              const typename Cplx<T>::type* __restrict__ R,
                                              typename Cplx<T>::type* __restrict__ ghat, int B, int cin, int cout,
-                                             T inv_n2, const int* __restrict__ status) {
+                                             T inv_n2, const int* __restrict__ status, int nparts) {
   using T2 = typename Cplx<T>::type;
   extern __shared__ __align__(16) unsigned char smraw[];
   T2* Rs = reinterpret_cast<T2*>(smraw);             // [cin][cout]
@@ -173,19 +176,39 @@ __global__ void __launch_bounds__(256) k_mix(const typename Cplx<T>::type* __res
   const int kk = blockIdx.x, b0 = blockIdx.y * kMixBatch, nb = min(kMixBatch, B - b0);
   const T2* Rk = R + (size_t)kk * cin * cout;
   for (int t = threadIdx.x; t < cin * cout; t += blockDim.x) Rs[t] = Rk[t];
-  const T2* Ck = chat + ((size_t)kk * B + b0) * cin;
-  for (int t = threadIdx.x; t < nb * cin; t += blockDim.x) Cs[t] = Ck[t];
-  __syncthreads();
-  for (int e = threadIdx.x; e < nb * cout; e += blockDim.x) {
-    const int bb = e / cout, o = e - bb * cout;
-    if (status && status[b0 + bb] != SYS_RUNNING) continue;
+  for (int t = threadIdx.x; t < nb * cin; t += blockDim.x) {
     T ar = 0, ai = 0;
-    for (int c = 0; c < cin; ++c) {
-      const T2 rv = Rs[c * cout + o], cv = Cs[bb * cin + c];
-      ar += rv.x * cv.x - rv.y * cv.y;
-      ai += rv.x * cv.y + rv.y * cv.x;
+    for (int p = 0; p < nparts; ++p) {
+      const T2 v = chat[(((size_t)p * kModes2 + kk) * B + b0) * cin + t];
+      ar += v.x; ai += v.y;
     }
-    ghat[((size_t)(b0 + bb) * cout + o) * kModes2 + kk] = T2{ar * inv_n2, ai * inv_n2};
+    Cs[t] = T2{ar, ai};
+  }
+  __syncthreads();
+  const int ob = (cout + 1) / 2, bbn = (nb + 1) / 2;
+  for (int e = threadIdx.x; e < bbn * ob; e += blockDim.x) {
+    const int o = (e % ob) * 2, bb = (e / ob) * 2;
+    const bool o1 = o + 1 < cout, b1 = bb + 1 < nb;
+    T a00r = 0, a00i = 0, a01r = 0, a01i = 0, a10r = 0, a10i = 0, a11r = 0, a11i = 0;
+    for (int c = 0; c < cin; ++c) {
+      const T2 r0 = Rs[c * cout + o], r1 = o1 ? Rs[c * cout + o + 1] : T2{T(0), T(0)};
+      const T2 c0 = Cs[bb * cin + c], c1 = b1 ? Cs[(bb + 1) * cin + c] : T2{T(0), T(0)};
+      a00r += r0.x * c0.x - r0.y * c0.y;  a00i += r0.x * c0.y + r0.y * c0.x;
+      a01r += r1.x * c0.x - r1.y * c0.y;  a01i += r1.x * c0.y + r1.y * c0.x;
+      a10r += r0.x * c1.x - r0.y * c1.y;  a10i += r0.x * c1.y + r0.y * c1.x;
+      a11r += r1.x * c1.x - r1.y * c1.y;  a11i += r1.x * c1.y + r1.y * c1.x;
+    }
+    const int g0 = b0 + bb;
+    const bool run0 = !status || status[g0] == SYS_RUNNING;
+    const bool run1 = b1 && (!status || status[g0 + 1] == SYS_RUNNING);
+    if (run0) {
+      ghat[((size_t)g0 * cout + o) * kModes2 + kk] = T2{a00r * inv_n2, a00i * inv_n2};
+      if (o1) ghat[((size_t)g0 * cout + o + 1) * kModes2 + kk] = T2{a01r * inv_n2, a01i * inv_n2};
+    }
+    if (run1) {
+      ghat[((size_t)(g0 + 1) * cout + o) * kModes2 + kk] = T2{a10r * inv_n2, a10i * inv_n2};
+      if (o1) ghat[((size_t)(g0 + 1) * cout + o + 1) * kModes2 + kk] = T2{a11r * inv_n2, a11i * inv_n2};
+    }
   }
 }
 
@@ -473,6 +496,25 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
   __syncthreads();
   const double s = sqrt(a.rr[b]);
   const T cst = a.cst[0];
+  T acc[kPerThread];
+  const T* vb = a.vin + (size_t)b * w * N;
+#pragma unroll
+  for (int q = 0; q < kPerThread; ++q) acc[q] = cst;
+  // bypass: 8 channels x 4 pixels of independent loads in flight
+  for (int c0 = 0; c0 < w; c0 += 8) {
+    T x[8][kPerThread];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc)
+#pragma unroll
+      for (int q = 0; q < kPerThread; ++q) {
+        const int e = e0 + q * kThreads + threadIdx.x;
+        x[cc][q] = (c0 + cc < w && e < N) ? __ldg(vb + (size_t)(c0 + cc) * N + e) : T(0);
+      }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc)
+#pragma unroll
+      for (int q = 0; q < kPerThread; ++q) acc[q] += (c0 + cc < w ? dws[c0 + cc] : T(0)) * x[cc][q];
+  }
   double wv[kPerThread];
 #pragma unroll
   for (int q = 0; q < kPerThread; ++q) {
@@ -480,15 +522,14 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
     wv[q] = 0.0;
     if (e < N) {
       const int i = e / n, j = e - i * n;
-      T acc = cst;
-      const T* vb = a.vin + (size_t)b * w * N + e;
-      for (int c = 0; c < w; ++c) acc += dws[c] * vb[(size_t)c * N];
+      T z = acc[q];
       const T2* Gr = Gs + (size_t)(i - rlo) * kModes;
+#pragma unroll 4
       for (int k2 = 0; k2 < kModes; ++k2) {
         const T2 f = __ldg(a.F + (size_t)j * kModes + k2);
-        acc += Gr[k2].x * f.x + Gr[k2].y * f.y;
+        z += Gr[k2].x * f.x + Gr[k2].y * f.y;
       }
-      wv[q] = s * (double)acc;
+      wv[q] = s * (double)z;
       a.wout[(size_t)b * N + e] = wv[q];
     }
   }
@@ -571,7 +612,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       r, rr, F, reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status);
   ++launches;
   // 2. layer-1 mixing with the lift folded in
-  k_lift_mix<T><<<B, 256, 0, s>>>(reinterpret_cast<const T2*>(no.rpart), no.ngroups,
+  k_lift_mix<T><<<dim3(B, (w + 7) / 8), 256, 0, s>>>(reinterpret_cast<const T2*>(no.rpart), no.ngroups,
                                   reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
                                   reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2),
                                   ghat, w, n2, inv_n2, status);
@@ -583,6 +624,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   T* vbuf[2] = {no.v0, no.v1};
   bool tc_path = false;
   if constexpr (sizeof(T) == sizeof(float)) tc_path = no.tc != 0;
+  const int ypart = tc_path ? yan_parts(n, w, B) : 1;   // row groups of the y-analysis (partials summed by k_mix)
   if (tc_path) {
     pb(PROF_NO_YDIR);
     launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.G, n, w, B, status, s);
@@ -604,7 +646,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       launch_tc_layer(h, s);
       pe(PROF_NO_LAYER);
       pb(PROF_NO_YDIR);
-      launch_yan(no.Tx, reinterpret_cast<const float*>(no.F), reinterpret_cast<float*>(chat), n, w, B, status, s);
+      launch_yan(no.Tx, reinterpret_cast<const float*>(no.F), reinterpret_cast<float*>(chat), n, w, B, ypart, status, s);
       pe(PROF_NO_YDIR);
       launches += 2;
     } else {
@@ -636,7 +678,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     const size_t msmem = ((size_t)w * cout + (size_t)kMixBatch * w) * sizeof(T2);
     pb(PROF_NO_MIX);
     k_mix<T><<<dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), 256, msmem, s>>>(chat, Rm, ghat, B, w, cout, inv_n2,
-                                                                               status);
+                                                                               status, tc_path ? ypart : 1);
     pe(PROF_NO_MIX);
     ++launches;
     if (tc_path && l < 2) {
