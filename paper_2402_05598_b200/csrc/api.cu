@@ -16,6 +16,7 @@
 
 #include "../../include/fcgno.h"
 #include "internal.h"
+#include "tc_layout.cuh"
 
 using namespace fcgno;
 
@@ -88,10 +89,18 @@ ProblemWs carve_problem(Carver& c, int n, int B) {
   return w;
 }
 
+// Shapes the tensor-core NO path handles (device smem is re-checked at launch time).
+bool tc_layer_supported_host(int n, int w) {
+  if (w > 128 || w < 1 || n % 16 != 0 || n < 64 || n > 128) return false;
+  const TcGeom g(n, w);
+  return n % g.R == 0;
+}
+
 template <typename T>
 struct NoWs {
   T *rpart, *v0, *v1, *chat, *ghat;
-  float *G, *Tx;
+  unsigned char *vb0, *vb1, *Gb, *Tb;   // tensor-core path blobs (fp32 NO only)
+  size_t vb_bytes, gb_bytes;
 };
 template <typename T>
 NoWs<T> carve_no(Carver& c, int n, int B, int w) {
@@ -100,11 +109,16 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
   r.rpart = c.take<T>((size_t)B * ngroups_of(n) * kModes2 * 2);
   r.v0 = c.take<T>((size_t)B * w * N);
   r.v1 = c.take<T>((size_t)B * w * N);
-  r.chat = c.take<T>((size_t)(sizeof(T) == sizeof(float) ? kMaxYParts : 1) * kModes2 * B * w * 2);
+  r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
   r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
-  if (sizeof(T) == sizeof(float)) {
-    r.G = c.take<float>((size_t)B * n * w * 2 * kModes);
-    r.Tx = c.take<float>((size_t)B * n * w * 2 * kModes);
+  if (sizeof(T) == sizeof(float) && tc_layer_supported_host(n, w)) {
+    const TcGeom g(n, w);
+    r.vb_bytes = g.v_bytes_total(B);
+    r.gb_bytes = g.g_bytes_total(B);
+    r.vb0 = c.take<unsigned char>(r.vb_bytes);
+    r.vb1 = c.take<unsigned char>(r.vb_bytes);
+    r.Gb = c.take<unsigned char>(r.gb_bytes);
+    r.Tb = c.take<unsigned char>(g.t_bytes_total(B));
   }
   return r;
 }
@@ -138,8 +152,8 @@ NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* 
   no.k = p->k; no.pk = static_cast<const T*>(packed); no.L = no_layout(d.width);
   no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
   no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
-  no.G = w.G; no.Tx = w.Tx;
-  no.tc = (sizeof(T) == sizeof(float)) && tc_enabled() && tc_layer_supported(p->n, d.width);
+  no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb;
+  no.tc = (sizeof(T) == sizeof(float)) && w.Gb != nullptr && tc_enabled() && tc_layer_supported(p->n, d.width);
   return no;
 }
 
@@ -383,6 +397,11 @@ int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, 
   NoWs<float> w32{}; NoWs<double> w64{};
   carve_no_any(c, p->n, p->B, d, &w32, &w64);
   CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * p->B, s));
+  if (w32.Gb) {   // blob padding (channels >= w, modes 40..47, K rows >= R*CP) must read as zeros
+    CK(cudaMemsetAsync(w32.vb0, 0, w32.vb_bytes, s));
+    CK(cudaMemsetAsync(w32.vb1, 0, w32.vb_bytes, s));
+    CK(cudaMemsetAsync(w32.Gb, 0, w32.gb_bytes, s));
+  }
   CK(launch_dot(r, r, rr, part, cnt, p->n, p->B, s));
   if (d.precision == FCGNO_FP64) {
     CK(prepare_no_kernels<double>());
@@ -611,6 +630,11 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     cudaError_t e;
     if ((e = cudaMemsetAsync(d.cnt, 0, sizeof(unsigned) * 3 * d.B, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
     if ((e = cudaMemsetAsync(d.iter, 0, 2 * sizeof(int), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+    if (nd && sw.n32.Gb) {   // blob padding must read as zeros
+      if ((e = cudaMemsetAsync(sw.n32.vb0, 0, sw.n32.vb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+      if ((e = cudaMemsetAsync(sw.n32.vb1, 0, sw.n32.vb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+      if ((e = cudaMemsetAsync(sw.n32.Gb, 0, sw.n32.gb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+    }
     if ((e = launch_init_residual(d, s)) != cudaSuccess) { rc = cuda_fail(e, "init_residual"); break; }
     if (o.maxit == 0) break;
     const int chunk = std::min(o.check_every > 0 ? o.check_every : 16, o.maxit);

@@ -63,8 +63,10 @@ struct NoDev {
   T* v1;                      // [B][w][N]
   T* chat;                    // [400][B][w] complex
   T* ghat;                    // [B][w][400] complex
-  float* G;                   // [B][n][w][40] y-synthesised spectral term (tensor-core path)
-  float* Tx;                  // [B][n][w][40] x-analysed activations (tensor-core path)
+  unsigned char* vb0;         // tensor-core path: activation blobs (ping-pong), tc_layout.cuh
+  unsigned char* vb1;
+  unsigned char* Gb;          // G blobs (y-synthesised spectral term)
+  unsigned char* Tb;          // T blobs (x-analysed activations)
   int tc;                     // 1: fp32 layers on tcgen05 (no_tc_kernels.cu)
 };
 
@@ -72,18 +74,20 @@ struct NoDev {
 struct TcLayerArgsHost {
   int n, w, cin, B, use_gelu, first;
   const double *r, *rr, *k;
-  const float *vin, *W, *bias, *G, *F;
-  float *vout, *T;
+  const unsigned char* vin;
+  const float *W, *bias;
+  const unsigned char* G;
+  const float* F;
+  unsigned char *vout, *T;
   const int* status;
 };
 bool tc_layer_supported(int n, int w);
 cudaError_t prepare_tc_kernels();
 cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s);
-cudaError_t launch_ysyn(const float* ghat, const float* F, float* G, int n, int w, int B, const int* status, cudaStream_t s);
-cudaError_t launch_yan(const float* T, const float* F, float* chat, int n, int w, int B, int nparts, const int* status,
+cudaError_t launch_ysyn(const float* ghat, const float* F, unsigned char* Gb, int n, int w, int B, const int* status,
+                        cudaStream_t s);
+cudaError_t launch_yan(const unsigned char* Tb, const float* F, float* chat, int n, int w, int B, const int* status,
                        cudaStream_t s);
-int yan_parts(int n, int w, int B);   // row groups of the y-analysis (each writes a partial c)
-constexpr int kMaxYParts = 8;
 
 // In-graph profiling hook: begin/end record CUDA events around launches of a kernel class.
 enum ProfClass : int { PROF_NO_LAYER = 0, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM,

@@ -15,6 +15,8 @@
 
 #include "internal.h"
 #include "fcg_device.cuh"
+#include "tc_layout.cuh"
+#include "tc_common.cuh"
 
 namespace fcgno {
 
@@ -457,6 +459,7 @@ template <typename T>
 struct OutArgs {
   int n, N, w, use_dots;
   const T* vin;                                   // [B][w][N]
+  const unsigned char* vblob;                     // tensor-core path: layer-3 activation blobs
   const T* dw;                                    // [w]
   const T* cst;                                   // [1]
   const typename Cplx<T>::type* gh4;              // [B][400] scaled by n^-2
@@ -540,6 +543,97 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
   }
 }
 
+// Tensor-core path variant: layer-3 activations come as bf16 hi/lo blobs (tc_layout.cuh).
+// Phase 1: 128 groups of 8 consecutive pixels x 2 channel halves accumulate dw . (hi + lo) with
+// 16-byte loads into shared memory; phase 2 is k_no_out's per-pixel synthesis + window dots.
+__global__ void __launch_bounds__(kThreads) k_no_out_blob(const OutArgs<float> a, const FcgDev d) {
+  const int b = blockIdx.y, blk = blockIdx.x;
+  if (a.status && a.status[b] != SYS_RUNNING) return;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  float2* gh = reinterpret_cast<float2*>(smraw);
+  const int n = a.n, N = a.N, w = a.w;
+  const int e0 = blk * kTile;
+  const int rlo = e0 / n, rhi = min(n - 1, (e0 + kTile - 1) / n), nr = rhi - rlo + 1;
+  const int nr_max = kTile / n + 2;
+  float2* Gs = gh + kModes2;
+  float* dws = reinterpret_cast<float*>(Gs + (size_t)nr_max * kModes);
+  float* outs = dws + ((w + 3) & ~3);
+  const TcGeom g(n, w);
+  for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)b * kModes2 + t];
+  for (int t = threadIdx.x; t < w; t += blockDim.x) dws[t] = a.dw[t];
+  __syncthreads();
+  // phase 1: bypass dot products from the blob
+  {
+    const int grp = threadIdx.x >> 1, half = threadIdx.x & 1;   // 128 groups of 8 pixels
+    const int p0 = e0 + grp * 8;
+    float acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+    if (p0 < N) {
+      const int i = p0 / n, j = p0 - i * n;
+      const unsigned char* vb = a.vblob + ((size_t)b * g.tiles_per_sys + i / g.R) * 2 * g.v_half();
+      const int r = i % g.R;
+      const int chalf = (w + 1) / 2, clo = half * chalf, chi = min(w, clo + chalf);
+      for (int c = clo; c < chi; ++c) {
+        const uint32_t off = tc::mnmajor_off(j, (uint32_t)(r * g.CP + c), g.v_sbo(), 128);
+        const uint4 h = __ldg(reinterpret_cast<const uint4*>(vb + off));
+        const uint4 l = __ldg(reinterpret_cast<const uint4*>(vb + g.v_half() + off));
+        const float wc = dws[c];
+        const uint32_t hh[4] = {h.x, h.y, h.z, h.w}, ll[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          acc[2 * q] += wc * (tc::bf16pair_lo(hh[q]) + tc::bf16pair_lo(ll[q]));
+          acc[2 * q + 1] += wc * (tc::bf16pair_hi(hh[q]) + tc::bf16pair_hi(ll[q]));
+        }
+      }
+    }
+    if (half == 1)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) outs[grp * 8 + q] = acc[q];
+    __syncthreads();
+    if (half == 0)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) outs[grp * 8 + q] += acc[q];
+  }
+  for (int e = threadIdx.x; e < nr * kModes; e += blockDim.x) {
+    const int r = e / kModes, k2 = e - r * kModes;
+    float gr = 0, gi = 0;
+    for (int k1 = 0; k1 < kModes; ++k1) {
+      const float2 gg = gh[k1 * kModes + k2];
+      const float2 f = __ldg(a.F + (size_t)(rlo + r) * kModes + k1);
+      gr += gg.x * f.x + gg.y * f.y;
+      gi += gg.y * f.x - gg.x * f.y;
+    }
+    Gs[e] = make_float2(gr, gi);
+  }
+  __syncthreads();
+  const double s = sqrt(a.rr[b]);
+  const float cst = a.cst[0];
+  double wv[kPerThread];
+#pragma unroll
+  for (int q = 0; q < kPerThread; ++q) {
+    const int e = e0 + q * kThreads + threadIdx.x;
+    wv[q] = 0.0;
+    if (e < N) {
+      const int i = e / n, j = e - i * n;
+      float z = cst + outs[e - e0];
+      const float2* Gr = Gs + (size_t)(i - rlo) * kModes;
+#pragma unroll 4
+      for (int k2 = 0; k2 < kModes; ++k2) {
+        const float2 f = __ldg(a.F + (size_t)j * kModes + k2);
+        z += Gr[k2].x * f.x + Gr[k2].y * f.y;
+      }
+      wv[q] = s * (double)z;
+      a.wout[(size_t)b * N + e] = wv[q];
+    }
+  }
+  if (a.use_dots) {
+    const int i = *d.iter;
+    const int mi = m_schedule(i, d.m, d.schedule);
+    if (mi > 0) window_dots_beta(d, b, blk, i, mi, wv);
+  }
+}
+
 // ------------------------------------------------------------------ launcher
 // Largest dynamic shared memory a CTA may request on this device (opt-in limit).
 static int optin_smem() {
@@ -570,6 +664,7 @@ cudaError_t prepare_no_kernels() {
   if ((e = set_smem((const void*)k_no_layer<T, false, GO>)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_mix<T>)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_no_out<T>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_no_out_blob)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_dft_rows<T, true>)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_dft_rows<T, false>)) != cudaSuccess) return e;
   done = true;
@@ -624,13 +719,13 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   T* vbuf[2] = {no.v0, no.v1};
   bool tc_path = false;
   if constexpr (sizeof(T) == sizeof(float)) tc_path = no.tc != 0;
-  const int ypart = tc_path ? yan_parts(n, w, B) : 1;   // row groups of the y-analysis (partials summed by k_mix)
   if (tc_path) {
     pb(PROF_NO_YDIR);
-    launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.G, n, w, B, status, s);
+    launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.Gb, n, w, B, status, s);
     pe(PROF_NO_YDIR);
     launches += 1;
   }
+  unsigned char* vblob[2] = {no.vb0, no.vb1};
   for (int l = 0; l < 3; ++l) {
     if (tc_path) {
       TcLayerArgsHost h{};
@@ -639,14 +734,14 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       h.cin = l == 0 ? 2 : w;
       h.W = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.W1E : no.L.W[l - 1]));
       h.bias = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.b1 : no.L.b[l - 1]));
-      h.vin = l == 0 ? nullptr : reinterpret_cast<const float*>(vbuf[(l - 1) & 1]);
-      h.vout = reinterpret_cast<float*>(vbuf[l & 1]);
-      h.G = no.G; h.T = no.Tx; h.F = reinterpret_cast<const float*>(no.F); h.status = status;
+      h.vin = l == 0 ? nullptr : vblob[(l - 1) & 1];
+      h.vout = vblob[l & 1];
+      h.G = no.Gb; h.T = no.Tb; h.F = reinterpret_cast<const float*>(no.F); h.status = status;
       pb(PROF_NO_LAYER);
       launch_tc_layer(h, s);
       pe(PROF_NO_LAYER);
       pb(PROF_NO_YDIR);
-      launch_yan(no.Tx, reinterpret_cast<const float*>(no.F), reinterpret_cast<float*>(chat), n, w, B, ypart, status, s);
+      launch_yan(no.Tb, reinterpret_cast<const float*>(no.F), reinterpret_cast<float*>(chat), n, w, B, status, s);
       pe(PROF_NO_YDIR);
       launches += 2;
     } else {
@@ -678,12 +773,12 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     const size_t msmem = ((size_t)w * cout + (size_t)kMixBatch * w) * sizeof(T2);
     pb(PROF_NO_MIX);
     k_mix<T><<<dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), 256, msmem, s>>>(chat, Rm, ghat, B, w, cout, inv_n2,
-                                                                               status, tc_path ? ypart : 1);
+                                                                               status, 1);
     pe(PROF_NO_MIX);
     ++launches;
     if (tc_path && l < 2) {
       pb(PROF_NO_YDIR);
-      launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.G, n, w, B, status, s);
+      launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.Gb, n, w, B, status, s);
       pe(PROF_NO_YDIR);
       ++launches;
     }
@@ -696,10 +791,19 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   oa.gh4 = ghat; oa.F = F; oa.rr = rr; oa.wout = wout; oa.status = status;
   const int nblk = (N + kTile - 1) / kTile;
   const int nr_max = kTile / n + 2;
-  const size_t osmem = (size_t)(kModes2 + (size_t)nr_max * kModes) * sizeof(T2) + (size_t)w * sizeof(T);
+  const size_t osmem = (size_t)(kModes2 + (size_t)nr_max * kModes) * sizeof(T2) + (size_t)((w + 3) & ~3) * sizeof(T);
   FcgDev dummy{};
   pb(PROF_NO_OUT);
-  k_no_out<T><<<dim3(nblk, B), kThreads, osmem, s>>>(oa, fcg ? *fcg : dummy);
+  if constexpr (sizeof(T) == sizeof(float)) {
+    if (tc_path) {
+      oa.vblob = vblob[0];   // layer 3 wrote vblob[2 & 1]
+      k_no_out_blob<<<dim3(nblk, B), kThreads, osmem + kTile * sizeof(float), s>>>(oa, fcg ? *fcg : dummy);
+    } else {
+      k_no_out<T><<<dim3(nblk, B), kThreads, osmem, s>>>(oa, fcg ? *fcg : dummy);
+    }
+  } else {
+    k_no_out<T><<<dim3(nblk, B), kThreads, osmem, s>>>(oa, fcg ? *fcg : dummy);
+  }
   pe(PROF_NO_OUT);
   ++launches;
   launch_counter() += launches;
