@@ -99,7 +99,7 @@ bool tc_layer_supported_host(int n, int w) {
 template <typename T>
 struct NoWs {
   T *rpart, *v0, *v1, *chat, *ghat;
-  unsigned char *vb0, *vb1, *Gb, *Tb;   // tensor-core path blobs (fp32 NO only)
+  unsigned char *vb0, *vb1, *Gb, *Tb, *cst;   // tensor-core path blobs (fp32 NO only)
   size_t vb_bytes, gb_bytes;
 };
 template <typename T>
@@ -119,6 +119,7 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
     r.vb1 = c.take<unsigned char>(r.vb_bytes);
     r.Gb = c.take<unsigned char>(r.gb_bytes);
     r.Tb = c.take<unsigned char>(g.t_bytes_total(B));
+    r.cst = c.take<unsigned char>(tc_const_bytes(n, w));
   }
   return r;
 }
@@ -152,7 +153,7 @@ NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* 
   no.k = p->k; no.pk = static_cast<const T*>(packed); no.L = no_layout(d.width);
   no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
   no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
-  no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb;
+  no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb; no.cst = w.cst;
   no.tc = (sizeof(T) == sizeof(float)) && w.Gb != nullptr && tc_enabled() && tc_layer_supported(p->n, d.width);
   return no;
 }
@@ -411,6 +412,7 @@ int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, 
     CK(prepare_no_kernels<float>());
     CK(prepare_tc_kernels());
     NoDev<float> no = make_nodev<float>(p, d, packed, w32, p->F32, p->khat32);
+    CK(prepare_no_constants(no, s));
     CK(launch_no_forward<float>(no, r, rr, w, nullptr, nullptr, s, nullptr));
   }
   return FCGNO_OK;
@@ -634,6 +636,8 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
       if ((e = cudaMemsetAsync(sw.n32.vb0, 0, sw.n32.vb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if ((e = cudaMemsetAsync(sw.n32.vb1, 0, sw.n32.vb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if ((e = cudaMemsetAsync(sw.n32.Gb, 0, sw.n32.gb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+      NoDev<float> no = make_nodev<float>(p, *nd, packed, sw.n32, p->F32, p->khat32);
+      if ((e = prepare_no_constants(no, s)) != cudaSuccess) { rc = cuda_fail(e, "tc constants"); break; }
     }
     if ((e = launch_init_residual(d, s)) != cudaSuccess) { rc = cuda_fail(e, "init_residual"); break; }
     if (o.maxit == 0) break;

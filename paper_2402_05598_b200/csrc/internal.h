@@ -67,27 +67,31 @@ struct NoDev {
   unsigned char* vb1;
   unsigned char* Gb;          // G blobs (y-synthesised spectral term)
   unsigned char* Tb;          // T blobs (x-analysed activations)
+  unsigned char* cst;         // constant operand blobs (twiddles, block-diagonal weights)
   int tc;                     // 1: fp32 layers on tcgen05 (no_tc_kernels.cu)
 };
 
 // Tensor-core SNO layer (no_tc_kernels.cu).
 struct TcLayerArgsHost {
-  int n, w, cin, B, use_gelu, first;
+  int n, w, cin, B, use_gelu, first, layer;
   const double *r, *rr, *k;
   const unsigned char* vin;
   const float *W, *bias;
   const unsigned char* G;
-  const float* F;
+  const unsigned char* cst;   // constant operand blobs (launch_tc_prep)
   unsigned char *vout, *T;
   const int* status;
 };
 bool tc_layer_supported(int n, int w);
 cudaError_t prepare_tc_kernels();
 cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s);
-cudaError_t launch_ysyn(const float* ghat, const float* F, unsigned char* Gb, int n, int w, int B, const int* status,
-                        cudaStream_t s);
-cudaError_t launch_yan(const unsigned char* Tb, const float* F, float* chat, int n, int w, int B, const int* status,
-                       cudaStream_t s);
+cudaError_t launch_ysyn(const float* ghat, const unsigned char* cst, unsigned char* Gb, int n, int w, int B,
+                        const int* status, cudaStream_t s);
+cudaError_t launch_yan(const unsigned char* Tb, const unsigned char* cst, float* chat, int n, int w, int B,
+                       const int* status, cudaStream_t s);
+size_t tc_const_bytes(int n, int w);
+cudaError_t launch_tc_prep(int n, int w, const float* W1, const float* W2, const float* W3, const float* F,
+                           unsigned char* out, cudaStream_t s);
 
 // In-graph profiling hook: begin/end record CUDA events around launches of a kernel class.
 enum ProfClass : int { PROF_NO_LAYER = 0, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM,
@@ -122,6 +126,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
                               ProfHook* prof = nullptr);
 template <typename T>
 cudaError_t prepare_no_kernels();
+cudaError_t prepare_no_constants(const NoDev<float>& no, cudaStream_t s);
 template <typename T>
 size_t no_max_smem(int n, int w);   // largest dynamic smem any NO kernel needs for (n, w)
 

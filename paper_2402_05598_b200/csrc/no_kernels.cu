@@ -721,7 +721,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   if constexpr (sizeof(T) == sizeof(float)) tc_path = no.tc != 0;
   if (tc_path) {
     pb(PROF_NO_YDIR);
-    launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.Gb, n, w, B, status, s);
+    launch_ysyn(reinterpret_cast<const float*>(ghat), no.cst, no.Gb, n, w, B, status, s);
     pe(PROF_NO_YDIR);
     launches += 1;
   }
@@ -732,16 +732,18 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       h.n = n; h.w = w; h.B = B; h.use_gelu = no.use_gelu; h.first = l == 0;
       h.r = r; h.rr = rr; h.k = no.k;
       h.cin = l == 0 ? 2 : w;
+      h.layer = l;
+      h.cst = no.cst;
       h.W = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.W1E : no.L.W[l - 1]));
       h.bias = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.b1 : no.L.b[l - 1]));
       h.vin = l == 0 ? nullptr : vblob[(l - 1) & 1];
       h.vout = vblob[l & 1];
-      h.G = no.Gb; h.T = no.Tb; h.F = reinterpret_cast<const float*>(no.F); h.status = status;
+      h.G = no.Gb; h.T = no.Tb; h.status = status;
       pb(PROF_NO_LAYER);
       launch_tc_layer(h, s);
       pe(PROF_NO_LAYER);
       pb(PROF_NO_YDIR);
-      launch_yan(no.Tb, reinterpret_cast<const float*>(no.F), reinterpret_cast<float*>(chat), n, w, B, status, s);
+      launch_yan(no.Tb, no.cst, reinterpret_cast<float*>(chat), n, w, B, status, s);
       pe(PROF_NO_YDIR);
       launches += 2;
     } else {
@@ -778,7 +780,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     ++launches;
     if (tc_path && l < 2) {
       pb(PROF_NO_YDIR);
-      launch_ysyn(reinterpret_cast<const float*>(ghat), reinterpret_cast<const float*>(no.F), no.Gb, n, w, B, status, s);
+      launch_ysyn(reinterpret_cast<const float*>(ghat), no.cst, no.Gb, n, w, B, status, s);
       pe(PROF_NO_YDIR);
       ++launches;
     }
@@ -809,6 +811,13 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   launch_counter() += launches;
   if (nlaunch) *nlaunch = launches;
   return cudaGetLastError();
+}
+
+// Constant operand blobs of the tensor-core path (once per apply / solve, outside graphs).
+cudaError_t prepare_no_constants(const NoDev<float>& no, cudaStream_t s) {
+  if (!no.tc) return cudaSuccess;
+  const float* pk = no.pk;
+  return launch_tc_prep(no.n, no.w, pk + no.L.W1E, pk + no.L.W[0], pk + no.L.W[1], no.F, no.cst, s);
 }
 
 template cudaError_t launch_no_forward<float>(const NoDev<float>&, const double*, const double*, double*,

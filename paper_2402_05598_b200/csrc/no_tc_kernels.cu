@@ -49,35 +49,131 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[8]) {
                : "r"(taddr));
 }
 
+// ------------------------------------------------------------------ constant operand blobs
+// Built once per NO apply / solve by k_tc_prep (outside the iteration graph) and bulk-copied by
+// every persistent CTA: twiddles for the x-direction (BF), the block-diagonal layer weights (AW),
+// the y-synthesis twiddles (FP) and the y-analysis twiddles (AP), each as [hi][lo] bf16.
+struct TcConst {
+  size_t BF, AW[3], FP, AP, total;
+  uint32_t bf_half, aw_half[3], fp_half, ap_half;
+  int KB[3];
+  __host__ __device__ TcConst(const TcGeom& g) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 1023) & ~size_t(1023); return at; };
+    bf_half = (uint32_t)g.n * kKS * 2;
+    BF = take(2 * (size_t)bf_half);
+    for (int l = 0; l < 3; ++l) {
+      const int cin = l == 0 ? 2 : g.w, CP = (cin + 7) & ~7;
+      KB[l] = (g.R * CP + 15) & ~15;
+      aw_half[l] = 128u * KB[l] * 2;
+      AW[l] = take(2 * (size_t)aw_half[l]);
+    }
+    fp_half = 128u * kKS * 2;
+    FP = take(2 * (size_t)fp_half);
+    ap_half = (uint32_t)kKS * (2 * g.n) * 2;
+    AP = take(2 * (size_t)ap_half);
+    total = o;
+  }
+};
+
+struct TcPrepArgs {
+  int n, w;
+  const float* W[3];      // layer weights [w][cin] (layer 1: W1E [w][2])
+  const float2* F;        // [n][20]
+  unsigned char* out;
+};
+
+__global__ void __launch_bounds__(256) k_tc_prep(const TcPrepArgs a) {
+  const TcGeom g(a.n, a.w);
+  const TcConst C(g);
+  const int n = a.n, w = a.w, WP = g.WP, R = g.R;
+  const int nBF = n * (kKS / 8), nFP = 128 * (kKS / 8), nAP = kKS * (2 * n / 8);
+  int nAW[3], tot = nBF + nFP + nAP;
+  for (int l = 0; l < 3; ++l) { nAW[l] = 128 * (C.KB[l] / 8); tot += nAW[l]; }
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+    float v[8];
+    unsigned char* dst;
+    uint32_t half, off;
+    int u = t;
+    if (u < nBF) {                       // F[j][k'] K-major (N = j, K = k')
+      const int j = u % n, kc = u / n;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int kp = kc * 8 + q;
+        v[q] = 0.f;
+        if (kp < 2 * kModes) { const float2 f = a.F[(size_t)j * kModes + (kp >> 1)]; v[q] = (kp & 1) ? f.y : f.x; }
+      }
+      dst = a.out + C.BF; half = C.bf_half; off = tc::kmajor_off(j, kc * 8, (kKS / 8) * 128, 128);
+    } else if ((u -= nBF) < nFP) {       // Fp[i][(k1,p)] (rows i < n), K-major
+      const int i = u % 128, kc = u / 128;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = kc * 8 + q, k1 = k >> 1;
+        v[q] = 0.f;
+        if (i < n && k1 < kModes) { const float2 f = a.F[(size_t)i * kModes + k1]; v[q] = (k & 1) ? f.y : f.x; }
+      }
+      dst = a.out + C.FP; half = C.fp_half; off = tc::kmajor_off(i, kc * 8, (kKS / 8) * 128, 128);
+    } else if ((u -= nFP) < nAP) {       // Ap^T: row (k1, pout), K = (i, pin)
+      const int nn = u % kKS, kc = u / kKS, k1 = nn >> 1, pout = nn & 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int i = kc * 4 + q;
+        float2 f = make_float2(0.f, 0.f);
+        if (k1 < kModes) f = a.F[(size_t)i * kModes + k1];
+        v[2 * q] = pout ? f.y : f.x;
+        v[2 * q + 1] = pout ? f.x : -f.y;
+      }
+      dst = a.out + C.AP; half = C.ap_half; off = tc::kmajor_off(nn, kc * 8, ((2 * n) / 8) * 128, 128);
+    } else {                             // Wbd[(r,o)][(r',c)] per layer
+      u -= nAP;
+      int l = 0;
+      while (u >= nAW[l]) { u -= nAW[l]; ++l; }
+      const int cin = l == 0 ? 2 : w, CP = (cin + 7) & ~7, KB = C.KB[l];
+      const int Lr = u % 128, kc = u / 128, r = Lr / WP, o = Lr % WP;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int kk = kc * 8 + q, rp = kk / CP, c = kk % CP;
+        v[q] = (rp == r && rp < R && o < w && c < cin) ? a.W[l][(size_t)o * cin + c] : 0.f;
+      }
+      dst = a.out + C.AW[l]; half = C.aw_half[l]; off = tc::kmajor_off(Lr, kc * 8, (KB / 8) * 128, 128);
+    }
+    uint4 h, lo;
+    tc::split8(v, h, lo);
+    *reinterpret_cast<uint4*>(dst + off) = h;
+    *reinterpret_cast<uint4*>(dst + half + off) = lo;
+  }
+}
+
 // ------------------------------------------------------------------ k_tc_layer
 struct TcSmem {
-  // byte offsets; every region 1024-aligned; BV/AG hold [hi][lo] back to back like their blobs
-  uint32_t AW[2], BV, AG, BF[2], bar, tptr, bias, total;
+  // byte offsets; every region 1024-aligned; [hi][lo] back to back like their blobs
+  uint32_t BV, AG, BF, RK, TS, bar, tptr, bias, total;
   int KB, CP;
   __host__ __device__ TcSmem(const TcGeom& g, int cin) {
     CP = (cin + 7) & ~7;
     KB = (g.R * CP + 15) & ~15;
     uint32_t o = 0;
     auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
-    for (int h = 0; h < 2; ++h) AW[h] = take(128u * KB * 2);
     BV = take(2u * (uint32_t)g.n * KB * 2);
     AG = take(2u * g.g_half());
-    for (int h = 0; h < 2; ++h) BF[h] = take((uint32_t)g.n * kKS * 2);
+    BF = take(2u * (uint32_t)g.n * kKS * 2);
+    RK = take(cin == 2 ? 2u * g.R * g.n * 8 : 16u);   // layer 1: fp64 rows of r and k
+    TS = take(2u * (2 * g.R) * (uint32_t)(g.mtiles * 128) * 2);   // T tile staging [hi|lo][k_local][m]
     bar = take(64);
-    tptr = bar + 32;
+    tptr = bar + 40;
     bias = take(128 * 4);
     total = o;
   }
 };
 
 struct TcLayerArgs {
-  int n, w, cin, B, use_gelu;
+  int n, w, cin, B, use_gelu, layer;
   const double* r; const double* rr; const double* k;   // layer 1 inputs
   const unsigned char* vin;                              // V blobs (layers 2, 3)
-  const float* W;                                        // [w][cin]
+  const float* W;                                        // [w][cin] (layer 1: W1E [w][2])
   const float* bias;                                     // [w]
   const unsigned char* G;                                // G blobs
-  const float2* F;                                       // [n][20]
+  const unsigned char* cst;                              // constant blobs (TcConst)
   unsigned char* vout;                                   // V blobs of the next layer
   unsigned char* T;                                      // T blobs
   const int* status;
@@ -86,18 +182,22 @@ struct TcLayerArgs {
 template <int WP, bool FIRST>
 __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a) {
   const TcGeom g(a.n, a.w);
+  const TcConst C(g);
   constexpr int R = 128 / WP;
   extern __shared__ __align__(1024) unsigned char sm[];
   const int n = a.n, N = n * n, w = a.w, cin = a.cin;
   const TcSmem L(g, cin);
   const int KB = L.KB, CP = L.CP;                     // of this layer's input (FIRST: cin = 2)
   const uint32_t SBO_AW = (KB / 8) * 128, SBO_BV = (KB / 8) * 128, SBO_AG = g.g_sbo(), SBO_F = (kKS / 8) * 128;
+  const uint32_t aw_half = 128u * KB * 2, bv_half = (uint32_t)KB * n * 2, bf_half = (uint32_t)n * kKS * 2;
   const uint32_t vout_half = g.v_half(), vout_sbo = g.v_sbo();   // next layer's V blob geometry (cin = w)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0] loads, [1] D1, [2] D2
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0] tile loads, [1] D1, [2] D2, [3] constants
   uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
   float* sbias = reinterpret_cast<float*>(sm + L.bias);
+  const double* rk = reinterpret_cast<const double*>(sm + L.RK);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t need = (uint32_t)n + 64u + (uint32_t)n;
+  // TMEM: D1 / D2 (aliased) [0, n), v' hi/lo (A of D2) [n, 2n), Wbd hi/lo (A of the bypass) [2n, 2n+KB)
+  const uint32_t need = 2u * n + (uint32_t)KB;
   const uint32_t ncols = need <= 128 ? 128u : (need <= 256 ? 256u : 512u);
   const int ntiles = a.B * g.tiles_per_sys;
   auto running = [&](int t) { return !a.status || a.status[t / g.tiles_per_sys] == SYS_RUNNING; };
@@ -105,68 +205,78 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     while (t < ntiles && !running(t)) t += gridDim.x;
     return t;
   };
-  const uint32_t in_bytes = FIRST ? 2u * g.g_half() : 2u * (uint32_t)KB * n * 2 + 2u * g.g_half();
-  auto prefetch = [&](int t) {   // one thread: bulk copies of tile t's blobs
+  const uint32_t rk_bytes = (uint32_t)R * n * 8;
+  const uint32_t in_bytes = FIRST ? 2u * g.g_half() + 2u * rk_bytes : 2u * bv_half + 2u * g.g_half();
+  auto prefetch = [&](int t) {   // one thread: bulk copies of tile t's inputs
+    const int tb = t / g.tiles_per_sys, ti0 = (t % g.tiles_per_sys) * R;
     tc::mbar_expect_tx(&bar[0], in_bytes);
-    if (!FIRST) tc::bulk_g2s(sm + L.BV, a.vin + (size_t)t * 2 * KB * n * 2, 2u * KB * n * 2, &bar[0]);
+    if (FIRST) {
+      const size_t e = (size_t)tb * N + (size_t)ti0 * n;
+      tc::bulk_g2s(sm + L.RK, a.r + e, rk_bytes, &bar[0]);
+      tc::bulk_g2s(sm + L.RK + rk_bytes, a.k + e, rk_bytes, &bar[0]);
+    } else {
+      tc::bulk_g2s(sm + L.BV, a.vin + (size_t)t * 2 * bv_half, 2u * bv_half, &bar[0]);
+    }
     tc::bulk_g2s(sm + L.AG, a.G + (size_t)t * 2 * g.g_half(), 2u * g.g_half(), &bar[0]);
   };
 
-  // ---- one-time setup: barriers, TMEM, block-diagonal weights, twiddle operand, bias
+  // ---- one-time setup: barriers, TMEM, constant operands (bulk), bias
   int tile = next_tile(blockIdx.x);
   if (tid == 0) {
-    for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
+    for (int q = 0; q < 4; ++q) tc::mbar_init(&bar[q], 1);
     tc::fence_mbar_init();
+    tc::mbar_expect_tx(&bar[3], 2u * bf_half);
+    tc::bulk_g2s(sm + L.BF, a.cst + C.BF, 2u * bf_half, &bar[3]);
     if (tile < ntiles) prefetch(tile);
   }
   if (warp == 0) tc::tmem_alloc(tptr, ncols);
-  for (int t = tid; t < 128 * (KB / 8); t += blockDim.x) {        // Wbd[(r,o)][(r',c)]
-    const int Lr = t % 128, kc = t / 128;
-    const int r = Lr / WP, o = Lr % WP;
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int kk = kc * 8 + q, rp = kk / CP, c = kk % CP;
-      v[q] = (rp == r && rp < R && o < w && c < cin) ? a.W[(size_t)o * cin + c] : 0.f;
-    }
-    const uint32_t off = tc::kmajor_off(Lr, kc * 8, SBO_AW, 128);
-    store_split8(sm + L.AW[0] + off, sm + L.AW[1] + off, v);
-  }
-  for (int t = tid; t < n * (kKS / 8); t += blockDim.x) {         // F[j][k'] (K-major view: N = j, K = k')
-    const int j = t % n, kc = t / n;
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int kp = kc * 8 + q;
-      v[q] = 0.f;
-      if (kp < 2 * kModes) {
-        const float2 f = a.F[(size_t)j * kModes + (kp >> 1)];
-        v[q] = (kp & 1) ? f.y : f.x;
-      }
-    }
-    const uint32_t off = tc::kmajor_off(j, kc * 8, SBO_F, 128);
-    store_split8(sm + L.BF[0] + off, sm + L.BF[1] + off, v);
-  }
+  (void)aw_half;
   for (int t = tid; t < 128; t += blockDim.x) {
     const int o = t % WP;
     sbias[t] = o < w ? a.bias[o] : 0.f;
   }
-  tc::fence_proxy_async_smem();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tptr;
-  const uint32_t tD1 = tmem, tD2 = tmem + (uint32_t)n;
-  const uint32_t tAh = tmem + (uint32_t)n + 64u, tAl = tAh + (uint32_t)(n / 2);
-  const uint32_t id1 = tc::make_idesc_bf16(128, n, false, true);     // A K-major, B MN-major (bypass)
+  const uint32_t tD1 = tmem, tD2 = tmem;                 // D2 is issued after epilogue 1 drained D1
+  const uint32_t tAh = tmem + (uint32_t)n, tAl = tAh + (uint32_t)(n / 2);
+  const uint32_t tWh = tmem + 2u * n, tWl = tWh + (uint32_t)(KB / 2);
+  // Wbd rows into TMEM (lane = (r, o)): warps 0-3, one lane per row, K = (r', c) packed in pairs
+  if (warp < 4) {
+    const int Lr = warp * 32 + lane, r = Lr / WP, o = Lr % WP;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    for (int k0 = 0; k0 < KB; k0 += 16) {
+      uint32_t hi8[8], lo8[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        float x[2];
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
+          const int kk = k0 + 2 * t + z, rp = kk / CP, c = kk % CP;
+          x[z] = (rp == r && rp < R && o < w && c < cin) ? a.W[(size_t)o * cin + c] : 0.f;
+        }
+        tc::split2(x[0], x[1], hi8[t], lo8[t]);
+      }
+      tc::tmem_st8(tWh + lane_off + k0 / 2, hi8);
+      tc::tmem_st8(tWl + lane_off + k0 / 2, lo8);
+    }
+    tc::tmem_wait_st();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t id1 = tc::make_idesc_bf16(128, n, false, true);     // A (TMEM), B MN-major (bypass)
   const uint32_t id1s = tc::make_idesc_bf16(128, n, false, false);   // synthesis: both K-major
   const uint32_t id2 = tc::make_idesc_bf16(128, kKS, false, true);   // analysis: B = F viewed MN-major
   const uint32_t sm_base = tc::smem_u32(sm);
+  if (tid == 0) tc::mbar_wait(&bar[3], 0);
 
   uint32_t ph = 0;
   for (; tile < ntiles; tile = next_tile(tile + gridDim.x)) {
     const int b = tile / g.tiles_per_sys, i0 = (tile % g.tiles_per_sys) * R;
-    if (FIRST) {   // layer 1: V = [r/||r||, k] converted from fp64 in the block
+    if (FIRST) {   // layer 1: V = [r/||r||, k] converted from the prefetched fp64 rows
+      tc::mbar_wait(&bar[0], ph);
       const double s = sqrt(a.rr[b]);
       const double inv_s = s > 0.0 ? 1.0 / s : 0.0;
       for (int t = tid; t < KB * (n / 8); t += blockDim.x) {
@@ -176,33 +286,33 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
 #pragma unroll
         for (int q = 0; q < 8; ++q) v[q] = 0.f;
         if (rp < R && c < cin) {
-          const double* src = (c == 0 ? a.r : a.k) + (size_t)b * N + (size_t)(i0 + rp) * n + jc * 8;
+          const double* src = rk + (size_t)c * R * n + (size_t)rp * n + jc * 8;
 #pragma unroll
           for (int q = 0; q < 8; ++q) v[q] = (float)(c == 0 ? src[q] * inv_s : src[q]);
         }
         const uint32_t off = tc::mnmajor_off(jc * 8, kk, SBO_BV, 128);
-        store_split8(sm + L.BV + off, sm + L.BV + (uint32_t)KB * n * 2 + off, v);
+        store_split8(sm + L.BV + off, sm + L.BV + bv_half + off, v);
       }
       tc::fence_proxy_async_smem();
       __syncthreads();
     }
     // ---- D1 = Wbd V + G Basis   (3xBF16: hi*hi + hi*lo + lo*hi)
     if (tid == 0) {
-      tc::mbar_wait(&bar[0], ph);
+      if (!FIRST) tc::mbar_wait(&bar[0], ph);
       tc::fence_after_sync();
       uint32_t acc = 0;
       for (int s = 0; s < KB / 16; ++s) {
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
-          const uint32_t ao = L.AW[p == 2] + 256u * s, bo = L.BV + (p == 1 ? (uint32_t)KB * n * 2 : 0u) + 256u * s;
-          tc::mma_bf16(tD1, tc::make_sdesc(sm_base + ao, 128, SBO_AW), tc::make_sdesc(sm_base + bo, 128, SBO_BV), id1, acc);
+          const uint32_t at = (p == 2 ? tWl : tWh) + 8u * s, bo = L.BV + (p == 1 ? bv_half : 0u) + 256u * s;
+          tc::mma_bf16_ts(tD1, at, tc::make_sdesc(sm_base + bo, 128, SBO_BV), id1, acc);
           acc = 1;
         }
       }
       for (int s = 0; s < kKS / 16; ++s) {
 #pragma unroll
         for (int p = 0; p < 3; ++p) {
-          const uint32_t ao = L.AG + (p == 2 ? g.g_half() : 0u) + 256u * s, bo = L.BF[p == 1] + 256u * s;
+          const uint32_t ao = L.AG + (p == 2 ? g.g_half() : 0u) + 256u * s, bo = L.BF + (p == 1 ? bf_half : 0u) + 256u * s;
           tc::mma_bf16(tD1, tc::make_sdesc(sm_base + ao, 128, SBO_AG), tc::make_sdesc(sm_base + bo, 128, SBO_F), id1s, 1);
         }
       }
@@ -210,7 +320,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     }
     tc::mbar_wait(&bar[1], ph);
     tc::fence_after_sync();
-    // the MMAs have consumed BV / AG: prefetch the next tile while the epilogues run
+    // the MMAs have consumed BV / AG / RK: prefetch the next tile while the epilogues run
     if (tid == 0) {
       const int tn = next_tile(tile + gridDim.x);
       if (tn < ntiles) prefetch(tn);
@@ -263,7 +373,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
         for (int p = 0; p < 3; ++p) {
           const uint32_t at = (p == 2 ? tAl : tAh) + 8u * s;     // 16 bf16 of K = 8 TMEM columns
           // F viewed MN-major (N = k', K = j): LBO = K-group stride = SBO_F, SBO = N-group stride = 128
-          const uint64_t bd = tc::make_sdesc(sm_base + L.BF[p == 1] + 2u * SBO_F * s, SBO_F, 128);
+          const uint64_t bd = tc::make_sdesc(sm_base + L.BF + (p == 1 ? bf_half : 0u) + 2u * SBO_F * s, SBO_F, 128);
           tc::mma_bf16_ts(tD2, at, bd, id2, acc);
           acc = 1;
         }
@@ -272,14 +382,15 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     }
     tc::mbar_wait(&bar[2], ph);
     tc::fence_after_sync();
-    // ---- epilogue 2: D2 -> T blob: row m = (o, k2), K = (i, re|im) -> one 4-byte hi and lo word per k2
+    // ---- epilogue 2: D2 -> T blob.  Stage [hi|lo][k_local = (r, re|im)][m = (o, k2)] in smem, then
+    // copy 2R*16-byte runs per 8-row m group into the MN-major T blob (tc_layout.cuh).
     {
       const int q4 = warp & 3, half = warp >> 2;
       const int Lr = q4 * 32 + lane;
       const int r = Lr / WP, o = Lr % WP;
       const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
-      const int kcol = 2 * (i0 + r);
-      const uint32_t t_half = g.t_half(), t_sbo = g.t_sbo();
+      const int MT = g.mtiles * 128;
+      __nv_bfloat16* ts = reinterpret_cast<__nv_bfloat16*>(sm + L.TS);
 #pragma unroll
       for (int cc = 0; cc < 3; ++cc) {               // columns [24*half, 24*half + 24) in chunks of 8 (< 40)
         const int c0 = half * 24 + cc * 8;
@@ -289,16 +400,28 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
         tc::tmem_wait_ld();
         if (o < w) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int k2 = c0 / 2 + q, m = o * kModes + k2;
-            uint32_t hi, lo;
-            tc::split2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]), hi, lo);
-            unsigned char* tb = a.T + ((size_t)b * g.mtiles + m / 128) * 2 * t_half;
-            const uint32_t off = tc::kmajor_off(m % 128, kcol, t_sbo, 128);
-            *reinterpret_cast<uint32_t*>(tb + off) = hi;
-            *reinterpret_cast<uint32_t*>(tb + t_half + off) = lo;
+          for (int q = 0; q < 8; ++q) {
+            const int k2 = (c0 + q) >> 1, pin = (c0 + q) & 1, m = o * kModes + k2, kl = 2 * r + pin;
+            __nv_bfloat16 h, l;
+            tc::split_bf16(__uint_as_float(u[q]), h, l);
+            ts[(size_t)kl * MT + m] = h;
+            ts[(size_t)(2 * R + kl) * MT + m] = l;
           }
         }
+      }
+      __syncthreads();
+      const int KL = 2 * R, k0 = 2 * i0;                        // this tile's K range [k0, k0 + 2R)
+      const int ngroups = (w * kModes + 7) / 8;
+      const uint32_t t_half = g.t_half(), t_lbo = g.t_lbo();
+      unsigned char* tb = a.T + (size_t)b * g.mtiles * 2 * t_half;
+      for (int e = tid; e < 2 * ngroups; e += blockDim.x) {
+        const int hl = e / ngroups, grp = e % ngroups, mt = grp / 16, gi = grp % 16;
+        unsigned char* dst = tb + ((size_t)mt * 2 + hl) * t_half + (uint32_t)gi * 128 + (uint32_t)(k0 / 8) * t_lbo +
+                             (uint32_t)(k0 % 8) * 16;
+#pragma unroll 8
+        for (int kl = 0; kl < KL; ++kl)
+          *reinterpret_cast<uint4*>(dst + kl * 16) =
+              *reinterpret_cast<const uint4*>(ts + (size_t)(hl * KL + kl) * MT + grp * 8);
       }
     }
     tc::fence_before_sync();
@@ -316,182 +439,230 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
 //                Fp[i][(k1,0)] = Fx, Fp[i][(k1,1)] = Fy;  Gh rows (k1,0) = (gr | gi), (k1,1) = (gi | -gr)
 //   y-analysis   C^T[(o,k2)][(k1,re|im)] = sum_{(i,p)} T[(o,k2)][(i,p)] * Ap[(i,p)][(k1,re|im)]
 //                Ap[(i,0)][(k1,re)] = Fx, Ap[(i,1)][(k1,re)] = -Fy, Ap[(i,0)][(k1,im)] = Fy, Ap[(i,1)][(k1,im)] = Fx
-constexpr int kYsynCh = 6;                 // channels per CTA: N = 6 * 40 = 240
+constexpr int kYsynCh = 6;                 // channels per work item: N = 6 * 40 = 240
 constexpr int kYsynN = kYsynCh * 2 * kModes;
 
-__global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ ghat, const float2* __restrict__ F,
-                                                    unsigned char* __restrict__ Gb, int n, int w, const int* status) {
+struct YsynSmem {
+  uint32_t A, B, GS, bar, tptr, total;
+  __host__ __device__ YsynSmem() {
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
+    A = take(2u * 128 * kKS * 2);
+    B = take(2u * kYsynN * kKS * 2);
+    GS = take((uint32_t)kYsynCh * kModes2 * 8);
+    bar = take(64);
+    tptr = bar + 32;
+    total = o;
+  }
+};
+
+// persistent over work items (system, 6-channel chunk)
+__global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ ghat, const unsigned char* __restrict__ cst,
+                                                    unsigned char* __restrict__ Gb, int n, int w, int B,
+                                                    const int* status) {
   const TcGeom geo(n, w);
-  const int b = blockIdx.y, oc = blockIdx.x * kYsynCh;
-  if (status && status[b] != SYS_RUNNING) return;
+  const TcConst C(geo);
+  const YsynSmem L;
   extern __shared__ __align__(1024) unsigned char sm[];
   constexpr uint32_t SBO = (kKS / 8) * 128;             // K = 48 for both operands (K-major)
-  const uint32_t A0 = 0, A1 = 128 * kKS * 2, B0 = 2 * A1, B1 = B0 + kYsynN * kKS * 2, BAR = B1 + kYsynN * kKS * 2;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BAR);
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + BAR + 16);
+  const uint32_t a_half = 128u * kKS * 2, b_half = (uint32_t)kYsynN * kKS * 2;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0] staging, [1] MMA, [2] constants
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
+  const float2* gs = reinterpret_cast<const float2*>(sm + L.GS);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (tid == 0) { tc::mbar_init(bar, 1); tc::fence_mbar_init(); }
+  const int nch = (w + kYsynCh - 1) / kYsynCh, nitems = B * nch;
+  auto next_item = [&](int it) {
+    while (it < nitems && status && status[it / nch] != SYS_RUNNING) it += gridDim.x;
+    return it;
+  };
+  auto prefetch = [&](int it) {
+    const int b = it / nch, oc = (it % nch) * kYsynCh, nvalid = min(kYsynCh, w - oc);
+    const uint32_t bytes = (uint32_t)nvalid * kModes2 * 8;
+    tc::mbar_expect_tx(&bar[0], bytes);
+    tc::bulk_g2s(sm + L.GS, ghat + ((size_t)b * w + oc) * kModes2, bytes, &bar[0]);
+  };
+  int it = next_item(blockIdx.x);
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
+    tc::fence_mbar_init();
+    tc::mbar_expect_tx(&bar[2], 2u * a_half);
+    tc::bulk_g2s(sm + L.A, cst + C.FP, 2u * a_half, &bar[2]);
+    if (it < nitems) prefetch(it);
+  }
   if (warp == 0) tc::tmem_alloc(tptr, 256);
-  for (int t = tid; t < 128 * (kKS / 8); t += blockDim.x) {     // A = Fp (rows i < n), K-major
-    const int i = t % 128, kc = t / 128;
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int k = kc * 8 + q, k1 = k >> 1;
-      v[q] = 0.f;
-      if (i < n && k1 < kModes) { const float2 f = F[(size_t)i * kModes + k1]; v[q] = (k & 1) ? f.y : f.x; }
-    }
-    const uint32_t off = tc::kmajor_off(i, kc * 8, SBO, 128);
-    store_split8(sm + A0 + off, sm + A1 + off, v);
-  }
-  for (int t = tid; t < (kYsynN / 2) * (kKS / 8); t += blockDim.x) {   // B = Gh, rows (ol, k2, pout)
-    const int m = t % (kYsynN / 2), kc = t / (kYsynN / 2);
-    const int ol = m / kModes, k2 = m % kModes, o = oc + ol;
-    float vr[8], vi[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k1 = kc * 4 + q;
-      float2 gg = make_float2(0.f, 0.f);
-      if (o < w && k1 < kModes) gg = ghat[((size_t)b * w + o) * kModes2 + k1 * kModes + k2];
-      vr[2 * q] = gg.x;  vr[2 * q + 1] = gg.y;
-      vi[2 * q] = gg.y;  vi[2 * q + 1] = -gg.x;
-    }
-    const uint32_t offr = tc::kmajor_off(2 * m, kc * 8, SBO, 128), offi = tc::kmajor_off(2 * m + 1, kc * 8, SBO, 128);
-    store_split8(sm + B0 + offr, sm + B1 + offr, vr);
-    store_split8(sm + B0 + offi, sm + B1 + offi, vi);
-  }
-  tc::fence_proxy_async_smem();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tptr;
-  if (tid == 0) {
-    const uint32_t id = tc::make_idesc_bf16(128, kYsynN, false, false);
-    const uint32_t base = tc::smem_u32(sm);
-    uint32_t acc = 0;
-    for (int s = 0; s < kKS / 16; ++s)
+  const uint32_t id = tc::make_idesc_bf16(128, kYsynN, false, false);
+  const uint32_t base = tc::smem_u32(sm);
+  if (tid == 0) tc::mbar_wait(&bar[2], 0);
+  uint32_t ph = 0;
+  for (; it < nitems; it = next_item(it + gridDim.x)) {
+    const int b = it / nch, oc = (it % nch) * kYsynCh;
+    tc::mbar_wait(&bar[0], ph);
+    // B = Gh rows (ol, k2, pout), K = (k1, pin), from the staged g of the chunk
+    for (int t = tid; t < (kYsynN / 2) * (kKS / 8); t += blockDim.x) {
+      const int m = t % (kYsynN / 2), kc = t / (kYsynN / 2);
+      const int ol = m / kModes, k2 = m % kModes, o = oc + ol;
+      float vr[8], vi[8];
 #pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        const uint32_t aa = base + (p == 2 ? A1 : A0) + 256u * s, bb = base + (p == 1 ? B1 : B0) + 256u * s;
-        tc::mma_bf16(tmem, tc::make_sdesc(aa, 128, SBO), tc::make_sdesc(bb, 128, SBO), id, acc);
-        acc = 1;
+      for (int q = 0; q < 4; ++q) {
+        const int k1 = kc * 4 + q;
+        float2 gg = make_float2(0.f, 0.f);
+        if (o < w && k1 < kModes) gg = gs[ol * kModes2 + k1 * kModes + k2];
+        vr[2 * q] = gg.x;  vr[2 * q + 1] = gg.y;
+        vi[2 * q] = gg.y;  vi[2 * q + 1] = -gg.x;
       }
-    tc::mma_commit(bar);
-  }
-  tc::mbar_wait(bar, 0);
-  tc::fence_after_sync();
-  // epilogue: lane = row i -> G blob of tile (b, i / R), row Lr = (i % R, o), 16-byte hi/lo chunks of k'
-  const int i = warp * 32 + lane;
-  const uint32_t gh = geo.g_half(), gs = geo.g_sbo();
-  unsigned char* gt = Gb + ((size_t)b * geo.tiles_per_sys + (i < n ? i / geo.R : 0)) * 2 * gh;
-  for (int ol = 0; ol < kYsynCh; ++ol) {
-    const int o = oc + ol;
-    const uint32_t Lr = (uint32_t)((i % geo.R) * geo.WP + o);
+      const uint32_t offr = tc::kmajor_off(2 * m, kc * 8, SBO, 128), offi = tc::kmajor_off(2 * m + 1, kc * 8, SBO, 128);
+      store_split8(sm + L.B + offr, sm + L.B + b_half + offr, vr);
+      store_split8(sm + L.B + offi, sm + L.B + b_half + offi, vi);
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      const int itn = next_item(it + gridDim.x);       // staging buffer is free again
+      if (itn < nitems) prefetch(itn);
+      tc::fence_after_sync();
+      uint32_t acc = 0;
+      for (int s = 0; s < kKS / 16; ++s)
 #pragma unroll
-    for (int c = 0; c < 2 * kModes; c += 8) {
-      uint32_t u[8];
-      tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + ol * 2 * kModes + c, u);
-      tc::tmem_wait_ld();
-      if (i < n && o < w) {
-        float v[8];
+        for (int p = 0; p < 3; ++p) {
+          const uint32_t aa = base + L.A + (p == 2 ? a_half : 0u) + 256u * s, bb = base + L.B + (p == 1 ? b_half : 0u) + 256u * s;
+          tc::mma_bf16(tmem, tc::make_sdesc(aa, 128, SBO), tc::make_sdesc(bb, 128, SBO), id, acc);
+          acc = 1;
+        }
+      tc::mma_commit(&bar[1]);
+    }
+    tc::mbar_wait(&bar[1], ph);
+    tc::fence_after_sync();
+    // epilogue: lane = row i -> G blob of tile (b, i / R), row Lr = (i % R, o), 16-byte hi/lo chunks of k'
+    const int i = warp * 32 + lane;
+    const uint32_t gh = geo.g_half(), gsb = geo.g_sbo();
+    unsigned char* gt = Gb + ((size_t)b * geo.tiles_per_sys + (i < n ? i / geo.R : 0)) * 2 * gh;
+    for (int ol = 0; ol < kYsynCh; ++ol) {
+      const int o = oc + ol;
+      const uint32_t Lr = (uint32_t)((i % geo.R) * geo.WP + o);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(u[q]);
-        uint4 h, l;
-        tc::split8(v, h, l);
-        const uint32_t off = tc::kmajor_off(Lr, c, gs, 128);
-        *reinterpret_cast<uint4*>(gt + off) = h;
-        *reinterpret_cast<uint4*>(gt + gh + off) = l;
+      for (int c = 0; c < 2 * kModes; c += 8) {
+        uint32_t u[8];
+        tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + ol * 2 * kModes + c, u);
+        tc::tmem_wait_ld();
+        if (i < n && o < w) {
+          float v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[q] = __uint_as_float(u[q]);
+          uint4 h, l;
+          tc::split8(v, h, l);
+          const uint32_t off = tc::kmajor_off(Lr, c, gsb, 128);
+          *reinterpret_cast<uint4*>(gt + off) = h;
+          *reinterpret_cast<uint4*>(gt + gh + off) = l;
+        }
       }
     }
+    tc::fence_before_sync();
+    __syncthreads();
+    ph ^= 1;
   }
-  tc::fence_before_sync();
+  tc::fence_after_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
 
 constexpr int kYanN = kKS;                 // (k1, re|im) = 40 padded to 48
 
-__global__ void __launch_bounds__(128, 2) k_yan_tc(const unsigned char* __restrict__ Tb, const float2* __restrict__ F,
+// persistent over work items (system, 128-row m tile)
+__global__ void __launch_bounds__(128, 2) k_yan_tc(const unsigned char* __restrict__ Tb, const unsigned char* __restrict__ cst,
                                                    float2* __restrict__ chat, int n, int w, int B, const int* status) {
   const TcGeom geo(n, w);
-  const int b = blockIdx.y, mt = blockIdx.x, m0 = mt * 128;
-  if (status && status[b] != SYS_RUNNING) return;
+  const TcConst C(geo);
   extern __shared__ __align__(1024) unsigned char sm[];
   const int K = 2 * n;
-  const uint32_t SBO_A = geo.t_sbo(), SBO_B = (K / 8) * 128, th = geo.t_half();
-  const uint32_t A0 = 0, B0 = 2 * th, B1 = B0 + kYanN * K * 2, BAR = B1 + kYanN * K * 2;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BAR);     // [0] load, [1] MMA
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + BAR + 16);
+  const uint32_t SBO_A = geo.t_sbo(), LBO_A = geo.t_lbo(), SBO_B = (K / 8) * 128, th = geo.t_half(), bh = C.ap_half;
+  const uint32_t A0 = 0, B0 = (2 * th + 1023) & ~1023u, BAR = (B0 + 2 * bh + 1023) & ~1023u;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + BAR);     // [0] tile load, [1] MMA, [2] constants
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + BAR + 32);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int M = w * kModes;
-  if (tid == 0) {
-    tc::mbar_init(&bar[0], 1);
-    tc::mbar_init(&bar[1], 1);
-    tc::fence_mbar_init();
+  const int M = w * kModes, nitems = B * geo.mtiles;
+  auto next_item = [&](int it) {
+    while (it < nitems && status && status[it / geo.mtiles] != SYS_RUNNING) it += gridDim.x;
+    return it;
+  };
+  auto prefetch = [&](int it) {
     tc::mbar_expect_tx(&bar[0], 2 * th);
-    tc::bulk_g2s(sm + A0, Tb + ((size_t)b * geo.mtiles + mt) * 2 * th, 2 * th, &bar[0]);
+    tc::bulk_g2s(sm + A0, Tb + (size_t)it * 2 * th, 2 * th, &bar[0]);
+  };
+  int it = next_item(blockIdx.x);
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
+    tc::fence_mbar_init();
+    tc::mbar_expect_tx(&bar[2], 2 * bh);
+    tc::bulk_g2s(sm + B0, cst + C.AP, 2 * bh, &bar[2]);
+    if (it < nitems) prefetch(it);
   }
   if (warp == 0) tc::tmem_alloc(tptr, 64);
-  for (int t = tid; t < kYanN * (K / 8); t += blockDim.x) {     // B = Ap^T: row (k1, pout), K = (i, pin)
-    const int nn = t % kYanN, kc = t / kYanN, k1 = nn >> 1, pout = nn & 1;
-    float v[8];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int i = kc * 4 + q;
-      float2 f = make_float2(0.f, 0.f);
-      if (k1 < kModes) f = F[(size_t)i * kModes + k1];
-      v[2 * q] = pout ? f.y : f.x;            // pin = re
-      v[2 * q + 1] = pout ? f.x : -f.y;       // pin = im
-    }
-    const uint32_t off = tc::kmajor_off(nn, kc * 8, SBO_B, 128);
-    store_split8(sm + B0 + off, sm + B1 + off, v);
-  }
-  tc::fence_proxy_async_smem();
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tptr;
-  if (tid == 0) {
-    tc::mbar_wait(&bar[0], 0);
+  const uint32_t id = tc::make_idesc_bf16(128, kYanN, true, false);   // A (T) MN-major
+  const uint32_t base = tc::smem_u32(sm);
+  if (tid == 0) tc::mbar_wait(&bar[2], 0);
+  uint32_t ph = 0;
+  for (; it < nitems; it = next_item(it + gridDim.x)) {
+    const int b = it / geo.mtiles, m0 = (it % geo.mtiles) * 128;
+    if (tid == 0) {
+      tc::mbar_wait(&bar[0], ph);
+      tc::fence_after_sync();
+      uint32_t acc = 0;
+      for (int s = 0; s < K / 16; ++s)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          const uint32_t aa = base + A0 + (p == 2 ? th : 0u) + 2u * LBO_A * s, bb = base + B0 + (p == 1 ? bh : 0u) + 256u * s;
+          tc::mma_bf16(tmem, tc::make_sdesc(aa, LBO_A, SBO_A), tc::make_sdesc(bb, 128, SBO_B), id, acc);
+          acc = 1;
+        }
+      tc::mma_commit(&bar[1]);
+    }
+    tc::mbar_wait(&bar[1], ph);
     tc::fence_after_sync();
-    const uint32_t id = tc::make_idesc_bf16(128, kYanN, false, false);
-    const uint32_t base = tc::smem_u32(sm);
-    uint32_t acc = 0;
-    for (int s = 0; s < K / 16; ++s)
+    if (tid == 0) {                                   // A consumed: prefetch the next tile
+      const int itn = next_item(it + gridDim.x);
+      if (itn < nitems) prefetch(itn);
+    }
+    {
+      const int m = m0 + warp * 32 + lane;
+      const int o = m / kModes, k2 = m % kModes;
 #pragma unroll
-      for (int p = 0; p < 3; ++p) {
-        const uint32_t aa = base + A0 + (p == 2 ? th : 0u) + 256u * s, bb = base + (p == 1 ? B1 : B0) + 256u * s;
-        tc::mma_bf16(tmem, tc::make_sdesc(aa, 128, SBO_A), tc::make_sdesc(bb, 128, SBO_B), id, acc);
-        acc = 1;
-      }
-    tc::mma_commit(&bar[1]);
-  }
-  tc::mbar_wait(&bar[1], 0);
-  tc::fence_after_sync();
-  {
-    const int m = m0 + warp * 32 + lane;
-    const int o = m / kModes, k2 = m % kModes;
+      for (int c = 0; c < 2 * kModes; c += 8) {
+        uint32_t u[8];
+        tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, u);
+        tc::tmem_wait_ld();
+        if (m < M) {
 #pragma unroll
-    for (int c = 0; c < 2 * kModes; c += 8) {
-      uint32_t u[8];
-      tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c, u);
-      tc::tmem_wait_ld();
-      if (m < M) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int k1 = c / 2 + q;
-          chat[((size_t)(k1 * kModes + k2) * B + b) * w + o] = make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
+          for (int q = 0; q < 4; ++q) {
+            const int k1 = c / 2 + q;
+            chat[((size_t)(k1 * kModes + k2) * B + b) * w + o] = make_float2(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1]));
+          }
         }
       }
     }
+    tc::fence_before_sync();
+    __syncthreads();
+    ph ^= 1;
   }
-  tc::fence_before_sync();
+  tc::fence_after_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 64);
 }
 
-static size_t ysyn_tc_smem() { return (size_t)2 * 128 * kKS * 2 + (size_t)2 * kYsynN * kKS * 2 + 64; }
-static size_t yan_tc_smem(int n) { return (size_t)2 * 128 * (2 * n) * 2 + (size_t)2 * kYanN * (2 * n) * 2 + 64; }
+static size_t ysyn_tc_smem() { return YsynSmem().total; }
+static size_t yan_tc_smem(int n) {
+  const TcGeom g(n, 1);
+  const uint32_t th = g.t_half(), bh = (uint32_t)kKS * (2 * n) * 2;
+  return (((2 * th + 1023) & ~1023u) + 2 * bh + 1023 & ~1023u) + 64;
+}
 
 // ------------------------------------------------------------------ host side
 static int optin_bytes() {
@@ -544,14 +715,14 @@ cudaError_t prepare_tc_kernels() {
 
 cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s) {
   TcLayerArgs a{};
-  a.n = h.n; a.w = h.w; a.cin = h.cin; a.B = h.B; a.use_gelu = h.use_gelu;
-  a.r = h.r; a.rr = h.rr; a.k = h.k; a.vin = h.vin; a.W = h.W; a.bias = h.bias; a.G = h.G;
-  a.F = reinterpret_cast<const float2*>(h.F); a.vout = h.vout; a.T = h.T; a.status = h.status;
+  a.n = h.n; a.w = h.w; a.cin = h.cin; a.B = h.B; a.use_gelu = h.use_gelu; a.layer = h.layer;
+  a.r = h.r; a.rr = h.rr; a.k = h.k; a.vin = h.vin; a.W = h.W; a.bias = h.bias; a.G = h.G; a.cst = h.cst;
+  a.vout = h.vout; a.T = h.T; a.status = h.status;
   const TcGeom g(h.n, h.w);
   const int ntiles = h.B * g.tiles_per_sys;
   const size_t smem = TcSmem(g, h.cin).total;
   // persistent grid: as many CTAs as fit per SM by shared memory (<= 2) and TMEM columns
-  const uint32_t need_cols = (uint32_t)h.n + 64u + (uint32_t)h.n;
+  const uint32_t need_cols = 2u * h.n + (uint32_t)TcSmem(g, h.cin).KB;
   const int by_tmem = need_cols <= 256 ? 2 : 1;
   const int by_smem = (int)((228u * 1024u) / (smem + 1024u));
   const int per_sm = std::max(1, std::min(by_tmem, std::min(by_smem, 2)));
@@ -569,18 +740,31 @@ cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_ysyn(const float* ghat, const float* F, unsigned char* Gb, int n, int w, int B, const int* status,
-                        cudaStream_t s) {
-  k_ysyn_tc<<<dim3((w + kYsynCh - 1) / kYsynCh, B), 128, ysyn_tc_smem(), s>>>(
-      reinterpret_cast<const float2*>(ghat), reinterpret_cast<const float2*>(F), Gb, n, w, status);
+cudaError_t launch_ysyn(const float* ghat, const unsigned char* cst, unsigned char* Gb, int n, int w, int B,
+                        const int* status, cudaStream_t s) {
+  const int items = B * ((w + kYsynCh - 1) / kYsynCh);
+  const int grid = std::min(items, 2 * num_sms());
+  k_ysyn_tc<<<grid, 128, ysyn_tc_smem(), s>>>(reinterpret_cast<const float2*>(ghat), cst, Gb, n, w, B, status);
   return cudaGetLastError();
 }
 
-cudaError_t launch_yan(const unsigned char* Tb, const float* F, float* chat, int n, int w, int B, const int* status,
-                       cudaStream_t s) {
+cudaError_t launch_yan(const unsigned char* Tb, const unsigned char* cst, float* chat, int n, int w, int B,
+                       const int* status, cudaStream_t s) {
   const TcGeom g(n, w);
-  k_yan_tc<<<dim3(g.mtiles, B), 128, yan_tc_smem(n), s>>>(Tb, reinterpret_cast<const float2*>(F),
-                                                          reinterpret_cast<float2*>(chat), n, w, B, status);
+  const int items = B * g.mtiles;
+  const int per_sm = yan_tc_smem(n) <= 110 * 1024 ? 2 : 1;
+  const int grid = std::min(items, per_sm * num_sms());
+  k_yan_tc<<<grid, 128, yan_tc_smem(n), s>>>(Tb, cst, reinterpret_cast<float2*>(chat), n, w, B, status);
+  return cudaGetLastError();
+}
+
+size_t tc_const_bytes(int n, int w) { return TcConst(TcGeom(n, w)).total; }
+
+cudaError_t launch_tc_prep(int n, int w, const float* W1, const float* W2, const float* W3, const float* F,
+                           unsigned char* out, cudaStream_t s) {
+  TcPrepArgs a{};
+  a.n = n; a.w = w; a.W[0] = W1; a.W[1] = W2; a.W[2] = W3; a.F = reinterpret_cast<const float2*>(F); a.out = out;
+  k_tc_prep<<<2 * num_sms(), 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

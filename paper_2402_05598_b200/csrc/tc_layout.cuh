@@ -29,9 +29,12 @@ struct TcGeom {
   // G blob of a tile (A operand of the x-synthesis): K-major, M = (r, o) (128), K = k' (48)
   __host__ __device__ uint32_t g_half() const { return 128u * kKS * 2; }
   __host__ __device__ uint32_t g_sbo() const { return (uint32_t)(kKS / 8) * 128; }
-  // T blob of an (system, m-tile) (A operand of the y-analysis): K-major, M = (o, kappa2), K = (i, re|im) (2n)
+  // T blob of an (system, m-tile) (A operand of the y-analysis): MN-major, M = (o, kappa2) (128 per tile),
+  // K = (i, re|im) (2n); m-groups adjacent (SBO = 128), k-groups at LBO = 16 * 128, so the 2R
+  // consecutive k written by one layer tile form 2R*16-byte contiguous runs.
   __host__ __device__ uint32_t t_half() const { return 128u * (2 * n) * 2; }
-  __host__ __device__ uint32_t t_sbo() const { return (uint32_t)((2 * n) / 8) * 128; }
+  __host__ __device__ uint32_t t_sbo() const { return 128u; }
+  __host__ __device__ uint32_t t_lbo() const { return 16u * 128u; }
   __host__ __device__ size_t v_bytes_total(int B) const { return (size_t)B * tiles_per_sys * 2 * v_half(); }
   __host__ __device__ size_t g_bytes_total(int B) const { return (size_t)B * tiles_per_sys * 2 * g_half(); }
   __host__ __device__ size_t t_bytes_total(int B) const { return (size_t)B * mtiles * 2 * t_half(); }
