@@ -123,6 +123,13 @@ __device__ __forceinline__ bool arrive_last(unsigned* counter, int nblk) {
   return last != 0;
 }
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels of one FCG iteration are launched with programmatic stream serialization: a kernel may
+// start (and run its prologue) while its predecessor drains; pdl_wait() blocks until the
+// predecessor grid has completed and its memory is visible.  No-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 // ------------------------------------------------------------------ schedule
 __device__ __forceinline__ int m_schedule(int i, int m, int schedule) {
   if (schedule == 1) return i < m ? i : m;               // sliding

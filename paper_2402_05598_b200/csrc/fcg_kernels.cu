@@ -21,12 +21,23 @@ uint64_t& launch_counter() {
   return c;
 }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FCGNO_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static inline dim3 sys_grid(int nblk, int B) { return dim3((unsigned)nblk, (unsigned)B, 1); }
 
 
 // ------------------------------------------------------------------ apply_A
 __global__ void __launch_bounds__(kThreads) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
                                                       double* __restrict__ y, int n, int N, double scale) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.y;
   const double* kb = k + (size_t)b * N;
   const double* xb = x + (size_t)b * N;
@@ -43,7 +54,8 @@ __global__ void __launch_bounds__(kThreads) k_apply_A(const double* __restrict__
 
 cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, cudaStream_t s) {
   const int N = n * n, nblk = (N + kTile - 1) / kTile;
-  k_apply_A<<<sys_grid(nblk, B), kThreads, 0, s>>>(k, x, y, n, N, double(n + 1) * double(n + 1));
+  cudaError_t e = launch_k(k_apply_A, sys_grid(nblk, B), dim3(kThreads), 0, s, k, x, y, n, N, double(n + 1) * double(n + 1));
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
@@ -52,6 +64,8 @@ cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, i
 __global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ x, const double* __restrict__ y,
                                                   double* __restrict__ out, dd* part, unsigned* cnt, int N,
                                                   int nblk) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ dd sm[8];
   const int b = blockIdx.y;
   double s = 0.0, c = 0.0;
@@ -72,13 +86,16 @@ __global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ x, 
 cudaError_t launch_dot(const double* x, const double* y, double* out, dd* part, unsigned* cnt, int n, int B,
                        cudaStream_t s) {
   const int N = n * n, nblk = (N + kTile - 1) / kTile;
-  k_dot<<<sys_grid(nblk, B), kThreads, 0, s>>>(x, y, out, part, cnt, N, nblk);
+  cudaError_t e = launch_k(k_dot, sys_grid(nblk, B), dim3(kThreads), 0, s, x, y, out, part, cnt, N, nblk);
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ k validation
 __global__ void k_check_k(const double* __restrict__ k, size_t count, int* bad) {
+  pdl_wait();
+  pdl_trigger();
   int local = 0;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < count; t += (size_t)gridDim.x * blockDim.x) {
     const double v = k[t];
@@ -95,6 +112,8 @@ cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t
 
 // ------------------------------------------------------------------ r0 = f - A u0
 __global__ void __launch_bounds__(kThreads) k_init_residual(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ dd sm[8];
   const int b = blockIdx.y, N = d.N;
   const double* kb = d.k + (size_t)b * N;
@@ -129,12 +148,15 @@ __global__ void __launch_bounds__(kThreads) k_init_residual(FcgDev d) {
 }
 
 cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s) {
-  k_init_residual<<<sys_grid(d.nblk, d.B), kThreads, 0, s>>>(d);
+  cudaError_t e = launch_k(k_init_residual, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 __global__ void __launch_bounds__(kThreads) k_window_dots(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.y;
   if (d.status[b] != SYS_RUNNING) return;
   const int i = *d.iter;
@@ -150,13 +172,16 @@ __global__ void __launch_bounds__(kThreads) k_window_dots(FcgDev d) {
 }
 
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
-  k_window_dots<<<sys_grid(d.nblk, d.B), kThreads, 0, s>>>(d);
+  cudaError_t e = launch_k(k_window_dots, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ p = w - sum beta_k p_k
 __global__ void __launch_bounds__(kThreads) k_pform(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.y;
   if (d.status[b] != SYS_RUNNING) return;
   const int i = *d.iter;
@@ -187,13 +212,16 @@ __global__ void __launch_bounds__(kThreads) k_pform(FcgDev d) {
 }
 
 cudaError_t launch_pform(const FcgDev& d, cudaStream_t s) {
-  k_pform<<<sys_grid(d.nblk, d.B), kThreads, 0, s>>>(d);
+  cudaError_t e = launch_k(k_pform, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ s = A p ; (p,s), (p,r)
 __global__ void __launch_bounds__(kThreads) k_stencil_dots(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ dd sm[16];
   const int b = blockIdx.y;
   if (d.status[b] != SYS_RUNNING) return;
@@ -234,13 +262,16 @@ __global__ void __launch_bounds__(kThreads) k_stencil_dots(FcgDev d) {
 }
 
 cudaError_t launch_stencil_dots(const FcgDev& d, cudaStream_t s) {
-  k_stencil_dots<<<sys_grid(d.nblk, d.B), kThreads, 0, s>>>(d);
+  cudaError_t e = launch_k(k_stencil_dots, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ u += alpha p ; r -= alpha s ; (r,r)
 __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ dd sm[8];
   const int b = blockIdx.y;
   if (d.status[b] != SYS_RUNNING || d.flags[b] != 0) return;
@@ -271,13 +302,16 @@ __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
 }
 
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s) {
-  k_update<<<sys_grid(d.nblk, d.B), kThreads, 0, s>>>(d);
+  cudaError_t e = launch_k(k_update, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ convergence bookkeeping
 __global__ void __launch_bounds__(kThreads) k_finalize(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   const int i = *d.iter;
   __shared__ int total;
   if (threadIdx.x == 0) total = 0;
@@ -307,7 +341,8 @@ __global__ void __launch_bounds__(kThreads) k_finalize(FcgDev d) {
 }
 
 cudaError_t launch_finalize(const FcgDev& d, cudaStream_t s) {
-  k_finalize<<<1, kThreads, 0, s>>>(d);
+  cudaError_t e = launch_k(k_finalize, dim3(1), dim3(kThreads), 0, s, d);
+  if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }

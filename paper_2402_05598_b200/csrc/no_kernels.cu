@@ -59,6 +59,8 @@ __global__ void __launch_bounds__(256) k_dft_rows(const double* __restrict__ x, 
                                                   const typename Cplx<T>::type* __restrict__ F,
                                                   typename Cplx<T>::type* __restrict__ part, int n, int ngroups,
                                                   const int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename Cplx<T>::type;
   const int b = blockIdx.y, g = blockIdx.x;
   if (status && status[b] != SYS_RUNNING) return;
@@ -101,6 +103,8 @@ __global__ void __launch_bounds__(256) k_dft_rows(const double* __restrict__ x, 
 template <typename T>
 __global__ void k_reduce_groups(const typename Cplx<T>::type* __restrict__ part, typename Cplx<T>::type* __restrict__ out,
                                 int ngroups) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename Cplx<T>::type;
   const int b = blockIdx.x;
   for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
@@ -136,6 +140,8 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
                                                   const typename Cplx<T>::type* __restrict__ A2,
                                                   typename Cplx<T>::type* __restrict__ ghat, int w, T n2, T inv_n2,
                                                   const int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename Cplx<T>::type;
   const int b = blockIdx.x, ochunk = blockIdx.y;   // 8 output channels per CTA
   if (status && status[b] != SYS_RUNNING) return;
@@ -171,6 +177,8 @@ __global__ void __launch_bounds__(256) k_mix(const typename Cplx<T>::type* __res
                                              const typename Cplx<T>::type* __restrict__ R,
                                              typename Cplx<T>::type* __restrict__ ghat, int B, int cin, int cout,
                                              T inv_n2, const int* __restrict__ status, int nparts) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename Cplx<T>::type;
   extern __shared__ __align__(16) unsigned char smraw[];
   T2* Rs = reinterpret_cast<T2*>(smraw);             // [cin][cout]
@@ -282,6 +290,8 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <typename T, bool FIRST, int GO>
 __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename Cplx<T>::type;
   constexpr int NACC = (GO * kModes2 + 255) / 256;
   constexpr int VEC = 16 / sizeof(T);
@@ -472,6 +482,8 @@ struct OutArgs {
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   using T2 = typename Cplx<T>::type;
   const int b = blockIdx.y, blk = blockIdx.x;
   if (a.status && a.status[b] != SYS_RUNNING) return;
@@ -547,6 +559,8 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
 // Phase 1: 128 groups of 8 consecutive pixels x 2 channel halves accumulate dw . (hi + lo) with
 // 16-byte loads into shared memory; phase 2 is k_no_out's per-pixel synthesis + window dots.
 __global__ void __launch_bounds__(kThreads) k_no_out_blob(const OutArgs<float> a, const FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
   const int b = blockIdx.y, blk = blockIdx.x;
   if (a.status && a.status[b] != SYS_RUNNING) return;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -703,14 +717,14 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
 
   // 1. DFT_M of r/||r|| (row-group partials)
   pb(PROF_NO_INPUT);
-  k_dft_rows<T, true><<<dim3(no.ngroups, B), 256, dft_smem(n, sizeof(T)), s>>>(
-      r, rr, F, reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status);
+  launch_k(k_dft_rows<T, true>, dim3(no.ngroups, B), dim3(256), dft_smem(n, sizeof(T)), s, r, rr, F,
+           reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status);
   ++launches;
   // 2. layer-1 mixing with the lift folded in
-  k_lift_mix<T><<<dim3(B, (w + 7) / 8), 256, 0, s>>>(reinterpret_cast<const T2*>(no.rpart), no.ngroups,
-                                  reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
-                                  reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2),
-                                  ghat, w, n2, inv_n2, status);
+  launch_k(k_lift_mix<T>, dim3(B, (w + 7) / 8), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
+           reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
+           reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2), ghat, w, n2, inv_n2,
+           status);
   pe(PROF_NO_INPUT);
   ++launches;
   // 3. layers 1..3, each followed by the mixing of the next layer
@@ -762,9 +776,9 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, nbuf).total * sizeof(T);
       pb(PROF_NO_LAYER);
       if (l == 0) {
-        k_no_layer<T, true, GO><<<lgrid, 256, smem, s>>>(la);
+        launch_k(k_no_layer<T, true, GO>, lgrid, dim3(256), smem, s, la);
       } else {
-        k_no_layer<T, false, GO><<<lgrid, 256, smem, s>>>(la);
+        launch_k(k_no_layer<T, false, GO>, lgrid, dim3(256), smem, s, la);
       }
       pe(PROF_NO_LAYER);
       ++launches;
@@ -774,8 +788,8 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     const T2* Rm = reinterpret_cast<const T2*>(pk + (l < 2 ? no.L.R[l] : no.L.Q));
     const size_t msmem = ((size_t)w * cout + (size_t)kMixBatch * w) * sizeof(T2);
     pb(PROF_NO_MIX);
-    k_mix<T><<<dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), 256, msmem, s>>>(chat, Rm, ghat, B, w, cout, inv_n2,
-                                                                               status, 1);
+    launch_k(k_mix<T>, dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), dim3(256), msmem, s,
+             (const T2*)chat, Rm, ghat, B, w, cout, inv_n2, status, 1);
     pe(PROF_NO_MIX);
     ++launches;
     if (tc_path && l < 2) {
@@ -799,12 +813,12 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   if constexpr (sizeof(T) == sizeof(float)) {
     if (tc_path) {
       oa.vblob = vblob[0];   // layer 3 wrote vblob[2 & 1]
-      k_no_out_blob<<<dim3(nblk, B), kThreads, osmem + kTile * sizeof(float), s>>>(oa, fcg ? *fcg : dummy);
+      launch_k(k_no_out_blob, dim3(nblk, B), dim3(kThreads), osmem + kTile * sizeof(float), s, oa, fcg ? *fcg : dummy);
     } else {
-      k_no_out<T><<<dim3(nblk, B), kThreads, osmem, s>>>(oa, fcg ? *fcg : dummy);
+      launch_k(k_no_out<T>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);
     }
   } else {
-    k_no_out<T><<<dim3(nblk, B), kThreads, osmem, s>>>(oa, fcg ? *fcg : dummy);
+    launch_k(k_no_out<T>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);
   }
   pe(PROF_NO_OUT);
   ++launches;

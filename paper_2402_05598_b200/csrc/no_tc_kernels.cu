@@ -220,17 +220,19 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     tc::bulk_g2s(sm + L.AG, a.G + (size_t)t * 2 * g.g_half(), 2u * g.g_half(), &bar[0]);
   };
 
-  // ---- one-time setup: barriers, TMEM, constant operands (bulk), bias
-  int tile = next_tile(blockIdx.x);
+  // ---- one-time setup: barriers, TMEM, constant operands (bulk), bias; then wait for the predecessor
   if (tid == 0) {
     for (int q = 0; q < 4; ++q) tc::mbar_init(&bar[q], 1);
     tc::fence_mbar_init();
     tc::mbar_expect_tx(&bar[3], 2u * bf_half);
     tc::bulk_g2s(sm + L.BF, a.cst + C.BF, 2u * bf_half, &bar[3]);
-    if (tile < ntiles) prefetch(tile);
   }
+  pdl_wait();
+  pdl_trigger();
+  int tile = next_tile(blockIdx.x);
+  if (tid == 0 && tile < ntiles) prefetch(tile);
   if (warp == 0) tc::tmem_alloc(tptr, ncols);
-  (void)aw_half;
+
   for (int t = tid; t < 128; t += blockDim.x) {
     const int o = t % WP;
     sbias[t] = o < w ? a.bias[o] : 0.f;
@@ -242,21 +244,20 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   const uint32_t tD1 = tmem, tD2 = tmem;                 // D2 is issued after epilogue 1 drained D1
   const uint32_t tAh = tmem + (uint32_t)n, tAl = tAh + (uint32_t)(n / 2);
   const uint32_t tWh = tmem + 2u * n, tWl = tWh + (uint32_t)(KB / 2);
-  // Wbd rows into TMEM (lane = (r, o)): warps 0-3, one lane per row, K = (r', c) packed in pairs
+  // Wbd rows into TMEM (lane = (r, o)) from the prebuilt K-major blob: warps 0-3, one lane per row
   if (warp < 4) {
-    const int Lr = warp * 32 + lane, r = Lr / WP, o = Lr % WP;
+    const int Lr = warp * 32 + lane;
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const unsigned char* aw = a.cst + C.AW[a.layer];
     for (int k0 = 0; k0 < KB; k0 += 16) {
       uint32_t hi8[8], lo8[8];
 #pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        float x[2];
-#pragma unroll
-        for (int z = 0; z < 2; ++z) {
-          const int kk = k0 + 2 * t + z, rp = kk / CP, c = kk % CP;
-          x[z] = (rp == r && rp < R && o < w && c < cin) ? a.W[(size_t)o * cin + c] : 0.f;
-        }
-        tc::split2(x[0], x[1], hi8[t], lo8[t]);
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t off = tc::kmajor_off(Lr, k0 + 8 * hh, SBO_AW, 128);
+        const uint4 h = __ldg(reinterpret_cast<const uint4*>(aw + off));
+        const uint4 l = __ldg(reinterpret_cast<const uint4*>(aw + aw_half + off));
+        hi8[4 * hh] = h.x; hi8[4 * hh + 1] = h.y; hi8[4 * hh + 2] = h.z; hi8[4 * hh + 3] = h.w;
+        lo8[4 * hh] = l.x; lo8[4 * hh + 1] = l.y; lo8[4 * hh + 2] = l.z; lo8[4 * hh + 3] = l.w;
       }
       tc::tmem_st8(tWh + lane_off + k0 / 2, hi8);
       tc::tmem_st8(tWl + lane_off + k0 / 2, lo8);
@@ -481,14 +482,16 @@ __global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ g
     tc::mbar_expect_tx(&bar[0], bytes);
     tc::bulk_g2s(sm + L.GS, ghat + ((size_t)b * w + oc) * kModes2, bytes, &bar[0]);
   };
-  int it = next_item(blockIdx.x);
   if (tid == 0) {
     for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
     tc::fence_mbar_init();
     tc::mbar_expect_tx(&bar[2], 2u * a_half);
     tc::bulk_g2s(sm + L.A, cst + C.FP, 2u * a_half, &bar[2]);
-    if (it < nitems) prefetch(it);
   }
+  pdl_wait();
+  pdl_trigger();
+  int it = next_item(blockIdx.x);
+  if (tid == 0 && it < nitems) prefetch(it);
   if (warp == 0) tc::tmem_alloc(tptr, 256);
   tc::fence_before_sync();
   __syncthreads();
@@ -593,14 +596,16 @@ __global__ void __launch_bounds__(128, 2) k_yan_tc(const unsigned char* __restri
     tc::mbar_expect_tx(&bar[0], 2 * th);
     tc::bulk_g2s(sm + A0, Tb + (size_t)it * 2 * th, 2 * th, &bar[0]);
   };
-  int it = next_item(blockIdx.x);
   if (tid == 0) {
     for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
     tc::fence_mbar_init();
     tc::mbar_expect_tx(&bar[2], 2 * bh);
     tc::bulk_g2s(sm + B0, cst + C.AP, 2 * bh, &bar[2]);
-    if (it < nitems) prefetch(it);
   }
+  pdl_wait();
+  pdl_trigger();
+  int it = next_item(blockIdx.x);
+  if (tid == 0 && it < nitems) prefetch(it);
   if (warp == 0) tc::tmem_alloc(tptr, 64);
   tc::fence_before_sync();
   __syncthreads();
@@ -728,14 +733,14 @@ cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s) {
   const int per_sm = std::max(1, std::min(by_tmem, std::min(by_smem, 2)));
   const int grid = std::min(ntiles, per_sm * num_sms());
   if (g.WP == 32) {
-    if (h.first) k_tc_layer<32, true><<<grid, kTcThreads, smem, s>>>(a);
-    else k_tc_layer<32, false><<<grid, kTcThreads, smem, s>>>(a);
+    if (h.first) launch_k(k_tc_layer<32, true>, dim3(grid), dim3(kTcThreads), smem, s, a);
+    else launch_k(k_tc_layer<32, false>, dim3(grid), dim3(kTcThreads), smem, s, a);
   } else if (g.WP == 64) {
-    if (h.first) k_tc_layer<64, true><<<grid, kTcThreads, smem, s>>>(a);
-    else k_tc_layer<64, false><<<grid, kTcThreads, smem, s>>>(a);
+    if (h.first) launch_k(k_tc_layer<64, true>, dim3(grid), dim3(kTcThreads), smem, s, a);
+    else launch_k(k_tc_layer<64, false>, dim3(grid), dim3(kTcThreads), smem, s, a);
   } else {
-    if (h.first) k_tc_layer<128, true><<<grid, kTcThreads, smem, s>>>(a);
-    else k_tc_layer<128, false><<<grid, kTcThreads, smem, s>>>(a);
+    if (h.first) launch_k(k_tc_layer<128, true>, dim3(grid), dim3(kTcThreads), smem, s, a);
+    else launch_k(k_tc_layer<128, false>, dim3(grid), dim3(kTcThreads), smem, s, a);
   }
   return cudaGetLastError();
 }
@@ -744,7 +749,8 @@ cudaError_t launch_ysyn(const float* ghat, const unsigned char* cst, unsigned ch
                         const int* status, cudaStream_t s) {
   const int items = B * ((w + kYsynCh - 1) / kYsynCh);
   const int grid = std::min(items, 2 * num_sms());
-  k_ysyn_tc<<<grid, 128, ysyn_tc_smem(), s>>>(reinterpret_cast<const float2*>(ghat), cst, Gb, n, w, B, status);
+  launch_k(k_ysyn_tc, dim3(grid), dim3(128), ysyn_tc_smem(), s, reinterpret_cast<const float2*>(ghat), cst, Gb, n, w, B,
+           status);
   return cudaGetLastError();
 }
 
@@ -754,7 +760,7 @@ cudaError_t launch_yan(const unsigned char* Tb, const unsigned char* cst, float*
   const int items = B * g.mtiles;
   const int per_sm = yan_tc_smem(n) <= 110 * 1024 ? 2 : 1;
   const int grid = std::min(items, per_sm * num_sms());
-  k_yan_tc<<<grid, 128, yan_tc_smem(n), s>>>(Tb, cst, reinterpret_cast<float2*>(chat), n, w, B, status);
+  launch_k(k_yan_tc, dim3(grid), dim3(128), yan_tc_smem(n), s, Tb, cst, reinterpret_cast<float2*>(chat), n, w, B, status);
   return cudaGetLastError();
 }
 

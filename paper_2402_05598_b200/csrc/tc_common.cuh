@@ -129,13 +129,16 @@ __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bflo
   hi = __float2bfloat16_rn(x);
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
-// two values -> packed hi pair and packed lo pair (element 0 in the low half)
+// two values -> packed hi pair and packed lo pair (element 0 in the low half); packed cvt
+__device__ __forceinline__ uint32_t cvt_bf16x2(float x0, float x1) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;\n" : "=r"(r) : "f"(x1), "f"(x0));   // first source -> upper half
+  return r;
+}
 __device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  __nv_bfloat16 h0, l0, h1, l1;
-  split_bf16(x0, h0, l0);
-  split_bf16(x1, h1, l1);
-  hi = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-  lo = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+  hi = cvt_bf16x2(x0, x1);
+  const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xFFFF0000u);
+  lo = cvt_bf16x2(x0 - h0, x1 - h1);
 }
 // 8 values -> 16-byte hi chunk and 16-byte lo chunk
 __device__ __forceinline__ void split8(const float* v, uint4& hi, uint4& lo) {
