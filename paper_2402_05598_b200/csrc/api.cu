@@ -100,6 +100,7 @@ template <typename T>
 struct NoWs {
   T *rpart, *v0, *v1, *chat, *ghat;
   unsigned char *vb0, *vb1, *Gb, *Tb, *cst;   // tensor-core path blobs (fp32 NO only)
+  float* p3;
   size_t vb_bytes, gb_bytes;
 };
 template <typename T>
@@ -120,6 +121,7 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
     r.Gb = c.take<unsigned char>(r.gb_bytes);
     r.Tb = c.take<unsigned char>(g.t_bytes_total(B));
     r.cst = c.take<unsigned char>(tc_const_bytes(n, w));
+    r.p3 = c.take<float>((size_t)B * n * n);
   }
   return r;
 }
@@ -153,7 +155,7 @@ NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* 
   no.k = p->k; no.pk = static_cast<const T*>(packed); no.L = no_layout(d.width);
   no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
   no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
-  no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb; no.cst = w.cst;
+  no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb; no.cst = w.cst; no.p3 = w.p3;
   no.tc = (sizeof(T) == sizeof(float)) && w.Gb != nullptr && tc_enabled() && tc_layer_supported(p->n, d.width);
   return no;
 }

@@ -70,6 +70,7 @@ struct NoDev {
   unsigned char* Gb;          // G blobs (y-synthesised spectral term)
   unsigned char* Tb;          // T blobs (x-analysed activations)
   unsigned char* cst;         // constant operand blobs (twiddles, block-diagonal weights)
+  float* p3;                  // [B][n][n] layer-3 projection bypass term (tensor-core path)
   int tc;                     // 1: fp32 layers on tcgen05 (no_tc_kernels.cu)
 };
 
@@ -82,6 +83,8 @@ struct TcLayerArgsHost {
   const unsigned char* G;
   const unsigned char* cst;   // constant operand blobs (launch_tc_prep)
   unsigned char *vout, *T;
+  const float* dw;   // layer 3: projection weights -> pout (fused projection)
+  float* pout;
   const int* status;
 };
 bool tc_layer_supported(int n, int w);

@@ -469,7 +469,7 @@ template <typename T>
 struct OutArgs {
   int n, N, w, use_dots;
   const T* vin;                                   // [B][w][N]
-  const unsigned char* vblob;                     // tensor-core path: layer-3 activation blobs
+  const float* p3;                                // tensor-core path: layer-3 projection bypass term [B][N]
   const T* dw;                                    // [w]
   const T* cst;                                   // [1]
   const typename Cplx<T>::type* gh4;              // [B][400] scaled by n^-2
@@ -555,9 +555,9 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
   }
 }
 
-// Tensor-core path variant: layer-3 activations come as bf16 hi/lo blobs (tc_layout.cuh).
-// Phase 1: 128 groups of 8 consecutive pixels x 2 channel halves accumulate dw . (hi + lo) with
-// 16-byte loads into shared memory; phase 2 is k_no_out's per-pixel synthesis + window dots.
+// Tensor-core path variant: the layer-4 bypass sum_o (D W4)[o] v3[o] arrives as one fp32 field
+// reduced by layer 3's epilogue; this kernel adds cst + the 1-channel synthesis, scales by ||r||
+// and computes the FCG window dots.
 __global__ void __launch_bounds__(kThreads) k_no_out_blob(const OutArgs<float> a, const FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -576,39 +576,8 @@ __global__ void __launch_bounds__(kThreads) k_no_out_blob(const OutArgs<float> a
   for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)b * kModes2 + t];
   for (int t = threadIdx.x; t < w; t += blockDim.x) dws[t] = a.dw[t];
   __syncthreads();
-  // phase 1: bypass dot products from the blob
-  {
-    const int grp = threadIdx.x >> 1, half = threadIdx.x & 1;   // 128 groups of 8 pixels
-    const int p0 = e0 + grp * 8;
-    float acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.f;
-    if (p0 < N) {
-      const int i = p0 / n, j = p0 - i * n;
-      const unsigned char* vb = a.vblob + ((size_t)b * g.tiles_per_sys + i / g.R) * 2 * g.v_half();
-      const int r = i % g.R;
-      const int chalf = (w + 1) / 2, clo = half * chalf, chi = min(w, clo + chalf);
-      for (int c = clo; c < chi; ++c) {
-        const uint32_t off = tc::mnmajor_off(j, (uint32_t)(r * g.CP + c), g.v_sbo(), 128);
-        const uint4 h = __ldg(reinterpret_cast<const uint4*>(vb + off));
-        const uint4 l = __ldg(reinterpret_cast<const uint4*>(vb + g.v_half() + off));
-        const float wc = dws[c];
-        const uint32_t hh[4] = {h.x, h.y, h.z, h.w}, ll[4] = {l.x, l.y, l.z, l.w};
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          acc[2 * q] += wc * (tc::bf16pair_lo(hh[q]) + tc::bf16pair_lo(ll[q]));
-          acc[2 * q + 1] += wc * (tc::bf16pair_hi(hh[q]) + tc::bf16pair_hi(ll[q]));
-        }
-      }
-    }
-    if (half == 1)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) outs[grp * 8 + q] = acc[q];
-    __syncthreads();
-    if (half == 0)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) outs[grp * 8 + q] += acc[q];
-  }
+  // phase 1: the bypass term sum_o dw[o] v3[o] was reduced by layer 3 (k_tc_layer, fused projection)
+  for (int t = threadIdx.x; t < kTile; t += blockDim.x) outs[t] = (e0 + t < N) ? a.p3[(size_t)b * N + e0 + t] : 0.f;
   for (int e = threadIdx.x; e < nr * kModes; e += blockDim.x) {
     const int r = e / kModes, k2 = e - r * kModes;
     float gr = 0, gi = 0;
@@ -753,6 +722,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       h.vin = l == 0 ? nullptr : vblob[(l - 1) & 1];
       h.vout = vblob[l & 1];
       h.G = no.Gb; h.T = no.Tb; h.status = status;
+      if (l == 2) { h.dw = reinterpret_cast<const float*>(pk + no.L.dw); h.pout = no.p3; }
       pb(PROF_NO_LAYER);
       launch_tc_layer(h, s);
       pe(PROF_NO_LAYER);
@@ -812,7 +782,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   pb(PROF_NO_OUT);
   if constexpr (sizeof(T) == sizeof(float)) {
     if (tc_path) {
-      oa.vblob = vblob[0];   // layer 3 wrote vblob[2 & 1]
+      oa.p3 = no.p3;
       launch_k(k_no_out_blob, dim3(nblk, B), dim3(kThreads), osmem + kTile * sizeof(float), s, oa, fcg ? *fcg : dummy);
     } else {
       launch_k(k_no_out<T>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);

@@ -7,7 +7,7 @@
 // The DFTs are separable; every contraction is a dense GEMM on the 5th-gen tensor cores:
 //
 //   k_ysyn_tc   per (system, 6 channels): G[i][(o,k')] = Fp[i][(k1,p)] . Gh[(k1,p)][(o,k')]          (y-synthesis)
-//   k_tc_layer  tile = R rows of one system; TMEM lanes = (row r, padded channel o), R * WP = 128
+//   k_tc_layer  tile = R rows of one system; TMEM lane = o * R + r (channel-major so padding channels fill whole warps), R * WP = 128
 //     D1[(r,o)][j]  = sum_{(r',c)} Wbd[(r,o)][(r',c)] V[(r',c)][j]      bypass, block-diagonal in r
 //                   + sum_{k'} G[(r,o)][k'] Basis[k'][j]                 x-synthesis (k' = (kappa2, re|im))
 //     epilogue      v' = GELU(D1 + b) -> next layer's V blob, and into TMEM (A operand of D2)
@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) k_tc_prep(const TcPrepArgs a) {
       int l = 0;
       while (u >= nAW[l]) { u -= nAW[l]; ++l; }
       const int cin = l == 0 ? 2 : w, CP = (cin + 7) & ~7, KB = C.KB[l];
-      const int Lr = u % 128, kc = u / 128, r = Lr / WP, o = Lr % WP;
+      const int Lr = u % 128, kc = u / 128, r = Lr % R, o = Lr / R;   // lane = (o, r): padding in whole warps
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int kk = kc * 8 + q, rp = kk / CP, c = kk % CP;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) k_tc_prep(const TcPrepArgs a) {
 // ------------------------------------------------------------------ k_tc_layer
 struct TcSmem {
   // byte offsets; every region 1024-aligned; [hi][lo] back to back like their blobs
-  uint32_t BV, AG, BF, RK, TS, bar, tptr, bias, total;
+  uint32_t BV, AG, BF, RK, TS, PJ, bar, tptr, bias, total;
   int KB, CP;
   __host__ __device__ TcSmem(const TcGeom& g, int cin) {
     CP = (cin + 7) & ~7;
@@ -159,6 +159,7 @@ struct TcSmem {
     BF = take(2u * (uint32_t)g.n * kKS * 2);
     RK = take(cin == 2 ? 2u * g.R * g.n * 8 : 16u);   // layer 1: fp64 rows of r and k
     TS = take(2u * (2 * g.R) * (uint32_t)(g.mtiles * 128) * 2);   // T tile staging [hi|lo][k_local][m]
+    PJ = take(4u * g.R * (uint32_t)g.n * 4);                      // layer 3: per-warp-quad projection partials
     bar = take(64);
     tptr = bar + 40;
     bias = take(128 * 4);
@@ -176,6 +177,8 @@ struct TcLayerArgs {
   const unsigned char* cst;                              // constant blobs (TcConst)
   unsigned char* vout;                                   // V blobs of the next layer
   unsigned char* T;                                      // T blobs
+  const float* dw;                                       // layer 3: projection weights (D W4) [w]
+  float* pout;                                           // layer 3: sum_o dw[o] v3[o] per pixel [B][n][n]
   const int* status;
 };
 
@@ -195,6 +198,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
   float* sbias = reinterpret_cast<float*>(sm + L.bias);
   const double* rk = reinterpret_cast<const double*>(sm + L.RK);
+  const bool proj = a.pout != nullptr;                  // layer 3 of the fused projection path
+  float* pj = reinterpret_cast<float*>(sm + L.PJ);      // [4 warp quads][R][n]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // TMEM: D1 / D2 (aliased) [0, n), v' hi/lo (A of D2) [n, 2n), Wbd hi/lo (A of the bypass) [2n, 2n+KB)
   const uint32_t need = 2u * n + (uint32_t)KB;
@@ -234,7 +239,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   if (warp == 0) tc::tmem_alloc(tptr, ncols);
 
   for (int t = tid; t < 128; t += blockDim.x) {
-    const int o = t % WP;
+    const int o = t / R;
     sbias[t] = o < w ? a.bias[o] : 0.f;
   }
   tc::fence_before_sync();
@@ -327,11 +332,13 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
       if (tn < ntiles) prefetch(tn);
     }
     // ---- epilogue 1: v' = GELU(D1 + b) -> next V blob (bf16 hi/lo) and -> TMEM (A operand of D2)
-    {
+    // Lane = (o, r); warps whose 32 lanes are all padding channels skip (their D2 rows are unused).
+    if ((32 * (warp & 3)) / R < g.CP) {
       const int q4 = warp & 3, half = warp >> 2;
       const int Lr = q4 * 32 + lane;
-      const int r = Lr / WP, o = Lr % WP;
+      const int r = Lr % R, o = Lr / R;
       const float bo = sbias[Lr];
+      const float dwo = (proj && o < w) ? a.dw[o] : 0.f;
       const bool store = o < g.CP;                       // rows (r, o >= w) carry exact zeros
       unsigned char* vb = a.vout + (size_t)tile * 2 * vout_half;
       const uint32_t kk = (uint32_t)(r * g.CP + o);
@@ -349,7 +356,18 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
         uint32_t ph8[8], pl8[8];
 #pragma unroll
         for (int t = 0; t < 8; ++t) tc::split2(v[2 * t], v[2 * t + 1], ph8[t], pl8[t]);
-        if (store) {
+        if (proj) {                                     // layer 3: sum_o dw[o] v3[(o, r)][j] instead of the blob
+          float pp[16];
+#pragma unroll
+          for (int t = 0; t < 16; ++t) pp[t] = dwo * v[t];
+#pragma unroll
+          for (int off = 16; off >= R; off >>= 1)
+#pragma unroll
+            for (int t = 0; t < 16; ++t) pp[t] += __shfl_xor_sync(0xffffffffu, pp[t], off);
+          if (lane < R)
+#pragma unroll
+            for (int t = 0; t < 16; ++t) pj[((size_t)q4 * R + r) * n + c0 + t] = pp[t];
+        } else if (store) {
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
             const uint32_t off = tc::mnmajor_off(c0 + 8 * hh, kk, vout_sbo, 128);
@@ -365,6 +383,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     }
     tc::fence_before_sync();
     __syncthreads();
+    if (proj) {   // fixed-order sum over the 4 warp quads (quads made only of padding lanes wrote nothing)
+      const int nq = min(4, (g.CP * R + 31) / 32);
+      for (int e = tid; e < R * n; e += blockDim.x) {
+        float acc = 0.f;
+        for (int q = 0; q < nq; ++q) acc += pj[(size_t)q * R * n + e];
+        a.pout[(size_t)b * N + (size_t)i0 * n + e] = acc;
+      }
+    }
     // ---- D2 = v' F  (x-analysis)
     if (tid == 0) {
       tc::fence_after_sync();
@@ -388,7 +414,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     {
       const int q4 = warp & 3, half = warp >> 2;
       const int Lr = q4 * 32 + lane;
-      const int r = Lr / WP, o = Lr % WP;
+      const int r = Lr % R, o = Lr / R;
       const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
       const int MT = g.mtiles * 128;
       __nv_bfloat16* ts = reinterpret_cast<__nv_bfloat16*>(sm + L.TS);
@@ -546,7 +572,7 @@ __global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ g
     unsigned char* gt = Gb + ((size_t)b * geo.tiles_per_sys + (i < n ? i / geo.R : 0)) * 2 * gh;
     for (int ol = 0; ol < kYsynCh; ++ol) {
       const int o = oc + ol;
-      const uint32_t Lr = (uint32_t)((i % geo.R) * geo.WP + o);
+      const uint32_t Lr = (uint32_t)(o * geo.R + (i % geo.R));   // lane = (o, r)
 #pragma unroll
       for (int c = 0; c < 2 * kModes; c += 8) {
         uint32_t u[8];
@@ -722,7 +748,7 @@ cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s) {
   TcLayerArgs a{};
   a.n = h.n; a.w = h.w; a.cin = h.cin; a.B = h.B; a.use_gelu = h.use_gelu; a.layer = h.layer;
   a.r = h.r; a.rr = h.rr; a.k = h.k; a.vin = h.vin; a.W = h.W; a.bias = h.bias; a.G = h.G; a.cst = h.cst;
-  a.vout = h.vout; a.T = h.T; a.status = h.status;
+  a.vout = h.vout; a.T = h.T; a.dw = h.dw; a.pout = h.pout; a.status = h.status;
   const TcGeom g(h.n, h.w);
   const int ntiles = h.B * g.tiles_per_sys;
   const size_t smem = TcSmem(g, h.cin).total;

@@ -26,7 +26,7 @@ struct TcGeom {
   // activation blob of a tile (B operand of the next layer): MN-major, N = j (n), K = (r, c) (KB)
   __host__ __device__ uint32_t v_half() const { return (uint32_t)KB * n * 2; }          // bytes of hi (= lo)
   __host__ __device__ uint32_t v_sbo() const { return (uint32_t)(KB / 8) * 128; }
-  // G blob of a tile (A operand of the x-synthesis): K-major, M = (r, o) (128), K = k' (48)
+  // G blob of a tile (A operand of the x-synthesis): K-major, M = (o, r) (lane o*R + r, 128), K = k' (48)
   __host__ __device__ uint32_t g_half() const { return 128u * kKS * 2; }
   __host__ __device__ uint32_t g_sbo() const { return (uint32_t)(kKS / 8) * 128; }
   // T blob of an (system, m-tile) (A operand of the y-analysis): MN-major, M = (o, kappa2) (128 per tile),
