@@ -95,8 +95,10 @@ cudaError_t launch_ysyn(const float* ghat, const unsigned char* cst, unsigned ch
 cudaError_t launch_yan(const unsigned char* Tb, const unsigned char* cst, float* chat, int n, int w, int B,
                        const int* status, cudaStream_t s);
 size_t tc_const_bytes(int n, int w);
-cudaError_t launch_tc_prep(int n, int w, const float* W1, const float* W2, const float* W3, const float* F,
-                           unsigned char* out, cudaStream_t s);
+cudaError_t launch_tc_prep(int n, int w, const float* W1, const float* W2, const float* W3, const float* R2,
+                           const float* R3, const float* Q, const float* F, unsigned char* out, cudaStream_t s);
+cudaError_t launch_mix_tc(int mix, const float* chat, const unsigned char* cst, float* ghat, int n, int w, int B,
+                          float inv_n2, const int* status, cudaStream_t s);
 
 // In-graph profiling hook: begin/end record CUDA events around launches of a kernel class.
 enum ProfClass : int { PROF_NO_LAYER = 0, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM,

@@ -758,8 +758,12 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     const T2* Rm = reinterpret_cast<const T2*>(pk + (l < 2 ? no.L.R[l] : no.L.Q));
     const size_t msmem = ((size_t)w * cout + (size_t)kMixBatch * w) * sizeof(T2);
     pb(PROF_NO_MIX);
-    launch_k(k_mix<T>, dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), dim3(256), msmem, s,
-             (const T2*)chat, Rm, ghat, B, w, cout, inv_n2, status, 1);
+    if (tc_path)
+      launch_mix_tc(l, reinterpret_cast<const float*>(chat), no.cst, reinterpret_cast<float*>(ghat), n, w, B,
+                    (float)inv_n2, status, s);
+    else
+      launch_k(k_mix<T>, dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), dim3(256), msmem, s,
+               (const T2*)chat, Rm, ghat, B, w, cout, inv_n2, status, 1);
     pe(PROF_NO_MIX);
     ++launches;
     if (tc_path && l < 2) {
@@ -801,7 +805,8 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
 cudaError_t prepare_no_constants(const NoDev<float>& no, cudaStream_t s) {
   if (!no.tc) return cudaSuccess;
   const float* pk = no.pk;
-  return launch_tc_prep(no.n, no.w, pk + no.L.W1E, pk + no.L.W[0], pk + no.L.W[1], no.F, no.cst, s);
+  return launch_tc_prep(no.n, no.w, pk + no.L.W1E, pk + no.L.W[0], pk + no.L.W[1], pk + no.L.R[0], pk + no.L.R[1],
+                        pk + no.L.Q, no.F, no.cst, s);
 }
 
 template cudaError_t launch_no_forward<float>(const NoDev<float>&, const double*, const double*, double*,

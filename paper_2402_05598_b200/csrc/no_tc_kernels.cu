@@ -54,9 +54,9 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[8]) {
 // every persistent CTA: twiddles for the x-direction (BF), the block-diagonal layer weights (AW),
 // the y-synthesis twiddles (FP) and the y-analysis twiddles (AP), each as [hi][lo] bf16.
 struct TcConst {
-  size_t BF, AW[3], FP, AP, total;
-  uint32_t bf_half, aw_half[3], fp_half, ap_half;
-  int KB[3];
+  size_t BF, AW[3], FP, AP, MX[3], total;
+  uint32_t bf_half, aw_half[3], fp_half, ap_half, mx_half[3];
+  int KB[3], KM, NM[3];
   __host__ __device__ TcConst(const TcGeom& g) {
     size_t o = 0;
     auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 1023) & ~size_t(1023); return at; };
@@ -72,12 +72,22 @@ struct TcConst {
     FP = take(2 * (size_t)fp_half);
     ap_half = (uint32_t)kKS * (2 * g.n) * 2;
     AP = take(2 * (size_t)ap_half);
+    // mode-mixing B operands per mode: rows (o, re|im) (NM), K = (c, re|im) (KM); mixes for layers 2, 3
+    // and the layer-4/projection fold (cout = 1)
+    KM = (2 * g.w + 15) & ~15;
+    for (int l = 0; l < 3; ++l) {
+      const int cout = l < 2 ? g.w : 1;
+      NM[l] = (2 * cout + 15) & ~15;
+      mx_half[l] = (uint32_t)NM[l] * KM * 2;
+      MX[l] = take((size_t)kModes2 * 2 * mx_half[l]);
+    }
     total = o;
   }
 };
 
 struct TcPrepArgs {
   int n, w;
+  const float2* Rm[3];    // mixing weights [400][w][cout] (layers 2, 3; Q with cout = 1)
   const float* W[3];      // layer weights [w][cin] (layer 1: W1E [w][2])
   const float2* F;        // [n][20]
   unsigned char* out;
@@ -88,8 +98,9 @@ __global__ void __launch_bounds__(256) k_tc_prep(const TcPrepArgs a) {
   const TcConst C(g);
   const int n = a.n, w = a.w, WP = g.WP, R = g.R;
   const int nBF = n * (kKS / 8), nFP = 128 * (kKS / 8), nAP = kKS * (2 * n / 8);
-  int nAW[3], tot = nBF + nFP + nAP;
+  int nAW[3], nMX[3], tot = nBF + nFP + nAP;
   for (int l = 0; l < 3; ++l) { nAW[l] = 128 * (C.KB[l] / 8); tot += nAW[l]; }
+  for (int l = 0; l < 3; ++l) { nMX[l] = kModes2 * C.NM[l] * (C.KM / 8); tot += nMX[l]; }
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
     float v[8];
     unsigned char* dst;
@@ -124,8 +135,24 @@ __global__ void __launch_bounds__(256) k_tc_prep(const TcPrepArgs a) {
         v[2 * q + 1] = pout ? f.x : -f.y;
       }
       dst = a.out + C.AP; half = C.ap_half; off = tc::kmajor_off(nn, kc * 8, ((2 * n) / 8) * 128, 128);
+    } else if ((u -= nAP) >= nAW[0] + nAW[1] + nAW[2]) {   // mixing B: row (o, pout), K = (c, pin)
+      u -= nAW[0] + nAW[1] + nAW[2];
+      int l = 0;
+      while (u >= nMX[l]) { u -= nMX[l]; ++l; }
+      const int cout = l < 2 ? w : 1, NM = C.NM[l], KM = C.KM;
+      const int per_mode = NM * (KM / 8), kk = u / per_mode, rem = u % per_mode, nn = rem % NM, kc = rem / NM;
+      const int o = nn >> 1, pout = nn & 1;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = kc * 4 + q;
+        float rr = 0.f, ri = 0.f;
+        if (c < w && o < cout) { const float2 R2 = a.Rm[l][((size_t)kk * w + c) * cout + o]; rr = R2.x; ri = R2.y; }
+        v[2 * q] = pout ? ri : rr;            // pin = re
+        v[2 * q + 1] = pout ? rr : -ri;       // pin = im
+      }
+      dst = a.out + C.MX[l] + (size_t)kk * 2 * C.mx_half[l]; half = C.mx_half[l];
+      off = tc::kmajor_off(nn, kc * 8, (KM / 8) * 128, 128);
     } else {                             // Wbd[(r,o)][(r',c)] per layer
-      u -= nAP;
       int l = 0;
       while (u >= nAW[l]) { u -= nAW[l]; ++l; }
       const int cin = l == 0 ? 2 : w, CP = (cin + 7) & ~7, KB = C.KB[l];
@@ -688,6 +715,118 @@ __global__ void __launch_bounds__(128, 2) k_yan_tc(const unsigned char* __restri
   if (warp == 0) tc::tmem_dealloc(tmem, 64);
 }
 
+// ------------------------------------------------------------------ mode-diagonal mixing on tensor cores
+// per mode kappa: G[b][(o, re|im)] = sum_{(c, re|im)} C[b][(c, re|im)] * R'[(c, re|im)][(o, re|im)] / n^2,
+// R' the 2x2-real form of R[c][o](kappa) (prebuilt per mode); M = systems (<= 128 per item).
+struct MixSmem {
+  uint32_t A, B, bar, tptr, total;
+  __host__ __device__ MixSmem(int KM, int NM) {
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
+    A = take(2u * 128 * KM * 2);
+    B = take(2u * NM * KM * 2);
+    bar = take(64);
+    tptr = bar + 32;
+    total = o;
+  }
+};
+
+__global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat, const unsigned char* __restrict__ cst,
+                                               float2* __restrict__ ghat, int n, int w, int B, int mix, float inv_n2,
+                                               const int* status) {
+  const TcGeom geo(n, w);
+  const TcConst C(geo);
+  const int KM = C.KM, NM = C.NM[mix], cout = mix < 2 ? w : 1;
+  const MixSmem L(KM, NM);
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const uint32_t SBO = (KM / 8) * 128, a_half = 128u * KM * 2, b_half = C.mx_half[mix];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0] B load, [1] MMA
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nbc = (B + 127) / 128, nitems = kModes2 * nbc;
+  auto prefetch = [&](int it) {
+    const int kk = it / nbc;
+    tc::mbar_expect_tx(&bar[0], 2 * b_half);
+    tc::bulk_g2s(sm + L.B, cst + C.MX[mix] + (size_t)kk * 2 * b_half, 2 * b_half, &bar[0]);
+  };
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+    if ((int)blockIdx.x < nitems) prefetch(blockIdx.x);   // weights do not depend on the predecessor
+  }
+  if (warp == 0) tc::tmem_alloc(tptr, 256);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tptr;
+  const uint32_t id = tc::make_idesc_bf16(128, NM, false, false);
+  const uint32_t base = tc::smem_u32(sm);
+  pdl_wait();
+  pdl_trigger();
+  uint32_t ph = 0;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int kk = it / nbc, b0 = (it % nbc) * 128, nb = min(128, B - b0);
+    // A: rows b, K = (c, re|im) = the float2 layout of c[kappa][b][c]
+    for (int t = tid; t < 128 * (KM / 8); t += blockDim.x) {
+      const int row = t % 128, kc = t / 128;
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = kc * 4 + q;
+        float2 x = make_float2(0.f, 0.f);
+        if (row < nb && c < w) x = chat[((size_t)kk * B + b0 + row) * w + c];
+        v[2 * q] = x.x; v[2 * q + 1] = x.y;
+      }
+      const uint32_t off = tc::kmajor_off(row, kc * 8, SBO, 128);
+      store_split8(sm + L.A + off, sm + L.A + a_half + off, v);
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::mbar_wait(&bar[0], ph);
+      tc::fence_after_sync();
+      uint32_t acc = 0;
+      for (int s = 0; s < KM / 16; ++s)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          const uint32_t aa = base + L.A + (p == 2 ? a_half : 0u) + 256u * s, bb = base + L.B + (p == 1 ? b_half : 0u) + 256u * s;
+          tc::mma_bf16(tmem, tc::make_sdesc(aa, 128, SBO), tc::make_sdesc(bb, 128, SBO), id, acc);
+          acc = 1;
+        }
+      tc::mma_commit(&bar[1]);
+    }
+    tc::mbar_wait(&bar[1], ph);
+    tc::fence_after_sync();
+    if (tid == 0 && it + (int)gridDim.x < nitems) prefetch(it + gridDim.x);   // B consumed
+    {
+      const int row = warp * 32 + lane, b = b0 + row;
+      const bool ok = row < nb && (!status || status[b] == SYS_RUNNING);
+      for (int c0 = 0; c0 < 2 * cout; c0 += 8) {
+        uint32_t u[8];
+        tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c0, u);
+        tc::tmem_wait_ld();
+        if (ok) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int o = c0 / 2 + q;
+            if (o < cout)
+              ghat[((size_t)b * cout + o) * kModes2 + kk] =
+                  make_float2(__uint_as_float(u[2 * q]) * inv_n2, __uint_as_float(u[2 * q + 1]) * inv_n2);
+          }
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    ph ^= 1;
+  }
+  tc::fence_after_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
 static size_t ysyn_tc_smem() { return YsynSmem().total; }
 static size_t yan_tc_smem(int n) {
   const TcGeom g(n, 1);
@@ -740,6 +879,7 @@ cudaError_t prepare_tc_kernels() {
   if ((e = prep_tc<128>()) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute((const void*)k_ysyn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute((const void*)k_yan_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute((const void*)k_mix_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)) != cudaSuccess) return e;
   done = true;
   return cudaSuccess;
 }
@@ -792,10 +932,24 @@ cudaError_t launch_yan(const unsigned char* Tb, const unsigned char* cst, float*
 
 size_t tc_const_bytes(int n, int w) { return TcConst(TcGeom(n, w)).total; }
 
-cudaError_t launch_tc_prep(int n, int w, const float* W1, const float* W2, const float* W3, const float* F,
-                           unsigned char* out, cudaStream_t s) {
+cudaError_t launch_mix_tc(int mix, const float* chat, const unsigned char* cst, float* ghat, int n, int w, int B,
+                          float inv_n2, const int* status, cudaStream_t s) {
+  const TcGeom g(n, w);
+  const TcConst C(g);
+  const size_t smem = MixSmem(C.KM, C.NM[mix]).total;
+  const int nitems = kModes2 * ((B + 127) / 128);
+  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  const int grid = std::min(nitems, per_sm * num_sms());
+  return launch_k(k_mix_tc, dim3(grid), dim3(128), smem, s, reinterpret_cast<const float2*>(chat), cst,
+                  reinterpret_cast<float2*>(ghat), n, w, B, mix, inv_n2, status);
+}
+
+cudaError_t launch_tc_prep(int n, int w, const float* W1, const float* W2, const float* W3, const float* R2,
+                           const float* R3, const float* Q, const float* F, unsigned char* out, cudaStream_t s) {
   TcPrepArgs a{};
   a.n = n; a.w = w; a.W[0] = W1; a.W[1] = W2; a.W[2] = W3; a.F = reinterpret_cast<const float2*>(F); a.out = out;
+  a.Rm[0] = reinterpret_cast<const float2*>(R2); a.Rm[1] = reinterpret_cast<const float2*>(R3);
+  a.Rm[2] = reinterpret_cast<const float2*>(Q);
   k_tc_prep<<<2 * num_sms(), 256, 0, s>>>(a);
   return cudaGetLastError();
 }
