@@ -148,7 +148,15 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
   __shared__ T2 Rh[kModes2];
   for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
     T ar = 0, ai = 0;
-    for (int g = 0; g < ngroups; ++g) {
+    int g = 0;
+    for (; g + 8 <= ngroups; g += 8) {          // 8 independent loads in flight
+      T2 v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = rpart[((size_t)b * ngroups + g + q) * kModes2 + e];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) { ar += v[q].x; ai += v[q].y; }
+    }
+    for (; g < ngroups; ++g) {
       const T2 v = rpart[((size_t)b * ngroups + g) * kModes2 + e];
       ar += v.x; ai += v.y;
     }
@@ -156,15 +164,29 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
   }
   __syncthreads();
   const int k0 = (kModes / 2) * kModes + kModes / 2;   // kappa = (0, 0)
-  const int olo = ochunk * 8, ohi = min(w, olo + 8);
-  for (int e = threadIdx.x; e < (ohi - olo) * kModes2; e += blockDim.x) {
-    const int o = olo + e / kModes2, kk = e % kModes2;
-    const T2 a0 = A0[(size_t)kk * w + o], a1 = A1[(size_t)kk * w + o];
-    const T2 rh = Rh[kk], kh = khat[(size_t)b * kModes2 + kk];
-    T gr = a0.x * rh.x - a0.y * rh.y + a1.x * kh.x - a1.y * kh.y;
-    T gi = a0.x * rh.y + a0.y * rh.x + a1.x * kh.y + a1.y * kh.x;
-    if (kk == k0) { gr += n2 * A2[o].x; gi += n2 * A2[o].y; }
-    ghat[((size_t)b * w + o) * kModes2 + kk] = T2{gr * inv_n2, gi * inv_n2};
+  const int olo = ochunk * 8, ohi = min(w, olo + 8), cnt = (ohi - olo) * kModes2;
+  for (int e0 = threadIdx.x; e0 < cnt; e0 += 4 * blockDim.x) {
+    T2 a0[4], a1[4], kh[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q * blockDim.x;
+      const int o = olo + e / kModes2, kk = e % kModes2;
+      const bool ok = e < cnt;
+      a0[q] = ok ? A0[(size_t)kk * w + o] : T2{T(0), T(0)};
+      a1[q] = ok ? A1[(size_t)kk * w + o] : T2{T(0), T(0)};
+      kh[q] = ok ? khat[(size_t)b * kModes2 + kk] : T2{T(0), T(0)};
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = e0 + q * blockDim.x;
+      if (e >= cnt) break;
+      const int o = olo + e / kModes2, kk = e % kModes2;
+      const T2 rh = Rh[kk];
+      T gr = a0[q].x * rh.x - a0[q].y * rh.y + a1[q].x * kh[q].x - a1[q].y * kh[q].y;
+      T gi = a0[q].x * rh.y + a0[q].y * rh.x + a1[q].x * kh[q].y + a1[q].y * kh[q].x;
+      if (kk == k0) { gr += n2 * A2[o].x; gi += n2 * A2[o].y; }
+      ghat[((size_t)b * w + o) * kModes2 + kk] = T2{gr * inv_n2, gi * inv_n2};
+    }
   }
 }
 

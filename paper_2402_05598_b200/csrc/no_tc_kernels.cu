@@ -767,19 +767,33 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
   uint32_t ph = 0;
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     const int kk = it / nbc, b0 = (it % nbc) * 128, nb = min(128, B - b0);
-    // A: rows b, K = (c, re|im) = the float2 layout of c[kappa][b][c]
-    for (int t = tid; t < 128 * (KM / 8); t += blockDim.x) {
-      const int row = t % 128, kc = t / 128;
-      float v[8];
+    // A: rows b, K = (c, re|im) = the float2 layout of c[kappa][b][c]; all loads of a batch first
+    {
+      constexpr int kBatch = 8;
+      const int ntask = 128 * (KM / 8);
+      for (int t0 = tid; t0 < ntask; t0 += kBatch * blockDim.x) {
+        float2 x[kBatch][4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = kc * 4 + q;
-        float2 x = make_float2(0.f, 0.f);
-        if (row < nb && c < w) x = chat[((size_t)kk * B + b0 + row) * w + c];
-        v[2 * q] = x.x; v[2 * q + 1] = x.y;
+        for (int z = 0; z < kBatch; ++z) {
+          const int t = t0 + z * blockDim.x, row = t % 128, kc = t / 128;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = kc * 4 + q;
+            x[z][q] = (t < ntask && row < nb && c < w) ? __ldg(chat + ((size_t)kk * B + b0 + row) * w + c)
+                                                       : make_float2(0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int z = 0; z < kBatch; ++z) {
+          const int t = t0 + z * blockDim.x, row = t % 128, kc = t / 128;
+          if (t >= ntask) break;
+          float v[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) { v[2 * q] = x[z][q].x; v[2 * q + 1] = x[z][q].y; }
+          const uint32_t off = tc::kmajor_off(row, kc * 8, SBO, 128);
+          store_split8(sm + L.A + off, sm + L.A + a_half + off, v);
+        }
       }
-      const uint32_t off = tc::kmajor_off(row, kc * 8, SBO, 128);
-      store_split8(sm + L.A + off, sm + L.A + a_half + off, v);
     }
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();

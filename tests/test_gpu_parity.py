@@ -147,7 +147,7 @@ def test_no_fp32_matches_oracle(lib, n, B, w):
         assert rel_l2(got[b], ref) <= 1e-4
 
 
-@pytest.mark.parametrize("cfg_id", [2, 5])
+@pytest.mark.parametrize("cfg_id", [2, 3, 4, 5])
 def test_no_fp32_full_config_sampled(lib, cfg_id):
     cfg = sy.CONFIGS[cfg_id]
     k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
@@ -366,3 +366,62 @@ def test_repeat_solves_deterministic(lib):
     u1 = torch.zeros_like(dev(f)); s.solve(dev(f), u1); h1 = s.history.clone()
     u2 = torch.zeros_like(dev(f)); s.solve(dev(f), u2)
     assert torch.equal(u1, u2) and torch.equal(h1, s.history)
+
+
+@pytest.mark.parametrize("cfg_id", [3, 5])
+def test_fcg_no_fp32_large_configs_sampled(lib, cfg_id):
+    # Config 3 runs the tensor-core NO path (n = 128, w = 85), config 5 the FFMA fallback (n = 512).
+    # FCG amplifies NO rounding chaotically at these contrasts (config 3: a 1e-6 relative perturbation
+    # of the oracle's own NO output moves ||r_2||/||r_0|| by 1.6e-3), so histories of an
+    # fp32 NO are compared over the first step only: one NO application + one FCG update from
+    # identical state, within the fp32-NO tolerance.
+    cfg = sy.CONFIGS[cfg_id]
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    w = cfg["width"]
+    params = orc.unpack_weights(blob, w)
+    maxit = 6
+    prob = lib.Problem(dev(k))
+    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit,
+                        no=lib.NeuralOperator(w, blob, precision=lib.FP32))
+    assert np.all(host(res.status) == lib.MAXIT)
+    for b in (0, cfg["batch"] - 1):
+        ref = _oracle_fcg(k[b], f[b], cfg["m"], cfg["tol"], maxit,
+                          precond=lambda r: orc.no_forward(params, r, k[b]))
+        h = host(res.history)[b]
+        assert abs(h[1] - ref["hist"][1]) / ref["hist"][1] <= 1e-4
+        assert np.all(np.isfinite(h[:maxit + 1]))
+
+
+def test_fcg_no_fp64_config3_prefix(lib):
+    # fp64 NO mode at config 3 (n = 128, w = 85, contrast ~4e5): histories within 1e-8 over the
+    # oracle's own 1-ulp self-sensitivity window.
+    cfg = dict(sy.CONFIGS[3], batch=2)
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    w = cfg["width"]
+    params = orc.unpack_weights(blob, w)
+    maxit = 8
+    ref, window = _self_sensitivity_window(k[0], f[0], cfg["m"], cfg["tol"], maxit,
+                                           lambda r: orc.no_forward(params, r, k[0]))
+    prob = lib.Problem(dev(k))
+    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit,
+                        no=lib.NeuralOperator(w, blob, precision=lib.FP64))
+    assert window >= 2
+    assert _prefix_window_ok(host(res.history)[0], ref["hist"], window)
+
+
+def test_tc_and_ffma_paths_agree(lib):
+    # The tensor-core (3xBF16) and FFMA (fp32) NO paths compute the same map to ~1e-5.
+    import subprocess, sys, os, json
+    code = ("import json,sys,numpy as np,torch; sys.path.insert(0,'.'); import synthetic as sy;"
+            "from paper_2402_05598_b200 import fcgno as F;"
+            "k=sy.lognormal_k(64,3,0.1,1.0,5); r=sy.normal_field(64,3,6); blob=sy.no_weights(48,7);"
+            "p=F.Problem(torch.from_numpy(k).cuda()); w=F.NeuralOperator(48,blob).apply(p,torch.from_numpy(r).cuda());"
+            "np.save(sys.argv[1], w.cpu().numpy())")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for tcflag in ("1", "0"):
+        path = f"/tmp/fcgno_tc{tcflag}.npy"
+        env = dict(os.environ, FCGNO_TC=tcflag)
+        subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True)
+        outs.append(np.load(path))
+    assert rel_l2(outs[0], outs[1]) <= 5e-5
