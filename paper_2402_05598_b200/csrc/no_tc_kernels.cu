@@ -33,7 +33,20 @@ namespace fcgno {
 
 constexpr int kTcThreads = 256;
 
-__device__ __forceinline__ float gelu_f(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+// GELU(x) = x/2 (1 + erf(x / sqrt 2)) (reading R11) with a branch-free erf: Abramowitz & Stegun 7.1.26,
+// |erf error| <= 1.5e-7 (two orders below the 3xBF16 operand rounding of this path); CUDA's erff
+// branches on |x| and executes both sides under divergence.
+__device__ __forceinline__ float gelu_f(float x) {
+  const float z = fabsf(x) * 0.70710678118654752f;
+  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.0f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float pe = p * exp2f(-z * z * 1.4426950408889634f);        // erfc(z), no cancellation
+  return 0.5f * x * (x >= 0.f ? 2.0f - pe : pe);                     // 1 + erf(x/sqrt 2)
+}
 
 // 8 consecutive values -> 16 bytes of bf16 hi and 16 bytes of bf16 lo in shared memory
 __device__ __forceinline__ void store_split8(unsigned char* hi, unsigned char* lo, const float (&v)[8]) {
