@@ -76,6 +76,20 @@ def layer_flops(B, n, w, cin):
     return B * (2 * cin * w * N + 8 * K_MODES * w * N + 16 * K_MODES * K_MODES * w * n)
 
 
+def layer_bytes(B, n, w):
+    """Algorithmic HBM bytes of the three tensor-core SNO layer launches of one NO apply, averaged
+    (DESIGN.md §6): layer 1 reads r, k (fp64) and G, writes v1 and T; layer 2 reads v1, G, writes
+    v2, T; layer 3 reads v2, G, writes the 1-channel projection term p3 and T.  Activations count
+    4 B per value (bf16 hi + lo), G and T 40 values per (row, channel)."""
+    N = n * n
+    act = B * N * w * 4
+    gt = B * n * w * 40 * 4
+    l1 = 2 * B * N * 8 + gt + act + gt
+    l2 = act + gt + act + gt
+    l3 = act + gt + B * N * 4 + gt
+    return (l1 + l2 + l3) / 3
+
+
 def mean_window(m, iters):
     import synthetic  # noqa: F401
     tot = 0
@@ -234,9 +248,9 @@ def run_ours(args):
     # dominant kernel: the SNO layer kernel (3 launches per iteration), timed in-graph
     layer_ms, layer_n = prof["k_no_layer"]
     avg_layer_ms = layer_ms / max(layer_n, 1)
-    flops_iter = layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)
-    avg_flops = flops_iter / 3
-    achieved = avg_flops / (avg_layer_ms * 1e-3) / 1e12
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {"hbm_gbs": 6650.0}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -244,23 +258,35 @@ def run_ours(args):
             traffic = json.load(open(tpath)).get(f"config{args.config}", {}).get("k_no_layer")
         except (ValueError, OSError):
             traffic = None
-    roofline = {"kernel": "k_no_layer", "bound": "alu", "achieved": achieved, "peak": FP32_ALU_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": achieved / FP32_ALU_PEAK_TFLOPS, "traffic": traffic,
-                "flops_per_launch": avg_flops, "avg_launch_ms": avg_layer_ms, "launches_timed": layer_n,
-                "share_of_step": layer_ms / local_ms,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (FFMA path; DESIGN.md §6)"}
+    tc_path = cfg["no_precision"] == "fp32" and 64 <= n <= 128 and n % 16 == 0 and w <= 128
+    if tc_path:
+        # tcgen05 3xBF16 layer (k_tc_layer): activations stream through HBM; the MMA work (3 split
+        # passes, padding included) needs < 1/3 of the HBM time, so the bound is HBM.
+        alg = layer_bytes(B, n, w)
+        achieved = alg / (avg_layer_ms * 1e-3) / 1e9
+        roofline = {"kernel": "k_tc_layer", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": alg,
+                    "avg_launch_ms": avg_layer_ms, "launches_timed": layer_n, "share_of_step": layer_ms / local_ms,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, measured on this pool)",
+                    "useful_tflops": (layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)) / 3 / (avg_layer_ms * 1e-3) / 1e12}
+    else:
+        flops_iter = layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)
+        avg_flops = flops_iter / 3
+        achieved = avg_flops / (avg_layer_ms * 1e-3) / 1e12
+        roofline = {"kernel": "k_no_layer", "bound": "alu", "achieved": achieved, "peak": FP32_ALU_PEAK_TFLOPS,
+                    "unit": "TFLOP/s", "frac": achieved / FP32_ALU_PEAK_TFLOPS, "traffic": traffic,
+                    "flops_per_launch": avg_flops, "avg_launch_ms": avg_layer_ms, "launches_timed": layer_n,
+                    "share_of_step": layer_ms / local_ms,
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (FFMA path; DESIGN.md §6)"}
 
     # per-iteration HBM roofline (the metric's second half)
-    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
-        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6650.0}
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
     m_bar = mean_window(m, cfg["maxit"])
     bytes_iter = fcg_no_bytes_per_unknown(m_bar, w) * N * B
     hbm_frac = (bytes_iter / (hbm * 1e9)) / (ms_per_iter * 1e-3)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32 (NO) + f64 (FCG vectors, dots)",
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16x3 split (NO tensor cores, fp32 accumulate) + f64 (FCG vectors, dots)",
            "data": "synthetic (seeded; BASELINE configs[1] recipe, random-init NO weights)",
            "config": {"workload": f"config{args.config}", "n": n, "batch": B, "m": m, "tol": cfg["tol"],
                       "maxit": cfg["maxit"], "no_width": w, "no_precision": cfg["no_precision"],
@@ -299,7 +325,7 @@ def time_split(F, prob, no, cfg, df, iters=64):
     it = iters
     per = {name: ms / it for name, (ms, cnt) in prof.items() if cnt}
     stencil = per.get("k_stencil_dots", 0.0)
-    no_ms = sum(per.get(x, 0.0) for x in ("k_no_layer", "k_mix", "k_no_out", "k_dft_rows+k_lift_mix"))
+    no_ms = sum(per.get(x, 0.0) for x in ("k_no_layer", "k_mix", "k_no_out", "k_dft_rows+k_lift_mix", "k_yan+k_ysyn"))
     upd = sum(per.get(x, 0.0) for x in ("k_window_dots", "k_pform", "k_update", "k_finalize"))
     return {"stencil": stencil, "no": no_ms, "fcg_update": upd, "per_kernel": per,
             "note": "CUDA events around every launch inside the graph (instrumented run, 64 iterations)"}

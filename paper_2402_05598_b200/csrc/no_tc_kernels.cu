@@ -35,17 +35,27 @@ constexpr int kTcThreads = 256;
 
 // GELU(x) = x/2 (1 + erf(x / sqrt 2)) (reading R11) with a branch-free erf: Abramowitz & Stegun 7.1.26,
 // |erf error| <= 1.5e-7 (two orders below the 3xBF16 operand rounding of this path); CUDA's erff
-// branches on |x| and executes both sides under divergence.
+// branches on |x| and executes both sides under divergence.  The reciprocal and the exponential
+// are single MUFU operations (relative error ~2^-22, far inside the A&S bound).
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float gelu_f(float x) {
-  const float z = fabsf(x) * 0.70710678118654752f;
-  const float t = __frcp_rn(fmaf(0.3275911f, z, 1.0f));
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x), 1.0f));   // 1 / (1 + p z), z = |x|/sqrt 2
   float p = fmaf(1.061405429f, t, -1.453152027f);
   p = fmaf(p, t, 1.421413741f);
   p = fmaf(p, t, -0.284496736f);
   p = fmaf(p, t, 0.254829592f);
   p *= t;
-  const float pe = p * exp2f(-z * z * 1.4426950408889634f);        // erfc(z), no cancellation
-  return 0.5f * x * (x >= 0.f ? 2.0f - pe : pe);                     // 1 + erf(x/sqrt 2)
+  const float pe = p * ex2_approx((x * x) * -0.72134752044448170f);   // erfc(z) = p e^{-z^2}, z^2 = x^2 / 2
+  return 0.5f * x * (x >= 0.f ? 2.0f - pe : pe);                      // 1 + erf(x/sqrt 2)
 }
 
 // 8 consecutive values -> 16 bytes of bf16 hi and 16 bytes of bf16 lo in shared memory
@@ -56,11 +66,7 @@ __device__ __forceinline__ void store_split8(unsigned char* hi, unsigned char* l
   *reinterpret_cast<uint4*>(lo) = l;
 }
 
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&u)[8]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
-               : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
-               : "r"(taddr));
-}
+using tc::tmem_ld8;
 
 // ------------------------------------------------------------------ constant operand blobs
 // Built once per NO apply / solve by k_tc_prep (outside the iteration graph) and bulk-copied by
@@ -500,6 +506,355 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }
 
+// ------------------------------------------------------------------ k_tc_layer_ws: pipelined layer
+// Same arithmetic as k_tc_layer; one CTA (16 warps) per SM, split into two groups of 8 warps that
+// take the CTA's tiles alternately (group e: tiles it = e, e+2, ...).  Each group's leader thread
+// issues its own MMAs at the points its data is ready -- no dedicated producer / MMA warps, so no
+// thread spins and all 16 warps keep the 128-register budget:
+//   after epilogue 1 of tile it:  D2(it) and D1(it + 2) (separate TMEM accumulators)
+//   after D1(it) completed:       bulk loads of tile it + S into the stage D1(it) consumed
+// so the tensor pipe runs a group's next D1 under its epilogue 2, the other group's epilogues run
+// under this group's MMAs, and loads run S tiles ahead.  TMEM (512 columns): per group e, D1 at
+// e*n, D2 at 2n + 48e, v' hi|lo at 2n + 96 + e*n; Wbd hi|lo at 4n + 96 (needs 4n + 96 + KB <= 512).
+constexpr int kWsGroupWarps = 8;
+constexpr int kWsThreads = 2 * kWsGroupWarps * 32;
+constexpr int kWsStages = 3;
+constexpr int kWsMaxTiles = 2048;   // per-CTA tile list cached in shared memory
+
+struct TcWsSmem {
+  uint32_t BV, AG, RK, BF, TS, PJ, bar, tptr, bias, list, total;
+  int KB, CP, stages;
+  __host__ __device__ TcWsSmem(const TcGeom& g, int cin, int stages_) : stages(stages_) {
+    CP = (cin + 7) & ~7;
+    KB = (g.R * CP + 15) & ~15;
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
+    BV = take((uint32_t)stages * bv_stage_bytes(g));
+    AG = take((uint32_t)stages * 2u * g.g_half());
+    RK = take(cin == 2 ? (uint32_t)stages * 2u * g.R * g.n * 8 : 16u);
+    BF = take(2u * (uint32_t)g.n * kKS * 2);
+    TS = take(2u * ts_bytes(g));
+    PJ = take(2u * pj_bytes(g));
+    bar = take(256);           // mbarriers + TMEM pointer + tile count
+    tptr = bar + 192;
+    bias = take(128 * 4);
+    list = take(kWsMaxTiles * 4);
+    total = o;
+  }
+  __host__ __device__ uint32_t bv_stage_bytes(const TcGeom& g) const { return 2u * (uint32_t)g.n * KB * 2; }
+  __host__ __device__ static uint32_t ts_bytes(const TcGeom& g) { return 2u * (2 * g.R) * (uint32_t)(g.mtiles * 128) * 2; }
+  __host__ __device__ static uint32_t pj_bytes(const TcGeom& g) { return 4u * g.R * (uint32_t)g.n * 4; }
+};
+
+__host__ __device__ inline bool ws_tmem_fits(const TcGeom& g, int KB) { return 4 * g.n + 2 * kKS + KB <= 512; }
+
+template <int WP, bool FIRST>
+__global__ void __launch_bounds__(kWsThreads, 1) k_tc_layer_ws(const TcLayerArgs a, const int stages) {
+  const TcGeom g(a.n, a.w);
+  const TcConst C(g);
+  constexpr int R = 128 / WP;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int n = a.n, N = n * n, w = a.w, cin = a.cin;
+  const TcWsSmem L(g, cin, stages);
+  const int KB = L.KB, CP = L.CP;
+  const uint32_t SBO_AW = (KB / 8) * 128, SBO_BV = (KB / 8) * 128, SBO_AG = g.g_sbo(), SBO_F = (kKS / 8) * 128;
+  const uint32_t aw_half = 128u * KB * 2, bv_half = (uint32_t)KB * n * 2, bf_half = (uint32_t)n * kKS * 2;
+  const uint32_t g_half = g.g_half(), rk_bytes = (uint32_t)R * n * 8;
+  const uint32_t vout_half = g.v_half(), vout_sbo = g.v_sbo();
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);
+  uint64_t* full = bar;          // [3] stage loaded (layer 1: raw fp64 rows and G landed)
+  uint64_t* d1full = bar + 4;    // [2] D1 of group e's current tile complete
+  uint64_t* d2full = bar + 6;    // [2] D2 complete
+  uint64_t* cstb = bar + 8;      // constant x-direction twiddles landed
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
+  int* pcnt = reinterpret_cast<int*>(sm + L.tptr + 4);
+  float* sbias = reinterpret_cast<float*>(sm + L.bias);
+  int* list = reinterpret_cast<int*>(sm + L.list);
+  const bool proj = a.pout != nullptr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ntiles = a.B * g.tiles_per_sys;
+  const uint32_t sm_base = tc::smem_u32(sm);
+
+  auto issue_loads = [&](int it) {   // one thread: bulk copies of list[it] into stage it % stages
+    const int tile = list[it], s = it % stages;
+    const int tb = tile / g.tiles_per_sys, ti0 = (tile % g.tiles_per_sys) * R;
+    unsigned char* ag = sm + L.AG + (uint32_t)s * 2u * g_half;
+    if (FIRST) {
+      unsigned char* rk = sm + L.RK + (uint32_t)s * 2u * rk_bytes;
+      const size_t e = (size_t)tb * N + (size_t)ti0 * n;
+      tc::mbar_expect_tx(&full[s], 2u * rk_bytes + 2u * g_half);
+      tc::bulk_g2s(rk, a.r + e, rk_bytes, &full[s]);
+      tc::bulk_g2s(rk + rk_bytes, a.k + e, rk_bytes, &full[s]);
+    } else {
+      tc::mbar_expect_tx(&full[s], 2u * bv_half + 2u * g_half);
+      tc::bulk_g2s(sm + L.BV + (uint32_t)s * L.bv_stage_bytes(g), a.vin + (size_t)tile * 2 * bv_half, 2u * bv_half, &full[s]);
+    }
+    tc::bulk_g2s(ag, a.G + (size_t)tile * 2 * g_half, 2u * g_half, &full[s]);
+  };
+
+  if (tid == 0) {
+    for (int q = 0; q < 9; ++q) tc::mbar_init(&bar[q], 1);
+    tc::fence_mbar_init();
+    tc::mbar_expect_tx(cstb, 2u * bf_half);
+    tc::bulk_g2s(sm + L.BF, a.cst + C.BF, 2u * bf_half, cstb);
+  }
+  pdl_wait();
+  if (tid == 0) {   // this CTA's tiles (running systems only), in order
+    int cnt = 0;
+    for (int t = blockIdx.x; t < ntiles && cnt < kWsMaxTiles; t += gridDim.x)
+      if (!a.status || a.status[t / g.tiles_per_sys] == SYS_RUNNING) list[cnt++] = t;
+    *pcnt = cnt;
+    for (int it = 0; it < cnt && it < stages; ++it) issue_loads(it);
+  }
+  if (warp == 0) tc::tmem_alloc(tptr, 512);
+  for (int t = tid; t < 128; t += blockDim.x) {
+    const int o = t / R;
+    sbias[t] = o < w ? a.bias[o] : 0.f;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  pdl_trigger();   // after the TMEM allocation: a dependent CTA placed on this SM cannot take the columns first
+  const uint32_t tmem = *tptr;
+  const int cnt = *pcnt;
+  const uint32_t tWh = tmem + 4u * n + 2u * kKS, tWl = tWh + (uint32_t)(KB / 2);
+  if (warp < 4) {   // Wbd rows into TMEM (lane = (o, r)) from the prebuilt K-major blob
+    const int Lr = warp * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const unsigned char* aw = a.cst + C.AW[a.layer];
+    for (int k0 = 0; k0 < KB; k0 += 16) {
+      uint32_t hi8[8], lo8[8];
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const uint32_t off = tc::kmajor_off(Lr, k0 + 8 * hh, SBO_AW, 128);
+        const uint4 h = __ldg(reinterpret_cast<const uint4*>(aw + off));
+        const uint4 l = __ldg(reinterpret_cast<const uint4*>(aw + aw_half + off));
+        hi8[4 * hh] = h.x; hi8[4 * hh + 1] = h.y; hi8[4 * hh + 2] = h.z; hi8[4 * hh + 3] = h.w;
+        lo8[4 * hh] = l.x; lo8[4 * hh + 1] = l.y; lo8[4 * hh + 2] = l.z; lo8[4 * hh + 3] = l.w;
+      }
+      tc::tmem_st8(tWh + lane_off + k0 / 2, hi8);
+      tc::tmem_st8(tWl + lane_off + k0 / 2, lo8);
+    }
+    tc::tmem_wait_st();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+
+  const int grp = warp / kWsGroupWarps, q4 = warp & 3, slice = (warp >> 2) & 1;
+  const bool leader = (warp % kWsGroupWarps) == 0 && lane == 0;
+  constexpr uint32_t kGrpThreads = kWsGroupWarps * 32;
+  const uint32_t nbar = 1 + grp;
+  const int gtid = tid - grp * (int)kGrpThreads;
+  const uint32_t tD1 = tmem + (uint32_t)(grp * n), tD2 = tmem + 2u * n + (uint32_t)(grp * kKS);
+  const uint32_t tA = tmem + 2u * n + 2u * kKS + (uint32_t)(grp * n), tAl = tA + (uint32_t)(n / 2);
+  const uint32_t id1 = tc::make_idesc_bf16(128, n, false, true);
+  const uint32_t id1s = tc::make_idesc_bf16(128, n, false, false);
+  const uint32_t id2 = tc::make_idesc_bf16(128, kKS, false, true);
+
+  // layer 1: V = [r/||r||, k] of tile list[it] from its raw fp64 rows, by the group's 256 threads
+  auto convert = [&](int it) {
+    const int s = it % stages, tile = list[it], tb = tile / g.tiles_per_sys;
+    tc::mbar_wait(&full[s], (uint32_t)(it / stages) & 1);
+    const double sr = sqrt(a.rr[tb]);
+    const double inv_s = sr > 0.0 ? 1.0 / sr : 0.0;
+    const double* rkd = reinterpret_cast<const double*>(sm + L.RK + (uint32_t)s * 2u * rk_bytes);
+    unsigned char* bv = sm + L.BV + (uint32_t)s * L.bv_stage_bytes(g);
+    for (int t = gtid; t < KB * (n / 8); t += kGrpThreads) {
+      const int kk = t % KB, jc = t / KB, rp = kk / CP, c = kk % CP;
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = 0.f;
+      if (rp < R && c < cin) {
+        const double* src = rkd + (size_t)c * R * n + (size_t)rp * n + jc * 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = (float)(c == 0 ? src[q] * inv_s : src[q]);
+      }
+      const uint32_t off = tc::mnmajor_off(jc * 8, kk, SBO_BV, 128);
+      store_split8(bv + off, bv + bv_half + off, v);
+    }
+    tc::fence_proxy_async_smem();
+  };
+  // leader: D1 = Wbd V + G Basis of tile list[it] into this group's D1 accumulator
+  auto issue_d1 = [&](int it) {
+    const int s = it % stages;
+    if (!FIRST) tc::mbar_wait(&full[s], (uint32_t)(it / stages) & 1);
+    tc::fence_after_sync();
+    const uint32_t bvs = L.BV + (uint32_t)s * L.bv_stage_bytes(g), ags = L.AG + (uint32_t)s * 2u * g_half;
+    uint32_t acc = 0;
+    for (int q = 0; q < KB / 16; ++q) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const uint32_t at = (p == 2 ? tWl : tWh) + 8u * q, bo = bvs + (p == 1 ? bv_half : 0u) + 256u * q;
+        tc::mma_bf16_ts(tD1, at, tc::make_sdesc(sm_base + bo, 128, SBO_BV), id1, acc);
+        acc = 1;
+      }
+    }
+    for (int q = 0; q < kKS / 16; ++q) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const uint32_t ao = ags + (p == 2 ? g_half : 0u) + 256u * q, bo = L.BF + (p == 1 ? bf_half : 0u) + 256u * q;
+        tc::mma_bf16(tD1, tc::make_sdesc(sm_base + ao, 128, SBO_AG), tc::make_sdesc(sm_base + bo, 128, SBO_F), id1s, 1);
+      }
+    }
+    tc::mma_commit(&d1full[grp]);
+  };
+  // leader: D2 = v' F (x-analysis) of the group's current tile
+  auto issue_d2 = [&]() {
+    tc::fence_after_sync();
+    uint32_t acc = 0;
+    for (int q = 0; q < n / 16; ++q) {
+#pragma unroll
+      for (int p = 0; p < 3; ++p) {
+        const uint32_t at = (p == 2 ? tAl : tA) + 8u * q;
+        const uint64_t bd = tc::make_sdesc(sm_base + L.BF + (p == 1 ? bf_half : 0u) + 2u * SBO_F * q, SBO_F, 128);
+        tc::mma_bf16_ts(tD2, at, bd, id2, acc);
+        acc = 1;
+      }
+    }
+    tc::mma_commit(&d2full[grp]);
+  };
+
+  const int Lr = q4 * 32 + lane, r = Lr % R, o = Lr / R;
+  const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+  const bool live = (32 * q4) / R < g.CP;            // warp holds at least one real channel row
+  const float bo = sbias[Lr];
+  const float dwo = (proj && o < w) ? a.dw[o] : 0.f;
+  const bool store = o < g.CP;
+  const uint32_t kk = (uint32_t)(r * g.CP + o);
+  const int nch = n / 8;                               // 8-column chunks of D1; slice takes c = slice + 2k
+  const int MT = g.mtiles * 128;
+  __nv_bfloat16* ts = reinterpret_cast<__nv_bfloat16*>(sm + L.TS + (uint32_t)grp * TcWsSmem::ts_bytes(g));
+  float* pj = reinterpret_cast<float*>(sm + L.PJ + (uint32_t)grp * TcWsSmem::pj_bytes(g));
+
+  if (grp < cnt) {   // the group's first tile: stage it and start its D1
+    if (FIRST) {
+      tc::mbar_wait(cstb, 0);
+      convert(grp);
+      tc::named_sync(nbar, kGrpThreads);
+    }
+    if (leader) {
+      tc::mbar_wait(cstb, 0);
+      issue_d1(grp);
+    }
+  }
+  for (int it = grp; it < cnt; it += 2) {
+    const int tile = list[it], b = tile / g.tiles_per_sys, i0 = (tile % g.tiles_per_sys) * R;
+    const uint32_t par = (uint32_t)(it >> 1) & 1;
+    tc::mbar_wait(&d1full[grp], par);
+    tc::fence_after_sync();
+    if (leader && it + stages < cnt) issue_loads(it + stages);   // D1(it) has consumed stage it % S
+    // ---- epilogue 1: v' = GELU(D1 + b) -> next V blob and TMEM (A of D2); layer 3: projection partials
+    if (live) {
+      unsigned char* vb = a.vout + (size_t)tile * 2 * vout_half;
+      for (int c00 = slice; c00 < nch; c00 += 8) {       // batches of up to 4 chunks: c00, c00 + 2, ...
+        uint32_t u[4][8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (c00 + 2 * k < nch) tmem_ld8(tD1 + lane_off + 8 * (c00 + 2 * k), u[k]);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = c00 + 2 * k;
+          if (c >= nch) break;
+          float v[8];
+#pragma unroll
+          for (int t = 0; t < 8; ++t) {
+            const float x = __uint_as_float(u[k][t]) + bo;
+            v[t] = a.use_gelu ? gelu_f(x) : x;
+          }
+          uint32_t ph4[4], pl4[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) tc::split2(v[2 * t], v[2 * t + 1], ph4[t], pl4[t]);
+          if (proj) {
+            float pp[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) pp[t] = dwo * v[t];
+#pragma unroll
+            for (int off = 16; off >= R; off >>= 1)
+#pragma unroll
+              for (int t = 0; t < 8; ++t) pp[t] += __shfl_xor_sync(0xffffffffu, pp[t], off);
+            if (lane < R) {
+              float4* dst = reinterpret_cast<float4*>(pj + ((size_t)q4 * R + r) * n + 8 * c);
+              dst[0] = make_float4(pp[0], pp[1], pp[2], pp[3]);
+              dst[1] = make_float4(pp[4], pp[5], pp[6], pp[7]);
+            }
+          } else if (store) {
+            const uint32_t off = tc::mnmajor_off(8 * c, kk, vout_sbo, 128);
+            *reinterpret_cast<uint4*>(vb + off) = make_uint4(ph4[0], ph4[1], ph4[2], ph4[3]);
+            *reinterpret_cast<uint4*>(vb + vout_half + off) = make_uint4(pl4[0], pl4[1], pl4[2], pl4[3]);
+          }
+          tc::tmem_st4(tA + lane_off + 4 * c, ph4[0], ph4[1], ph4[2], ph4[3]);
+          tc::tmem_st4(tAl + lane_off + 4 * c, pl4[0], pl4[1], pl4[2], pl4[3]);
+        }
+      }
+      tc::tmem_wait_st();
+    }
+    if (FIRST && it + 2 < cnt) convert(it + 2);      // next tile's layer-1 operand, rows landed long ago
+    tc::fence_before_sync();
+    tc::named_sync(nbar, kGrpThreads);                // v' in TMEM, D1 drained, pj written
+    if (leader) {
+      issue_d2();
+      if (it + 2 < cnt) issue_d1(it + 2);
+    }
+    if (proj) {   // fixed-order sum over the 4 lane quadrants
+      const int nq = min(4, (g.CP * R + 31) / 32);
+      for (int e = gtid; e < R * n; e += kGrpThreads) {
+        float acc = 0.f;
+        for (int q = 0; q < nq; ++q) acc += pj[(size_t)q * R * n + e];
+        a.pout[(size_t)b * N + (size_t)i0 * n + e] = acc;
+      }
+    }
+    // ---- epilogue 2: D2 -> T blob via the group's [hi|lo][k_local][m] staging buffer
+    tc::mbar_wait(&d2full[grp], par);
+    tc::fence_after_sync();
+    {
+      uint32_t u[3][8];                                // 8-column chunks of the 40 (k2, re|im) columns
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        if (slice + 2 * k < 5) tmem_ld8(tD2 + lane_off + 8 * (slice + 2 * k), u[k]);
+      tc::tmem_wait_ld();
+      if (o < w) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const int c = slice + 2 * k;
+          if (c >= 5) break;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int col = 8 * c + q, k2 = col >> 1, pin = col & 1, m = o * kModes + k2, kl = 2 * r + pin;
+            __nv_bfloat16 h, l;
+            tc::split_bf16(__uint_as_float(u[k][q]), h, l);
+            ts[(size_t)kl * MT + m] = h;
+            ts[(size_t)(2 * R + kl) * MT + m] = l;
+          }
+        }
+      }
+    }
+    tc::fence_before_sync();
+    tc::named_sync(nbar, kGrpThreads);
+    {
+      const int KL = 2 * R, k0 = 2 * i0;
+      const int ngroups = (w * kModes + 7) / 8;
+      const uint32_t t_half = g.t_half(), t_lbo = g.t_lbo();
+      unsigned char* tb = a.T + (size_t)b * g.mtiles * 2 * t_half;
+      for (int e = gtid; e < 2 * ngroups; e += kGrpThreads) {
+        const int hl = e / ngroups, gr = e % ngroups, mt = gr / 16, gi = gr % 16;
+        unsigned char* dst = tb + ((size_t)mt * 2 + hl) * t_half + (uint32_t)gi * 128 + (uint32_t)(k0 / 8) * t_lbo +
+                             (uint32_t)(k0 % 8) * 16;
+#pragma unroll 8
+        for (int kl = 0; kl < KL; ++kl)
+          *reinterpret_cast<uint4*>(dst + kl * 16) =
+              *reinterpret_cast<const uint4*>(ts + (size_t)(hl * KL + kl) * MT + gr * 8);
+      }
+    }
+    tc::named_sync(nbar, kGrpThreads);   // staging buffers (ts, pj) free for the group's next tile
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
 // ------------------------------------------------------------------ y-direction transforms on tensor cores
 // Complex products written as 2x2 real blocks (F = (Fx, Fy) = exp(-2 pi i kappa i / n)):
 //   y-synthesis  G[i][(o,k2,re|im)] = sum_{(k1,p)} Fp[i][(k1,p)] * Gh[(k1,p)][(o,k2,re|im)]
@@ -892,9 +1247,24 @@ static int num_sms() {
 
 template <int WP>
 static cudaError_t prep_tc() {
-  cudaError_t e = cudaFuncSetAttribute((const void*)k_tc_layer<WP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute((const void*)k_tc_layer<WP, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  const void* fns[4] = {(const void*)k_tc_layer<WP, true>, (const void*)k_tc_layer<WP, false>,
+                        (const void*)k_tc_layer_ws<WP, true>, (const void*)k_tc_layer_ws<WP, false>};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// FCGNO_TC_WS=1 selects the pipelined two-group layer kernel (k_tc_layer_ws).  Default: k_tc_layer
+// with two CTAs per SM, measured faster on B200.
+static bool ws_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FCGNO_TC_WS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 cudaError_t prepare_tc_kernels() {
@@ -918,6 +1288,26 @@ cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s) {
   a.vout = h.vout; a.T = h.T; a.dw = h.dw; a.pout = h.pout; a.status = h.status;
   const TcGeom g(h.n, h.w);
   const int ntiles = h.B * g.tiles_per_sys;
+  if (ws_enabled()) {
+    int stages = kWsStages;
+    while (stages > 1 && TcWsSmem(g, h.cin, stages).total > (uint32_t)optin_bytes()) --stages;
+    const size_t wsmem = TcWsSmem(g, h.cin, stages).total;
+    if (wsmem <= (size_t)optin_bytes() && ws_tmem_fits(g, TcWsSmem(g, h.cin, stages).KB) &&
+        (ntiles + num_sms() - 1) / num_sms() <= kWsMaxTiles) {
+      const int grid = std::min(ntiles, num_sms());
+      if (g.WP == 32) {
+        if (h.first) launch_k(k_tc_layer_ws<32, true>, dim3(grid), dim3(kWsThreads), wsmem, s, a, stages);
+        else launch_k(k_tc_layer_ws<32, false>, dim3(grid), dim3(kWsThreads), wsmem, s, a, stages);
+      } else if (g.WP == 64) {
+        if (h.first) launch_k(k_tc_layer_ws<64, true>, dim3(grid), dim3(kWsThreads), wsmem, s, a, stages);
+        else launch_k(k_tc_layer_ws<64, false>, dim3(grid), dim3(kWsThreads), wsmem, s, a, stages);
+      } else {
+        if (h.first) launch_k(k_tc_layer_ws<128, true>, dim3(grid), dim3(kWsThreads), wsmem, s, a, stages);
+        else launch_k(k_tc_layer_ws<128, false>, dim3(grid), dim3(kWsThreads), wsmem, s, a, stages);
+      }
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = TcSmem(g, h.cin).total;
   // persistent grid: as many CTAs as fit per SM by shared memory (<= 2) and TMEM columns
   const uint32_t need_cols = 2u * h.n + (uint32_t)TcSmem(g, h.cin).KB;
