@@ -93,8 +93,10 @@ typedef struct {
   int32_t check_every;  /* iterations per convergence poll and per CUDA-graph replay (0 = default
                            16); work on converged systems stops immediately regardless, this only
                            bounds idle tail launches */
-  int32_t profile_mask; /* bit c set: time every launch of kernel class c (fcgno_prof_class) with
-                           CUDA events recorded inside the solve's graphs; 0 = no instrumentation */
+  int32_t profile_mask; /* bit c set: time the launches of kernel class c (fcgno_prof_class) in the
+                           first unrolled iteration of every graph chunk (one sampled iteration
+                           per check_every) with CUDA events recorded inside the solve's graphs;
+                           0 = no instrumentation */
 } fcgno_solve_opts;
 
 /* Kernel classes for in-graph CUDA-event profiling (diagnostics; bench.py). */

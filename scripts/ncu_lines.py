@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Warp-stall samples of an ncu --set full capture aggregated per CUDA source line.
 
-  python scripts/ncu_lines.py <report.ncu-rep> <kernel-name-substring> <mangled-function> [top]
+  python scripts/ncu_lines.py <report.ncu-rep> <kernel-name-substring> <mangled-name-substring> [top]
 
 ncu's source page in CSV form carries no line column, so the SASS rows (in address order) are
 matched by offset against `nvdisasm -g` of the in-tree library's cubin (built with -lineinfo).
@@ -25,9 +25,10 @@ def line_map(func):
                    cwd=tmp, capture_output=True)
     for cub in glob.glob(os.path.join(tmp, "*.cubin")):
         txt = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
-        start = txt.find(f".text.{func}:")
-        if start < 0:
+        m0 = re.search(r"^\.text\.(\S*" + re.escape(func) + r"\S*):", txt, re.M)
+        if not m0:
             continue
+        start = m0.start()
         end = txt.find("//--------------------- .text.", start)
         txt = txt[start:end if end > 0 else len(txt)]
         cur, m = None, {}
