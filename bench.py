@@ -323,11 +323,11 @@ def time_split(F, prob, no, cfg, df, iters=64):
     s.solve(df, u)
     torch.cuda.synchronize()
     prof = F.profile_read()
-    it = max(prof.get("k_stencil_dots", (0.0, 0))[1], 1)   # sampled iterations (one stencil launch each)
+    it = max(prof.get("k_pform_stencil", (0.0, 0))[1], 1)   # sampled iterations (one stencil launch each)
     per = {name: ms / it for name, (ms, cnt) in prof.items() if cnt}
-    stencil = per.get("k_stencil_dots", 0.0)
+    stencil = per.get("k_pform_stencil", 0.0)
     no_ms = sum(per.get(x, 0.0) for x in ("k_no_layer", "k_mix", "k_no_out", "k_dft_rows+k_lift_mix", "k_yan+k_ysyn"))
-    upd = sum(per.get(x, 0.0) for x in ("k_window_dots", "k_pform", "k_update", "k_finalize"))
+    upd = sum(per.get(x, 0.0) for x in ("k_window_dots", "k_update"))
     return {"stencil": stencil, "no": no_ms, "fcg_update": upd, "per_kernel": per,
             "note": "CUDA events around every launch of the first unrolled iteration of each graph chunk "
                     "(instrumented run, 64 iterations; per sampled iteration)"}

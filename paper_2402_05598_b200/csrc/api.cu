@@ -446,7 +446,8 @@ SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgn
   d.part_win = c.take<dd>((size_t)B * nblk * kMmax);
   d.part_step = c.take<dd>((size_t)B * nblk * 2);
   d.part_rr = c.take<dd>((size_t)B * nblk);
-  d.cnt = c.take<unsigned>((size_t)3 * B);
+  d.cnt = c.take<unsigned>((size_t)3 * B + 2);
+  d.gcnt = d.cnt + (size_t)3 * B;
   d.flags = c.take<int>(B);
   d.iter = c.take<int>(2);
   d.active = d.iter + 1;
@@ -545,19 +546,13 @@ int enqueue_iteration(const FcgDev& d, const fcgno_no_desc* nd, const void* pack
     pe(PROF_WINDOW);
     ++count;
   }
-  pb(PROF_PFORM);
-  if (launch_pform(d, s) != cudaSuccess) return -1;
-  pe(PROF_PFORM);
   pb(PROF_STENCIL);
-  if (launch_stencil_dots(d, s) != cudaSuccess) return -1;
+  if (launch_pform_stencil(d, s) != cudaSuccess) return -1;
   pe(PROF_STENCIL);
   pb(PROF_UPDATE);
   if (launch_update(d, s) != cudaSuccess) return -1;
   pe(PROF_UPDATE);
-  pb(PROF_FINALIZE);
-  if (launch_finalize(d, s) != cudaSuccess) return -1;
-  pe(PROF_FINALIZE);
-  return count + 4;
+  return count + 2;
 }
 
 // A CUDA graph replaying `iters` unrolled FCG iterations (+ its profiling events).
@@ -702,7 +697,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     for (int l = 0; l < nl && rc == FCGNO_OK; ++l) {
       const FcgDev& d = lanes[l].sw.d;
       const SolveWs& sw = lanes[l].sw;
-      if ((e = cudaMemsetAsync(d.cnt, 0, sizeof(unsigned) * 3 * d.B, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+      if ((e = cudaMemsetAsync(d.cnt, 0, sizeof(unsigned) * (3 * d.B + 2), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if ((e = cudaMemsetAsync(d.iter, 0, 2 * sizeof(int), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if (nd && sw.n32.Gb) {   // blob padding must read as zeros
         if ((e = cudaMemsetAsync(sw.n32.vb0, 0, sw.n32.vb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
@@ -777,7 +772,7 @@ void fcgno_profile_reset(void) { prof_totals() = ProfTotals{}; }
 
 const char* fcgno_profile_name(int cls) {
   static const char* names[PROF_NCLASS] = {"k_no_layer", "k_mix", "k_no_out", "k_dft_rows+k_lift_mix",
-                                           "k_window_dots", "k_pform", "k_stencil_dots", "k_update", "k_finalize",
+                                           "k_window_dots", "(unused 5)", "k_pform_stencil", "k_update", "(unused 8)",
                                            "k_yan+k_ysyn"};
   return (cls >= 0 && cls < PROF_NCLASS) ? names[cls] : "";
 }

@@ -143,17 +143,18 @@ __device__ __forceinline__ double harmonic(double a, double b) {
   return __ddiv_rn(2.0 * __dmul_rn(a, b), __dadd_rn(a, b));
 }
 
-// y(i,j) of one system; k and x point at the system's [n][n] arrays.
+// y(i,j) of one system; k points at the system's [n][n] array, x holds the system's field from
+// element xoff on (x[e - xoff]; xoff = 0 for the whole field, > 0 for a shared-memory halo tile).
 __device__ __forceinline__ double stencil_at(const double* __restrict__ k, const double* __restrict__ x,
-                                             int n, int i, int j, double scale) {
-  const int e = i * n + j;
+                                             int n, int i, int j, double scale, int xoff = 0) {
+  const int e = i * n + j, ex = e - xoff;
   const double kc = __ldg(k + e);
-  const double xc = x[e];
+  const double xc = x[ex];
   double kW = kc, kE = kc, kS = kc, kN = kc, xW = 0.0, xE = 0.0, xS = 0.0, xN = 0.0;
-  if (j > 0)     { kW = harmonic(kc, __ldg(k + e - 1)); xW = x[e - 1]; }
-  if (j < n - 1) { kE = harmonic(kc, __ldg(k + e + 1)); xE = x[e + 1]; }
-  if (i > 0)     { kS = harmonic(kc, __ldg(k + e - n)); xS = x[e - n]; }
-  if (i < n - 1) { kN = harmonic(kc, __ldg(k + e + n)); xN = x[e + n]; }
+  if (j > 0)     { kW = harmonic(kc, __ldg(k + e - 1)); xW = x[ex - 1]; }
+  if (j < n - 1) { kE = harmonic(kc, __ldg(k + e + 1)); xE = x[ex + 1]; }
+  if (i > 0)     { kS = harmonic(kc, __ldg(k + e - n)); xS = x[ex - n]; }
+  if (i < n - 1) { kN = harmonic(kc, __ldg(k + e + n)); xN = x[ex + n]; }
   const double d = __dadd_rn(__dadd_rn(kW, kE), __dadd_rn(kS, kN));
   double t = __dmul_rn(d, xc);
   t = __dsub_rn(t, __dmul_rn(kW, xW));

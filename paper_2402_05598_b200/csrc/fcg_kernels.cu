@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(kThreads) k_init_residual(FcgDev d) {
       d.iters[b] = 0;
       if (d.hist) d.hist[(size_t)b * (d.maxit + 1)] = 1.0;
       d.status[b] = (rho0 == 0.0) ? SYS_CONVERGED : (d.maxit == 0 ? SYS_MAXIT : SYS_RUNNING);
+      if (d.status[b] == SYS_RUNNING) atomicAdd(d.active, 1);
     }
   }
 }
@@ -178,67 +179,55 @@ cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ p = w - sum beta_k p_k
-__global__ void __launch_bounds__(kThreads) k_pform(FcgDev d) {
+// ------------------------------------------------------------------ p = w - sum beta_k p_k ; s = A p ; (p,s), (p,r)
+// One CTA per (tile of kTile elements, system).  p is formed for the tile plus a one-row halo on
+// each side (the halo values are recomputed here, bit-identical to the owning CTA's), kept in
+// shared memory for the stencil, and written to the ring for the tile only.
+__global__ void __launch_bounds__(kThreads) k_pform_stencil(FcgDev d) {
   pdl_wait();
   pdl_trigger();
+  extern __shared__ __align__(16) double sp[];   // p over [lo, hi)
+  __shared__ dd sm[16];
+  __shared__ double sbeta[kMmax];
+  __shared__ int sslot[kMmax];
   const int b = blockIdx.y;
   if (d.status[b] != SYS_RUNNING) return;
   const int i = *d.iter;
   const int mi = m_schedule(i, d.m, d.schedule);
-  const int N = d.N;
-  __shared__ double sbeta[kMmax];
-  __shared__ int sslot[kMmax];
+  const int N = d.N, n = d.n, slot = ring_slot(i, d.m);
+  const int e0 = blockIdx.x * kTile, e1 = min(N, e0 + kTile);
+  const int lo = max(0, e0 - n), hi = min(N, e1 + n);
   for (int q = threadIdx.x; q < mi; q += blockDim.x) {
     sbeta[q] = d.beta[(size_t)b * kMmax + q];
     sslot[q] = ring_slot(i - mi + q, d.m);
   }
   __syncthreads();
-  double* pout = d.ring_p + ((size_t)ring_slot(i, d.m) * d.B + b) * N;
+  double* pout = d.ring_p + ((size_t)slot * d.B + b) * N;
+  const double* wb = d.w + (size_t)b * N;
   int bad = 0;
-#pragma unroll
-  for (int q = 0; q < kPerThread; ++q) {
-    const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
-    if (e < N) {
-      const double wv = d.w[(size_t)b * N + e];
+  for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
+    const double wv = wb[e];
+    double p = wv;
+    for (int t = mi - 1; t >= 0; --t)   // newest -> oldest (R13)
+      p = __dsub_rn(p, __dmul_rn(sbeta[t], d.ring_p[((size_t)sslot[t] * d.B + b) * N + e]));
+    sp[e - lo] = p;
+    if (e >= e0 && e < e1) {
       if (!isfinite(wv)) bad = 1;
-      double p = wv;
-      for (int t = mi - 1; t >= 0; --t)   // newest -> oldest (R13)
-        p = __dsub_rn(p, __dmul_rn(sbeta[t], d.ring_p[((size_t)sslot[t] * d.B + b) * N + e]));
       pout[e] = p;
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d.flags + b, FLAG_NONFINITE);
-}
-
-cudaError_t launch_pform(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e = launch_k(k_pform, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
-  if (e != cudaSuccess) return e;
-  ++launch_counter();
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ s = A p ; (p,s), (p,r)
-__global__ void __launch_bounds__(kThreads) k_stencil_dots(FcgDev d) {
-  pdl_wait();
-  pdl_trigger();
-  __shared__ dd sm[16];
-  const int b = blockIdx.y;
-  if (d.status[b] != SYS_RUNNING) return;
-  const int i = *d.iter;
-  const int N = d.N, slot = ring_slot(i, d.m);
   const double* kb = d.k + (size_t)b * N;
-  const double* pb = d.ring_p + ((size_t)slot * d.B + b) * N;
   double* sb = d.ring_s + ((size_t)slot * d.B + b) * N;
   double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
 #pragma unroll
   for (int q = 0; q < kPerThread; ++q) {
-    const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
+    const int e = e0 + q * kThreads + threadIdx.x;
     if (e < N) {
-      const int ii = e / d.n, j = e - ii * d.n;
-      const double sv = stencil_at(kb, pb, d.n, ii, j, d.scale);
+      const int ii = e / n, j = e - ii * n;
+      const double sv = stencil_at(kb, sp, n, ii, j, d.scale, lo);
       sb[e] = sv;
-      const double pv = pb[e];
+      const double pv = sp[e - lo];
       dot2_acc(pv, sv, s0, c0);
       dot2_acc(pv, d.r[(size_t)b * N + e], s1, c1);
     }
@@ -261,87 +250,89 @@ __global__ void __launch_bounds__(kThreads) k_stencil_dots(FcgDev d) {
   }
 }
 
-cudaError_t launch_stencil_dots(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e = launch_k(k_stencil_dots, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+size_t pform_stencil_smem(int n) { return (size_t)(kTile + 2 * n) * sizeof(double); }
+
+cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s) {
+  static size_t set = 0;
+  const size_t smem = pform_stencil_smem(d.n);
+  if (smem > 48 * 1024 && smem > set) {   // never during graph capture of a smaller size
+    const cudaError_t e = cudaFuncSetAttribute((const void*)k_pform_stencil, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    set = smem;
+  }
+  cudaError_t e = launch_k(k_pform_stencil, sys_grid(d.nblk, d.B), dim3(kThreads), smem, s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ u += alpha p ; r -= alpha s ; (r,r)
+// ------------------------------------------------------------------ u += alpha p ; r -= alpha s ; (r,r) ; bookkeeping
+// The last CTA of each system reduces (r, r) and applies the system's convergence / breakdown
+// bookkeeping (Algorithm 1's stopping test); the last system to arrive publishes the number of
+// systems still running and advances the iteration counter.  Systems flagged this iteration
+// skip the vector update but still take part in the arrival protocol.
 __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
   pdl_wait();
   pdl_trigger();
   __shared__ dd sm[8];
   const int b = blockIdx.y;
-  if (d.status[b] != SYS_RUNNING || d.flags[b] != 0) return;
+  if (d.status[b] != SYS_RUNNING) return;
   const int i = *d.iter;
+  const int fl = d.flags[b];
   const int N = d.N, slot = ring_slot(i, d.m);
-  const double alpha = d.alpha[b];
-  const double* pb = d.ring_p + ((size_t)slot * d.B + b) * N;
-  const double* sb = d.ring_s + ((size_t)slot * d.B + b) * N;
   double s = 0.0, c = 0.0;
+  if (fl == 0) {
+    const double alpha = d.alpha[b];
+    const double* pb = d.ring_p + ((size_t)slot * d.B + b) * N;
+    const double* sb = d.ring_s + ((size_t)slot * d.B + b) * N;
 #pragma unroll
-  for (int q = 0; q < kPerThread; ++q) {
-    const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
-    if (e < N) {
-      const size_t g = (size_t)b * N + e;
-      d.u[g] = __dadd_rn(d.u[g], __dmul_rn(alpha, pb[e]));
-      const double rv = __dsub_rn(d.r[g], __dmul_rn(alpha, sb[e]));
-      d.r[g] = rv;
-      dot2_acc(rv, rv, s, c);
+    for (int q = 0; q < kPerThread; ++q) {
+      const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
+      if (e < N) {
+        const size_t g = (size_t)b * N + e;
+        d.u[g] = __dadd_rn(d.u[g], __dmul_rn(alpha, pb[e]));
+        const double rv = __dsub_rn(d.r[g], __dmul_rn(alpha, sb[e]));
+        d.r[g] = rv;
+        dot2_acc(rv, rv, s, c);
+      }
     }
   }
   dd v[1] = {dot2_finish(s, c)};
   block_reduce_dd<1>(v, sm);
   if (threadIdx.x == 0) d.part_rr[(size_t)b * d.nblk + blockIdx.x] = v[0];
-  if (arrive_last(d.cnt + 2 * d.B + b, d.nblk)) {
+  if (!arrive_last(d.cnt + 2 * d.B + b, d.nblk)) return;
+  bool running = false;
+  if (fl == 0) {
     const dd t = block_reduce_partials(d.part_rr + (size_t)b * d.nblk, d.nblk, 1, sm);
-    if (threadIdx.x == 0) d.rr[b] = dd_round(t);
+    if (threadIdx.x == 0) {
+      const double rr = dd_round(t);
+      d.rr[b] = rr;
+      const double h = __ddiv_rn(__dsqrt_rn(rr), d.rho0[b]);
+      if (d.hist) d.hist[(size_t)b * (d.maxit + 1) + i + 1] = h;
+      if (h <= d.tol) { d.status[b] = SYS_CONVERGED; d.iters[b] = i + 1; }
+      else if (i + 1 >= d.maxit) { d.status[b] = SYS_MAXIT; d.iters[b] = d.maxit; }
+      else running = true;
+    }
+  } else if (threadIdx.x == 0) {
+    d.status[b] = (fl & FLAG_NONFINITE) ? SYS_NONFINITE : SYS_BREAKDOWN;
+    d.iters[b] = i;
+  }
+  if (threadIdx.x == 0) {
+    const int expected = *d.active;          // systems running at the start of this iteration
+    if (running) atomicAdd(d.gcnt + 1, 1u);
+    __threadfence();
+    const unsigned prev = atomicAdd(d.gcnt, 1u);
+    if (prev == (unsigned)(expected - 1)) {  // last system: publish and re-arm
+      __threadfence();
+      *d.active = (int)atomicExch(d.gcnt + 1, 0u);
+      *d.gcnt = 0u;
+      *d.iter = i + 1;
+    }
   }
 }
 
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s) {
   cudaError_t e = launch_k(k_update, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
-  if (e != cudaSuccess) return e;
-  ++launch_counter();
-  return cudaGetLastError();
-}
-
-// ------------------------------------------------------------------ convergence bookkeeping
-__global__ void __launch_bounds__(kThreads) k_finalize(FcgDev d) {
-  pdl_wait();
-  pdl_trigger();
-  const int i = *d.iter;
-  __shared__ int total;
-  if (threadIdx.x == 0) total = 0;
-  __syncthreads();
-  int running = 0;
-  for (int b = threadIdx.x; b < d.B; b += blockDim.x) {
-    if (d.status[b] != SYS_RUNNING) continue;
-    const int fl = d.flags[b];
-    if (fl & FLAG_NONFINITE) {
-      d.status[b] = SYS_NONFINITE; d.iters[b] = i;
-    } else if (fl & FLAG_BREAKDOWN) {
-      d.status[b] = SYS_BREAKDOWN; d.iters[b] = i;
-    } else {
-      const double h = __ddiv_rn(__dsqrt_rn(d.rr[b]), d.rho0[b]);
-      if (d.hist) d.hist[(size_t)b * (d.maxit + 1) + i + 1] = h;
-      if (h <= d.tol) { d.status[b] = SYS_CONVERGED; d.iters[b] = i + 1; }
-      else if (i + 1 >= d.maxit) { d.status[b] = SYS_MAXIT; d.iters[b] = d.maxit; }
-      else ++running;
-    }
-  }
-  if (running) atomicAdd(&total, running);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    *d.active = total;
-    *d.iter = i + 1;
-  }
-}
-
-cudaError_t launch_finalize(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e = launch_k(k_finalize, dim3(1), dim3(kThreads), 0, s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();

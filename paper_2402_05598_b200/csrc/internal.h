@@ -36,7 +36,8 @@ struct FcgDev {
   int* iters;                 // [B] caller
   double* hist;               // [B][maxit+1] caller or nullptr
   int* iter;                  // global iteration counter
-  int* active;                // systems still running after the last finalize
+  int* active;                // systems still running (set by init, then by the last update CTA)
+  unsigned* gcnt;             // [2] systems arrived in this update / of them still running
 };
 
 // Packed NO weights (element offsets into the packed array of T; complex = 2 T).
@@ -116,10 +117,9 @@ cudaError_t launch_dot(const double* x, const double* y, double* out, dd* part, 
 cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t s);
 cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s);
-cudaError_t launch_pform(const FcgDev& d, cudaStream_t s);
-cudaError_t launch_stencil_dots(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s);
-cudaError_t launch_finalize(const FcgDev& d, cudaStream_t s);
+size_t pform_stencil_smem(int n);
 
 cudaError_t launch_twiddles(float* F32, double* F64, int n, cudaStream_t s);
 template <typename T>
