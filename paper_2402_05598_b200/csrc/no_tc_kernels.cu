@@ -191,9 +191,11 @@ __global__ void __launch_bounds__(256) k_tc_prep(const TcPrepArgs a) {
 }
 
 // ------------------------------------------------------------------ k_tc_layer
+constexpr int kTcMaxSys = 4096;   // running-system bitmask cached in shared memory up to this batch
+
 struct TcSmem {
   // byte offsets; every region 1024-aligned; [hi][lo] back to back like their blobs
-  uint32_t BV, AG, BF, RK, TS, PJ, bar, tptr, bias, total;
+  uint32_t BV, AG, BF, RK, TS, PJ, bar, tptr, bias, runb, total;
   int KB, CP;
   __host__ __device__ TcSmem(const TcGeom& g, int cin) {
     CP = (cin + 7) & ~7;
@@ -209,6 +211,7 @@ struct TcSmem {
     bar = take(64);
     tptr = bar + 40;
     bias = take(128 * 4);
+    runb = take(kTcMaxSys / 8);
     total = o;
   }
 };
@@ -251,7 +254,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   const uint32_t need = 2u * n + (uint32_t)KB;
   const uint32_t ncols = need <= 128 ? 128u : (need <= 256 ? 256u : 512u);
   const int ntiles = a.B * g.tiles_per_sys;
-  auto running = [&](int t) { return !a.status || a.status[t / g.tiles_per_sys] == SYS_RUNNING; };
+  uint32_t* runb = reinterpret_cast<uint32_t*>(sm + L.runb);   // running-system bitmask (B <= kTcMaxSys)
+  const bool cached = a.status && a.B <= kTcMaxSys;
+  auto running = [&](int t) {
+    const int sb = t / g.tiles_per_sys;
+    if (!a.status) return true;
+    if (cached) return ((runb[sb >> 5] >> (sb & 31)) & 1u) != 0;
+    return a.status[sb] == SYS_RUNNING;
+  };
   auto next_tile = [&](int t) {
     while (t < ntiles && !running(t)) t += gridDim.x;
     return t;
@@ -280,6 +290,14 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   }
   pdl_wait();
   pdl_trigger();
+  if (cached) {
+    for (int q = warp; q < (a.B + 31) / 32; q += blockDim.x / 32) {
+      const int sb = q * 32 + lane;
+      const unsigned bits = __ballot_sync(0xffffffffu, sb < a.B && a.status[sb] == SYS_RUNNING);
+      if (lane == 0) runb[q] = bits;
+    }
+    __syncthreads();
+  }
   int tile = next_tile(blockIdx.x);
   if (tid == 0 && tile < ntiles) prefetch(tile);
   if (warp == 0) tc::tmem_alloc(tptr, ncols);
