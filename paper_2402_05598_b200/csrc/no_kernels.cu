@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
                                                   const typename Cplx<T>::type* __restrict__ A1,
                                                   const typename Cplx<T>::type* __restrict__ A2,
                                                   typename Cplx<T>::type* __restrict__ ghat, int w, T n2, T inv_n2,
-                                                  const int* __restrict__ status) {
+                                                  const int* __restrict__ status, int mode_major) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename Cplx<T>::type;
@@ -164,13 +164,20 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
   }
   __syncthreads();
   const int k0 = (kModes / 2) * kModes + kModes / 2;   // kappa = (0, 0)
-  const int olo = ochunk * 8, ohi = min(w, olo + 8), cnt = (ohi - olo) * kModes2;
+  // element e -> (o, kappa): kappa fastest for the [B][w][400] layout (FFMA path), o fastest for the
+  // mode-major [400][B][w] layout of the tensor-core path, so the stores stay contiguous
+  const int olo = ochunk * 8, ohi = min(w, olo + 8), no_ = ohi - olo, cnt = no_ * kModes2;
+  auto decode = [&](int e, int& o, int& kk) {
+    if (mode_major) { kk = e / no_; o = olo + (e - kk * no_); }
+    else { o = olo + e / kModes2; kk = e % kModes2; }
+  };
   for (int e0 = threadIdx.x; e0 < cnt; e0 += 4 * blockDim.x) {
     T2 a0[4], a1[4], kh[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int e = e0 + q * blockDim.x;
-      const int o = olo + e / kModes2, kk = e % kModes2;
+      int o, kk;
+      decode(e < cnt ? e : 0, o, kk);
       const bool ok = e < cnt;
       a0[q] = ok ? A0[(size_t)kk * w + o] : T2{T(0), T(0)};
       a1[q] = ok ? A1[(size_t)kk * w + o] : T2{T(0), T(0)};
@@ -180,12 +187,14 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
     for (int q = 0; q < 4; ++q) {
       const int e = e0 + q * blockDim.x;
       if (e >= cnt) break;
-      const int o = olo + e / kModes2, kk = e % kModes2;
+      int o, kk;
+      decode(e, o, kk);
       const T2 rh = Rh[kk];
       T gr = a0[q].x * rh.x - a0[q].y * rh.y + a1[q].x * kh[q].x - a1[q].y * kh[q].y;
       T gi = a0[q].x * rh.y + a0[q].y * rh.x + a1[q].x * kh[q].y + a1[q].y * kh[q].x;
       if (kk == k0) { gr += n2 * A2[o].x; gi += n2 * A2[o].y; }
-      ghat[((size_t)b * w + o) * kModes2 + kk] = T2{gr * inv_n2, gi * inv_n2};
+      const size_t at = mode_major ? ((size_t)kk * gridDim.x + b) * w + o : ((size_t)b * w + o) * kModes2 + kk;
+      ghat[at] = T2{gr * inv_n2, gi * inv_n2};
     }
   }
 }
@@ -494,7 +503,8 @@ struct OutArgs {
   const float* p3;                                // tensor-core path: layer-3 projection bypass term [B][N]
   const T* dw;                                    // [w]
   const T* cst;                                   // [1]
-  const typename Cplx<T>::type* gh4;              // [B][400] scaled by n^-2
+  const typename Cplx<T>::type* gh4;              // [B][400] scaled by n^-2 (tensor-core path: [400][B])
+  int B;
   const typename Cplx<T>::type* F;
   const double* rr;
   double* wout;                                   // [B][N]
@@ -595,7 +605,7 @@ __global__ void __launch_bounds__(kThreads) k_no_out_blob(const OutArgs<float> a
   float* dws = reinterpret_cast<float*>(Gs + (size_t)nr_max * kModes);
   float* outs = dws + ((w + 3) & ~3);
   const TcGeom g(n, w);
-  for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)b * kModes2 + t];
+  for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)t * a.B + b];   // mode-major
   for (int t = threadIdx.x; t < w; t += blockDim.x) dws[t] = a.dw[t];
   __syncthreads();
   // phase 1: the bypass term sum_o dw[o] v3[o] was reduced by layer 3 (k_tc_layer, fused projection)
@@ -691,6 +701,13 @@ size_t no_max_smem(int n, int w) {
 template size_t no_max_smem<float>(int, int);
 template size_t no_max_smem<double>(int, int);
 
+// The tensor-core path keeps the mixed spectra mode-major ([400][B][cout]); the FFMA path [B][cout][400].
+template <typename T>
+static bool tc_layout_modes(const NoDev<T>& no) {
+  if constexpr (sizeof(T) == sizeof(float)) return no.tc != 0;
+  return false;
+}
+
 template <typename T>
 cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double* rr, double* wout,
                               const FcgDev* fcg, const int* status, cudaStream_t s, int* nlaunch, ProfHook* prof) {
@@ -715,7 +732,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   launch_k(k_lift_mix<T>, dim3(B, (w + 7) / 8), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
            reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
            reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2), ghat, w, n2, inv_n2,
-           status);
+           status, (int)tc_layout_modes(no));
   pe(PROF_NO_INPUT);
   ++launches;
   // 3. layers 1..3, each followed by the mixing of the next layer
@@ -800,7 +817,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   oa.n = n; oa.N = N; oa.w = w; oa.use_dots = fcg != nullptr;
   oa.vin = vbuf[0];                       // layer 3 wrote vbuf[2 & 1] = vbuf[0]
   oa.dw = pk + no.L.dw; oa.cst = pk + no.L.cst;
-  oa.gh4 = ghat; oa.F = F; oa.rr = rr; oa.wout = wout; oa.status = status;
+  oa.gh4 = ghat; oa.F = F; oa.rr = rr; oa.wout = wout; oa.status = status; oa.B = B;
   const int nblk = (N + kTile - 1) / kTile;
   const int nr_max = kTile / n + 2;
   const size_t osmem = (size_t)(kModes2 + (size_t)nr_max * kModes) * sizeof(T2) + (size_t)((w + 3) & ~3) * sizeof(T);

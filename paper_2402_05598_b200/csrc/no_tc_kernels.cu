@@ -13,7 +13,7 @@
 //     epilogue      v' = GELU(D1 + b) -> next layer's V blob, and into TMEM (A operand of D2)
 //     D2[(r,o)][k'] = sum_j v'[(r,o)][j] F[j][k']                        x-analysis
 //     epilogue      -> T blob
-//   k_yan_tc    per (system, 128 (o,kappa2) rows): C^T[(o,k2)][(k1,p)] = T[(o,k2)][(i,p')] . Ap[(i,p')][(k1,p)]
+//   k_yan_tc    per (system, 128 (kappa2,o) rows): C^T[(k2,o)][(k1,p)] = T[(k2,o)][(i,p')] . Ap[(i,p')][(k1,p)]
 //
 // Every tensor passed between these kernels lives in HBM as a "blob" already split into bf16
 // hi + lo in its consumer's canonical core-matrix layout (tc_layout.cuh), so consumers stage a
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
         if (o < w) {
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int k2 = (c0 + q) >> 1, pin = (c0 + q) & 1, m = o * kModes + k2, kl = 2 * r + pin;
+            const int k2 = (c0 + q) >> 1, pin = (c0 + q) & 1, m = k2 * w + o, kl = 2 * r + pin;
             __nv_bfloat16 h, l;
             tc::split_bf16(__uint_as_float(u[q]), h, l);
             ts[(size_t)kl * MT + m] = h;
@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tc_layer_ws(const TcLayerArgs
           if (c >= 5) break;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
-            const int col = 8 * c + q, k2 = col >> 1, pin = col & 1, m = o * kModes + k2, kl = 2 * r + pin;
+            const int col = 8 * c + q, k2 = col >> 1, pin = col & 1, m = k2 * w + o, kl = 2 * r + pin;
             __nv_bfloat16 h, l;
             tc::split_bf16(__uint_as_float(u[k][q]), h, l);
             ts[(size_t)kl * MT + m] = h;
@@ -882,6 +882,12 @@ __global__ void __launch_bounds__(kWsThreads, 1) k_tc_layer_ws(const TcLayerArgs
 constexpr int kYsynCh = 6;                 // channels per work item: N = 6 * 40 = 240
 constexpr int kYsynN = kYsynCh * 2 * kModes;
 
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(tc::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 struct YsynSmem {
   uint32_t A, B, GS, bar, tptr, total;
   __host__ __device__ YsynSmem() {
@@ -915,11 +921,15 @@ __global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ g
     while (it < nitems && status && status[it / nch] != SYS_RUNNING) it += gridDim.x;
     return it;
   };
+  // all threads: gather g[kappa][b][oc .. oc + 6) of the mode-major ghat into GS [kappa][6] (async)
   auto prefetch = [&](int it) {
     const int b = it / nch, oc = (it % nch) * kYsynCh, nvalid = min(kYsynCh, w - oc);
-    const uint32_t bytes = (uint32_t)nvalid * kModes2 * 8;
-    tc::mbar_expect_tx(&bar[0], bytes);
-    tc::bulk_g2s(sm + L.GS, ghat + ((size_t)b * w + oc) * kModes2, bytes, &bar[0]);
+    float2* gsw = reinterpret_cast<float2*>(sm + L.GS);
+    for (int t = tid; t < kModes2 * nvalid; t += blockDim.x) {
+      const int kk = t / nvalid, ol = t - kk * nvalid;
+      cp_async8(gsw + kk * kYsynCh + ol, ghat + ((size_t)kk * B + b) * w + oc + ol);
+    }
+    cp_async_commit();
   };
   if (tid == 0) {
     for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
@@ -930,7 +940,7 @@ __global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ g
   pdl_wait();
   pdl_trigger();
   int it = next_item(blockIdx.x);
-  if (tid == 0 && it < nitems) prefetch(it);
+  if (it < nitems) prefetch(it);
   if (warp == 0) tc::tmem_alloc(tptr, 256);
   tc::fence_before_sync();
   __syncthreads();
@@ -942,7 +952,8 @@ __global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ g
   uint32_t ph = 0;
   for (; it < nitems; it = next_item(it + gridDim.x)) {
     const int b = it / nch, oc = (it % nch) * kYsynCh;
-    tc::mbar_wait(&bar[0], ph);
+    cp_async_wait_all();
+    __syncthreads();
     // B = Gh rows (ol, k2, pout), K = (k1, pin), from the staged g of the chunk
     for (int t = tid; t < (kYsynN / 2) * (kKS / 8); t += blockDim.x) {
       const int m = t % (kYsynN / 2), kc = t / (kYsynN / 2);
@@ -952,7 +963,7 @@ __global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ g
       for (int q = 0; q < 4; ++q) {
         const int k1 = kc * 4 + q;
         float2 gg = make_float2(0.f, 0.f);
-        if (o < w && k1 < kModes) gg = gs[ol * kModes2 + k1 * kModes + k2];
+        if (o < w && k1 < kModes) gg = gs[(k1 * kModes + k2) * kYsynCh + ol];
         vr[2 * q] = gg.x;  vr[2 * q + 1] = gg.y;
         vi[2 * q] = gg.y;  vi[2 * q + 1] = -gg.x;
       }
@@ -963,9 +974,11 @@ __global__ void __launch_bounds__(128, 2) k_ysyn_tc(const float2* __restrict__ g
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();
     __syncthreads();
-    if (tid == 0) {
+    {
       const int itn = next_item(it + gridDim.x);       // staging buffer is free again
       if (itn < nitems) prefetch(itn);
+    }
+    if (tid == 0) {
       tc::fence_after_sync();
       uint32_t acc = 0;
       for (int s = 0; s < kKS / 16; ++s)
@@ -1077,7 +1090,7 @@ __global__ void __launch_bounds__(128, 2) k_yan_tc(const unsigned char* __restri
     }
     {
       const int m = m0 + warp * 32 + lane;
-      const int o = m / kModes, k2 = m % kModes;
+      const int k2 = m / w, o = m - k2 * w;          // T rows ordered (kappa2, o): stores coalesce over o
 #pragma unroll
       for (int c = 0; c < 2 * kModes; c += 8) {
         uint32_t u[8];
@@ -1209,10 +1222,10 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
         tc::tmem_wait_ld();
         if (ok) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < 4; ++q) {              // mode-major ghat [kappa][B][cout]: 32-byte runs per thread
             const int o = c0 / 2 + q;
             if (o < cout)
-              ghat[((size_t)b * cout + o) * kModes2 + kk] =
+              ghat[((size_t)kk * B + b) * cout + o] =
                   make_float2(__uint_as_float(u[2 * q]) * inv_n2, __uint_as_float(u[2 * q + 1]) * inv_n2);
           }
         }
