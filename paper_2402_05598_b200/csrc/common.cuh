@@ -19,7 +19,7 @@ constexpr int kTile = kThreads * kPerThread;  // elements of one system per CTA
 constexpr int kModes = 20;             // K
 constexpr int kModes2 = kModes * kModes;
 constexpr int kMmax = 64;              // FCGNO_MMAX
-constexpr int kDotChunk = 8;           // window dots reduced together
+constexpr int kDotChunk = 6;           // window dots reduced together
 
 enum : int { SYS_RUNNING = 0, SYS_CONVERGED = 1, SYS_MAXIT = 2, SYS_BREAKDOWN = 3, SYS_NONFINITE = 4 };
 enum : int { FLAG_NONFINITE = 1, FLAG_BREAKDOWN = 2 };

@@ -239,8 +239,16 @@ __global__ void __launch_bounds__(kThreads) k_pform_stencil(FcgDev d) {
     d.part_step[((size_t)b * d.nblk + blockIdx.x) * 2 + 1] = v[1];
   }
   if (arrive_last(d.cnt + d.B + b, d.nblk)) {
-    const dd g = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, d.nblk, 2, sm);
-    const dd p = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, d.nblk, 2, sm);
+    dd g, p;
+    if (d.nblk <= kSerialPartials) {
+      if (threadIdx.x == 0) {
+        g = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, d.nblk, 2);
+        p = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, d.nblk, 2);
+      }
+    } else {
+      g = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, d.nblk, 2, sm);
+      p = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, d.nblk, 2, sm);
+    }
     if (threadIdx.x == 0) {
       const double gamma = dd_round(g);
       d.gamma[(size_t)slot * d.B + b] = gamma;
@@ -303,7 +311,12 @@ __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
   if (!arrive_last(d.cnt + 2 * d.B + b, d.nblk)) return;
   bool running = false;
   if (fl == 0) {
-    const dd t = block_reduce_partials(d.part_rr + (size_t)b * d.nblk, d.nblk, 1, sm);
+    dd t;
+    if (d.nblk <= kSerialPartials) {
+      if (threadIdx.x == 0) t = serial_partials(d.part_rr + (size_t)b * d.nblk, d.nblk, 1);
+    } else {
+      t = block_reduce_partials(d.part_rr + (size_t)b * d.nblk, d.nblk, 1, sm);
+    }
     if (threadIdx.x == 0) {
       const double rr = dd_round(t);
       d.rr[b] = rr;

@@ -590,32 +590,40 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
 // Tensor-core path variant: the layer-4 bypass sum_o (D W4)[o] v3[o] arrives as one fp32 field
 // reduced by layer 3's epilogue; this kernel adds cst + the 1-channel synthesis, scales by ||r||
 // and computes the FCG window dots.
-__global__ void __launch_bounds__(kThreads) k_no_out_blob(const OutArgs<float> a, const FcgDev d) {
+__global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float> a, const FcgDev d) {
   pdl_wait();
   pdl_trigger();
   const int b = blockIdx.y, blk = blockIdx.x;
   if (a.status && a.status[b] != SYS_RUNNING) return;
   extern __shared__ __align__(16) unsigned char smraw[];
-  float2* gh = reinterpret_cast<float2*>(smraw);
-  const int n = a.n, N = a.N, w = a.w;
+  const int n = a.n, N = a.N;
   const int e0 = blk * kTile;
   const int rlo = e0 / n, rhi = min(n - 1, (e0 + kTile - 1) / n), nr = rhi - rlo + 1;
   const int nr_max = kTile / n + 2;
-  float2* Gs = gh + kModes2;
-  float* dws = reinterpret_cast<float*>(Gs + (size_t)nr_max * kModes);
-  float* outs = dws + ((w + 3) & ~3);
-  const TcGeom g(n, w);
+  float2* gh = reinterpret_cast<float2*>(smraw);              // [400] g4 of this system
+  float2* Gs = gh + kModes2;                                   // [nr_max][20] y-synthesised rows
+  float2* Fs = Gs + (size_t)nr_max * kModes;                   // [20][n] twiddles, transposed
+  float* outs = reinterpret_cast<float*>(Fs + (size_t)kModes * n);
+  // window vectors first: their loads are in flight during the synthesis below
+  const int it = a.use_dots ? *d.iter : 0;
+  const int mi = a.use_dots ? m_schedule(it, d.m, d.schedule) : 0;
+  double rv[kWinPre][kPerThread];
+  if (mi > 0) window_prefetch(d, b, blk, it, mi, rv);
   for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)t * a.B + b];   // mode-major
-  for (int t = threadIdx.x; t < w; t += blockDim.x) dws[t] = a.dw[t];
-  __syncthreads();
-  // phase 1: the bypass term sum_o dw[o] v3[o] was reduced by layer 3 (k_tc_layer, fused projection)
+  for (int t = threadIdx.x; t < kModes * n; t += blockDim.x) {
+    const int j = t / kModes, k = t - j * kModes;
+    Fs[k * n + j] = __ldg(a.F + t);
+  }
+  // the bypass term sum_o dw[o] v3[o] was reduced by layer 3 (k_tc_layer, fused projection)
   for (int t = threadIdx.x; t < kTile; t += blockDim.x) outs[t] = (e0 + t < N) ? a.p3[(size_t)b * N + e0 + t] : 0.f;
+  __syncthreads();
   for (int e = threadIdx.x; e < nr * kModes; e += blockDim.x) {
     const int r = e / kModes, k2 = e - r * kModes;
     float gr = 0, gi = 0;
+#pragma unroll 4
     for (int k1 = 0; k1 < kModes; ++k1) {
       const float2 gg = gh[k1 * kModes + k2];
-      const float2 f = __ldg(a.F + (size_t)(rlo + r) * kModes + k1);
+      const float2 f = Fs[k1 * n + rlo + r];
       gr += gg.x * f.x + gg.y * f.y;
       gi += gg.y * f.x - gg.x * f.y;
     }
@@ -635,18 +643,14 @@ __global__ void __launch_bounds__(kThreads) k_no_out_blob(const OutArgs<float> a
       const float2* Gr = Gs + (size_t)(i - rlo) * kModes;
 #pragma unroll 4
       for (int k2 = 0; k2 < kModes; ++k2) {
-        const float2 f = __ldg(a.F + (size_t)j * kModes + k2);
+        const float2 f = Fs[k2 * n + j];
         z += Gr[k2].x * f.x + Gr[k2].y * f.y;
       }
       wv[q] = s * (double)z;
       a.wout[(size_t)b * N + e] = wv[q];
     }
   }
-  if (a.use_dots) {
-    const int i = *d.iter;
-    const int mi = m_schedule(i, d.m, d.schedule);
-    if (mi > 0) window_dots_beta(d, b, blk, i, mi, wv);
-  }
+  if (mi > 0) window_dots_beta<true>(d, b, blk, it, mi, wv, rv);
 }
 
 // ------------------------------------------------------------------ launcher
@@ -826,7 +830,8 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   if constexpr (sizeof(T) == sizeof(float)) {
     if (tc_path) {
       oa.p3 = no.p3;
-      launch_k(k_no_out_blob, dim3(nblk, B), dim3(kThreads), osmem + kTile * sizeof(float), s, oa, fcg ? *fcg : dummy);
+      const size_t bsmem = (size_t)(kModes2 + (size_t)nr_max * kModes + (size_t)kModes * n) * sizeof(float2) + kTile * sizeof(float);
+      launch_k(k_no_out_blob, dim3(nblk, B), dim3(kThreads), bsmem, s, oa, fcg ? *fcg : dummy);
     } else {
       launch_k(k_no_out<T>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);
     }
