@@ -425,3 +425,35 @@ def test_tc_and_ffma_paths_agree(lib):
         subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True)
         outs.append(np.load(path))
     assert rel_l2(outs[0], outs[1]) <= 5e-5
+
+
+def _solve_in_subprocess(env_extra, tag, maxit=12, batch=64):
+    """Short fp32 FCG-NO solve at the config-2 geometry in a fresh process with extra env flags
+    (the flags are read once per process); returns (u, history)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys,numpy as np,torch; sys.path.insert(0,'.'); import synthetic as sy;"
+            "from paper_2402_05598_b200 import fcgno as F;"
+            f"cfg=dict(sy.CONFIGS[2], batch={batch}); k=sy.make_k(cfg); f=sy.make_f(cfg); blob=sy.make_weights(cfg);"
+            "p=F.Problem(torch.from_numpy(k).cuda());"
+            f"res=F.fcg_solve(p, torch.from_numpy(f).cuda(), m=cfg['m'], tol=cfg['tol'], maxit={maxit},"
+            " no=F.NeuralOperator(cfg['width'], blob));"
+            "np.savez(sys.argv[1], u=res.u.cpu().numpy(), h=res.history.cpu().numpy())")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = f"/tmp/fcgno_optin_{tag}.npz"
+    subprocess.run([sys.executable, "-c", code, path], cwd=root, env=dict(os.environ, **env_extra), check=True)
+    z = np.load(path)
+    return z["u"], z["h"]
+
+
+def test_opt_in_paths_match_default(lib):
+    # Opt-in variants compute the same per-system arithmetic as the default path:
+    #   FCGNO_LANES=2  -- the batch as two parallel graph branches (systems never interact): bitwise;
+    #   FCGNO_TC_WS=1  -- pipelined two-group layer kernel, same MMA and epilogue arithmetic: bitwise.
+    u0, h0 = _solve_in_subprocess({}, "default")
+    u1, h1 = _solve_in_subprocess({"FCGNO_LANES": "2"}, "lanes")
+    u2, h2 = _solve_in_subprocess({"FCGNO_TC_WS": "1"}, "ws")
+    assert np.isfinite(u0).all() and h0.shape == h1.shape == h2.shape
+    assert np.array_equal(u0, u1) and np.array_equal(h0, h1, equal_nan=True)
+    assert np.array_equal(u0, u2) and np.array_equal(h0, h2, equal_nan=True)
