@@ -206,8 +206,7 @@ def run_ours(args):
     df = torch.from_numpy(f).cuda()
     prob = F.Problem(dk)
     no = F.NeuralOperator(w, blob, precision=F.FP32 if cfg["no_precision"] == "fp32" else F.FP64)
-    solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False,
-                      profile_mask=1 << F.PROF_NO_LAYER)
+    solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False)
     u = torch.zeros_like(df)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     for _ in range(args.warmup):
@@ -237,6 +236,25 @@ def run_ours(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches = F.kernel_launches() - launches0
+    # dominant-kernel timing: a second timed pass of the same workload whose graphs carry CUDA
+    # events around the layer launches of one sampled iteration per chunk (kept out of the pass
+    # above: event nodes break programmatic-dependent-launch overlap and perturb the step time)
+    psolver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False,
+                       profile_mask=1 << F.PROF_NO_LAYER)
+    u.zero_()
+    psolver.solve(df, u)
+    F.profile_reset()
+    prof_ms = 0.0
+    for _ in range(max(1, min(args.steps, 2))):
+        flush.zero_()
+        u.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        psolver.solve(df, u)
+        e1.record()
+        e1.synchronize()
+        prof_ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
     clocks = sampler.stop()
     prof = F.profile_read()
     local_ms = sum(times)
@@ -268,6 +286,8 @@ def run_ours(args):
                     "frac": achieved / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": alg,
                     "avg_launch_ms": avg_layer_ms, "launches_timed": layer_n,
                     "share_of_step": 3 * avg_layer_ms / ms_per_iter,
+                    "timing": "CUDA events recorded inside the solve graphs around the layer launches of one sampled "
+                              "iteration per 16, in a second timed pass of the same workload",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, measured on this pool)",
                     "useful_tflops": (layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)) / 3 / (avg_layer_ms * 1e-3) / 1e12}
     else:

@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     const int sb = t / g.tiles_per_sys;
     if (!a.status) return true;
     if (cached) return ((runb[sb >> 5] >> (sb & 31)) & 1u) != 0;
-    return a.status[sb] == SYS_RUNNING;
+    return __ldcg(a.status + sb) == SYS_RUNNING;
   };
   auto next_tile = [&](int t) {
     while (t < ntiles && !running(t)) t += gridDim.x;
@@ -268,7 +268,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   };
   const uint32_t rk_bytes = (uint32_t)R * n * 8;
   const uint32_t in_bytes = FIRST ? 2u * g.g_half() + 2u * rk_bytes : 2u * bv_half + 2u * g.g_half();
-  auto prefetch = [&](int t) {   // one thread: bulk copies of tile t's inputs
+  // one thread: bulk copies of tile t's inputs.  V (or r, k) was produced before this kernel's
+  // predecessor started; G is the predecessor's output (copied only after griddepcontrol.wait).
+  auto prefetch_v = [&](int t) {
     const int tb = t / g.tiles_per_sys, ti0 = (t % g.tiles_per_sys) * R;
     tc::mbar_expect_tx(&bar[0], in_bytes);
     if (FIRST) {
@@ -278,28 +280,30 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
     } else {
       tc::bulk_g2s(sm + L.BV, a.vin + (size_t)t * 2 * bv_half, 2u * bv_half, &bar[0]);
     }
-    tc::bulk_g2s(sm + L.AG, a.G + (size_t)t * 2 * g.g_half(), 2u * g.g_half(), &bar[0]);
   };
+  auto prefetch_g = [&](int t) { tc::bulk_g2s(sm + L.AG, a.G + (size_t)t * 2 * g.g_half(), 2u * g.g_half(), &bar[0]); };
+  auto prefetch = [&](int t) { prefetch_v(t); prefetch_g(t); };
 
-  // ---- one-time setup: barriers, TMEM, constant operands (bulk), bias; then wait for the predecessor
+  // ---- one-time setup, overlapping the predecessor's tail (programmatic dependent launch): barriers,
+  // constant operands, the running-system bitmask (status is written only by k_update, which
+  // completed before the predecessor started; read through L2), the first tile's V operand, TMEM,
+  // bias and the block-diagonal weights.  Only the G operand waits for griddepcontrol.wait.
   if (tid == 0) {
     for (int q = 0; q < 4; ++q) tc::mbar_init(&bar[q], 1);
     tc::fence_mbar_init();
     tc::mbar_expect_tx(&bar[3], 2u * bf_half);
     tc::bulk_g2s(sm + L.BF, a.cst + C.BF, 2u * bf_half, &bar[3]);
   }
-  pdl_wait();
-  pdl_trigger();
   if (cached) {
     for (int q = warp; q < (a.B + 31) / 32; q += blockDim.x / 32) {
       const int sb = q * 32 + lane;
-      const unsigned bits = __ballot_sync(0xffffffffu, sb < a.B && a.status[sb] == SYS_RUNNING);
+      const unsigned bits = __ballot_sync(0xffffffffu, sb < a.B && __ldcg(a.status + sb) == SYS_RUNNING);
       if (lane == 0) runb[q] = bits;
     }
-    __syncthreads();
   }
+  __syncthreads();
   int tile = next_tile(blockIdx.x);
-  if (tid == 0 && tile < ntiles) prefetch(tile);
+  if (tid == 0 && tile < ntiles) prefetch_v(tile);
   if (warp == 0) tc::tmem_alloc(tptr, ncols);
 
   for (int t = tid; t < 128; t += blockDim.x) {
@@ -340,6 +344,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) k_tc_layer(const TcLayerArgs a)
   const uint32_t id1s = tc::make_idesc_bf16(128, n, false, false);   // synthesis: both K-major
   const uint32_t id2 = tc::make_idesc_bf16(128, kKS, false, true);   // analysis: B = F viewed MN-major
   const uint32_t sm_base = tc::smem_u32(sm);
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0 && tile < ntiles) prefetch_g(tile);
   if (tid == 0) tc::mbar_wait(&bar[3], 0);
 
   uint32_t ph = 0;
