@@ -91,12 +91,13 @@ struct TcConst {
     FP = take(2 * (size_t)fp_half);
     ap_half = (uint32_t)kKS * (2 * g.n) * 2;
     AP = take(2 * (size_t)ap_half);
-    // mode-mixing B operands per mode: rows (o, re|im) (NM), K = (c, re|im) (KM); mixes for layers 2, 3
-    // and the layer-4/projection fold (cout = 1)
+    // mode-mixing B operands per mode: rows o (NM), K = (c, re|im) (KM) holding (Rr, Ri) of R[c][o]
+    // (the A side carries the complex structure, k_mix_tc); mixes for layers 2, 3 and the
+    // layer-4/projection fold (cout = 1)
     KM = (2 * g.w + 15) & ~15;
     for (int l = 0; l < 3; ++l) {
       const int cout = l < 2 ? g.w : 1;
-      NM[l] = (2 * cout + 15) & ~15;
+      NM[l] = (cout + 15) & ~15;
       mx_half[l] = (uint32_t)NM[l] * KM * 2;
       MX[l] = take((size_t)kModes2 * 2 * mx_half[l]);
     }
@@ -154,20 +155,20 @@ __global__ void __launch_bounds__(256) k_tc_prep(const TcPrepArgs a) {
         v[2 * q + 1] = pout ? f.x : -f.y;
       }
       dst = a.out + C.AP; half = C.ap_half; off = tc::kmajor_off(nn, kc * 8, ((2 * n) / 8) * 128, 128);
-    } else if ((u -= nAP) >= nAW[0] + nAW[1] + nAW[2]) {   // mixing B: row (o, pout), K = (c, pin)
+    } else if ((u -= nAP) >= nAW[0] + nAW[1] + nAW[2]) {   // mixing B: row o, K = (c, re|im) = (Rr, Ri)
       u -= nAW[0] + nAW[1] + nAW[2];
       int l = 0;
       while (u >= nMX[l]) { u -= nMX[l]; ++l; }
       const int cout = l < 2 ? w : 1, NM = C.NM[l], KM = C.KM;
       const int per_mode = NM * (KM / 8), kk = u / per_mode, rem = u % per_mode, nn = rem % NM, kc = rem / NM;
-      const int o = nn >> 1, pout = nn & 1;
+      const int o = nn;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int c = kc * 4 + q;
         float rr = 0.f, ri = 0.f;
         if (c < w && o < cout) { const float2 R2 = a.Rm[l][((size_t)kk * w + c) * cout + o]; rr = R2.x; ri = R2.y; }
-        v[2 * q] = pout ? ri : rr;            // pin = re
-        v[2 * q + 1] = pout ? rr : -ri;       // pin = im
+        v[2 * q] = rr;
+        v[2 * q + 1] = ri;
       }
       dst = a.out + C.MX[l] + (size_t)kk * 2 * C.mx_half[l]; half = C.mx_half[l];
       off = tc::kmajor_off(nn, kc * 8, (KM / 8) * 128, 128);
@@ -1137,6 +1138,13 @@ struct MixSmem {
   }
 };
 
+// Mode-diagonal mixing, one work item = (mode kappa, 64 systems).  The complex product
+// g[b][o] = sum_c c[b][c] R[c][o] runs as one real GEMM with two A rows per system,
+//   row 2b   = (cr, -ci) per channel  ->  D = sum_c cr Rr - ci Ri = gr
+//   row 2b+1 = (ci,  cr) per channel  ->  D = sum_c ci Rr + cr Ri = gi
+// against B = (Rr, Ri) per channel (k_tc_prep), so the weight blob and N are not doubled.
+constexpr int kMixSys = 64;   // systems per work item (2 A rows each)
+
 __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat, const unsigned char* __restrict__ cst,
                                                float2* __restrict__ ghat, int n, int w, int B, int mix, float inv_n2,
                                                const int* status) {
@@ -1149,7 +1157,7 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0] B load, [1] MMA
   uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nbc = (B + 127) / 128, nitems = kModes2 * nbc;
+  const int nbc = (B + kMixSys - 1) / kMixSys, nitems = kModes2 * nbc;
   auto prefetch = [&](int it) {
     const int kk = it / nbc;
     tc::mbar_expect_tx(&bar[0], 2 * b_half);
@@ -1161,7 +1169,8 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
     tc::fence_mbar_init();
     if ((int)blockIdx.x < nitems) prefetch(blockIdx.x);   // weights do not depend on the predecessor
   }
-  if (warp == 0) tc::tmem_alloc(tptr, 256);
+  const uint32_t ncols = NM <= 32 ? 32u : (NM <= 64 ? 64u : 128u);
+  if (warp == 0) tc::tmem_alloc(tptr, ncols);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -1172,32 +1181,36 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
   pdl_trigger();
   uint32_t ph = 0;
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const int kk = it / nbc, b0 = (it % nbc) * 128, nb = min(128, B - b0);
-    // A: rows b, K = (c, re|im) = the float2 layout of c[kappa][b][c]; all loads of a batch first
+    const int kk = it / nbc, b0 = (it % nbc) * kMixSys, nb = min(kMixSys, B - b0);
+    // A: rows (b, re|im), K = (c, re|im); all loads of a batch first
     {
       constexpr int kBatch = 8;
-      const int ntask = 128 * (KM / 8);
+      const int ntask = kMixSys * (KM / 8);
       for (int t0 = tid; t0 < ntask; t0 += kBatch * blockDim.x) {
         float2 x[kBatch][4];
 #pragma unroll
         for (int z = 0; z < kBatch; ++z) {
-          const int t = t0 + z * blockDim.x, row = t % 128, kc = t / 128;
+          const int t = t0 + z * blockDim.x, bl = t % kMixSys, kc = t / kMixSys;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int c = kc * 4 + q;
-            x[z][q] = (t < ntask && row < nb && c < w) ? __ldg(chat + ((size_t)kk * B + b0 + row) * w + c)
-                                                       : make_float2(0.f, 0.f);
+            x[z][q] = (t < ntask && bl < nb && c < w) ? __ldg(chat + ((size_t)kk * B + b0 + bl) * w + c)
+                                                      : make_float2(0.f, 0.f);
           }
         }
 #pragma unroll
         for (int z = 0; z < kBatch; ++z) {
-          const int t = t0 + z * blockDim.x, row = t % 128, kc = t / 128;
+          const int t = t0 + z * blockDim.x, bl = t % kMixSys, kc = t / kMixSys;
           if (t >= ntask) break;
-          float v[8];
+          float vr[8], vi[8];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) { v[2 * q] = x[z][q].x; v[2 * q + 1] = x[z][q].y; }
-          const uint32_t off = tc::kmajor_off(row, kc * 8, SBO, 128);
-          store_split8(sm + L.A + off, sm + L.A + a_half + off, v);
+          for (int q = 0; q < 4; ++q) {
+            vr[2 * q] = x[z][q].x;  vr[2 * q + 1] = -x[z][q].y;
+            vi[2 * q] = x[z][q].y;  vi[2 * q + 1] = x[z][q].x;
+          }
+          const uint32_t offr = tc::kmajor_off(2 * bl, kc * 8, SBO, 128), offi = tc::kmajor_off(2 * bl + 1, kc * 8, SBO, 128);
+          store_split8(sm + L.A + offr, sm + L.A + a_half + offr, vr);
+          store_split8(sm + L.A + offi, sm + L.A + a_half + offi, vi);
         }
       }
     }
@@ -1221,19 +1234,30 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
     tc::fence_after_sync();
     if (tid == 0 && it + (int)gridDim.x < nitems) prefetch(it + gridDim.x);   // B consumed
     {
-      const int row = warp * 32 + lane, b = b0 + row;
-      const bool ok = row < nb && (!status || status[b] == SYS_RUNNING);
-      for (int c0 = 0; c0 < 2 * cout; c0 += 8) {
+      // lane pair (2bl, 2bl+1) holds (gr, gi) of system bl: swap halves of each 8-column chunk so the
+      // even lane writes o in [c0, c0+4) and the odd lane o in [c0+4, c0+8) as float2 runs
+      const int row = warp * 32 + lane, bl = row >> 1, p = row & 1, b = b0 + bl;
+      const bool ok = bl < nb && (!status || status[b] == SYS_RUNNING);
+      for (int c0 = 0; c0 < cout; c0 += 8) {
         uint32_t u[8];
         tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c0, u);
         tc::tmem_wait_ld();
+        float mine[4], other[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float keep = __uint_as_float(u[p ? 4 + q : q]);      // my half
+          const float give = __uint_as_float(u[p ? q : 4 + q]);      // partner's half
+          mine[q] = keep;
+          other[q] = __shfl_xor_sync(0xffffffffu, give, 1);
+        }
         if (ok) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {              // mode-major ghat [kappa][B][cout]: 32-byte runs per thread
-            const int o = c0 / 2 + q;
-            if (o < cout)
-              ghat[((size_t)kk * B + b) * cout + o] =
-                  make_float2(__uint_as_float(u[2 * q]) * inv_n2, __uint_as_float(u[2 * q + 1]) * inv_n2);
+          for (int q = 0; q < 4; ++q) {
+            const int o = c0 + 4 * p + q;
+            if (o < cout) {
+              const float gr = p ? other[q] : mine[q], gi = p ? mine[q] : other[q];
+              ghat[((size_t)kk * B + b) * cout + o] = make_float2(gr * inv_n2, gi * inv_n2);
+            }
           }
         }
       }
@@ -1244,7 +1268,7 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
   }
   tc::fence_after_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+  if (warp == 0) tc::tmem_dealloc(tmem, ncols);
 }
 
 static size_t ysyn_tc_smem() { return YsynSmem().total; }
@@ -1387,13 +1411,19 @@ cudaError_t launch_yan(const unsigned char* Tb, const unsigned char* cst, float*
 
 size_t tc_const_bytes(int n, int w) { return TcConst(TcGeom(n, w)).total; }
 
+static int mix_per_sm() {   // FCGNO_MIX_PER_SM (A/B experiments); default 3 (smem allows 3, measured best)
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("FCGNO_MIX_PER_SM"); v = e ? std::max(1, atoi(e)) : 3; }
+  return v;
+}
+
 cudaError_t launch_mix_tc(int mix, const float* chat, const unsigned char* cst, float* ghat, int n, int w, int B,
                           float inv_n2, const int* status, cudaStream_t s) {
   const TcGeom g(n, w);
   const TcConst C(g);
   const size_t smem = MixSmem(C.KM, C.NM[mix]).total;
-  const int nitems = kModes2 * ((B + 127) / 128);
-  const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+  const int nitems = kModes2 * ((B + kMixSys - 1) / kMixSys);
+  const int per_sm = std::max(1, std::min(mix_per_sm(), (int)((228u * 1024u) / (smem + 1024u))));
   const int grid = std::min(nitems, per_sm * num_sms());
   return launch_k(k_mix_tc, dim3(grid), dim3(128), smem, s, reinterpret_cast<const float2*>(chat), cst,
                   reinterpret_cast<float2*>(ghat), n, w, B, mix, inv_n2, status);
