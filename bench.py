@@ -40,6 +40,10 @@ def parse_args(argv=None):
     ap.add_argument("--maxit", type=int, default=None, help="override the config's maxit")
     ap.add_argument("--no-split", action="store_true", help="skip the instrumented time-split solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="BASELINE configs[4] second half: isolated HBM bandwidth sweep of apply_A, the batched "
+                         "dot and the FCG kernels at 1024^2 and 2048^2, batch 4 (one JSON line)")
+    ap.add_argument("--sweep-n", type=int, nargs="*", default=[1024, 2048])
     return ap.parse_args(argv)
 
 
@@ -432,8 +436,153 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------------------- bandwidth sweep
+SWEEP_SEEDS = {1024: 110, 2048: 111}
+
+
+def sweep_window_sizes(m, check_every, maxit):
+    """m_i of the iterations the in-graph profiler samples (the first of every graph chunk)."""
+    out = []
+    for i in range(0, maxit, check_every):
+        out.append(min(i, max(1, i % (m + 1))))
+    return out
+
+
+def run_sweep(args):
+    """Isolated bandwidth sweep (BASELINE.json configs[4]: "apply_A and FCG-update kernels at
+    1024x1024 and 2048x2048, batch 4"; SURVEY.md §8(d) D.3 sweep rows).
+
+    * apply_A and the batched dot: S independent (k, x, y) sets whose total footprint is >= 3x the
+      126 MB L2, cycled, so every launch reads its operands from HBM; R launches are captured in
+      one CUDA graph and timed with events on the replay stream.
+    * the FCG kernels (k_window_dots, k_pform_stencil, k_update): in place, inside an identity
+      FCG(m=10) solve, timed with CUDA events the library records inside its graphs around the
+      launches of one sampled iteration per chunk; check_every = 12 makes the sampled iterations'
+      windows m_i cycle through 1, 2, ..., 10 like the run's own.
+    Algorithmic bytes per unknown (fp64): apply_A 24 (x, k read; y written); dot 16;
+    window dots (1 + m_i) 8; p-form + stencil (5 + m_i) 8 (w, m_i p_k, k, r read; p, s written);
+    update 48 (u, p, r, s read; u, r written)."""
+    import torch
+
+    import synthetic as sy
+    from paper_2402_05598_b200 import fcgno as F
+
+    torch.cuda.set_device(0)
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {"hbm_gbs": 6650.0}
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    L2 = torch.cuda.get_device_properties(0).L2_cache_size
+    B, m, ce = 4, 10, 12
+    rows = []
+    sampler = ClockSampler(0)
+    sampler.start()
+    for n in args.sweep_n:
+        cfg = dict(n=n, batch=B, k="lognormal", length=0.1, variance=1.0, rhs="normal", seed=SWEEP_SEEDS.get(n, 112))
+        k = torch.from_numpy(sy.make_k(cfg)).cuda()
+        f = torch.from_numpy(sy.make_f(cfg)).cuda()
+        N = n * n
+        vec = B * N * 8
+        S = max(2, -(-3 * L2 // (3 * vec)))
+        sets = []
+        for s in range(S):
+            ks = k if s == 0 else k * (1.0 + 1e-3 * s)
+            sets.append((F.Problem(ks), f.clone() if s else f, torch.empty_like(f)))
+        dws = torch.empty(F._lib.fcgno_dot_workspace_bytes(sets[0][0].grid), dtype=torch.uint8, device="cuda")
+        dout = torch.empty(B, dtype=torch.float64, device="cuda")
+
+        def timed_graph(body, reps):
+            st = torch.cuda.Stream()
+            st.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(st):
+                for t in range(3):
+                    body(t)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=st):
+                    for t in range(reps):
+                        body(t)
+                g.replay()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                best = None
+                for _ in range(3):
+                    e0.record(st)
+                    g.replay()
+                    e1.record(st)
+                    e1.synchronize()
+                    ms = e0.elapsed_time(e1) / reps
+                    best = ms if best is None else min(best, ms)
+            torch.cuda.synchronize()
+            return best
+
+        def apply_body(t):
+            p, x, y = sets[t % S]
+            F._check(F._lib.fcgno_apply_A(p._h, F._ptr(x), F._ptr(y), F._stream()))
+
+        def dot_body(t):
+            p, x, y = sets[t % S]
+            F._check(F._lib.fcgno_batched_dot(p._h, F._ptr(x), F._ptr(f if t % S else k), F._ptr(dout), F._ptr(dws),
+                                              dws.numel(), F._stream()))
+
+        reps = 8 * S
+        for name, body, bpu in (("apply_A", apply_body, 24), ("batched_dot", dot_body, 16)):
+            ms = timed_graph(body, reps)
+            gbs = bpu * B * N / (ms * 1e-3) / 1e9
+            rows.append({"kernel": name, "n": n, "batch": B, "us_per_launch": ms * 1e3, "bytes_per_unknown": bpu,
+                         "achieved_gbs": gbs, "frac": gbs / hbm})
+        del sets
+        # FCG kernels inside an identity solve
+        maxit = ce * 22
+        prob = F.Problem(k)
+        mask = (1 << F.PROF_WINDOW) | (1 << F.PROF_STENCIL) | (1 << F.PROF_UPDATE)
+        solver = F.Solver(prob, m, 1e-14, maxit, history=False, check_every=ce, profile_mask=mask)
+        u = torch.zeros_like(f)
+        solver.solve(f, u)
+        F.profile_reset()
+        u.zero_()
+        solver.solve(f, u)
+        torch.cuda.synchronize()
+        prof = F.profile_read()
+        mis = sweep_window_sizes(m, ce, maxit)
+        for name, per_mi in (("k_window_dots", lambda mi: (1 + mi) * 8 if mi else 0),
+                             ("k_pform_stencil", lambda mi: (5 + mi) * 8),
+                             ("k_update", lambda mi: 48)):
+            ms, cnt = prof.get(name, (0.0, 0))
+            if not cnt:
+                continue
+            nb = sum(per_mi(mi) for mi in mis) * B * N
+            gbs = nb / (ms * 1e-3) / 1e9
+            rows.append({"kernel": name, "n": n, "batch": B, "us_per_launch": ms * 1e3 / cnt,
+                         "bytes_per_unknown": nb / (B * N * cnt), "achieved_gbs": gbs, "frac": gbs / hbm,
+                         "launches_timed": cnt, "context": "identity FCG(10) solve, in-graph events"})
+        # whole identity iteration (no instrumentation)
+        plain = F.Solver(prob, m, 1e-14, maxit, history=False, check_every=16)
+        u.zero_()
+        plain.solve(f, u)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        u.zero_()
+        e0.record()
+        plain.solve(f, u)
+        e1.record()
+        e1.synchronize()
+        it_ms = e0.elapsed_time(e1) / maxit
+        m_bar = mean_window(m, maxit)
+        bpu = (12 + 2 * m_bar) * 8
+        gbs = bpu * B * N / (it_ms * 1e-3) / 1e9
+        rows.append({"kernel": "identity FCG iteration", "n": n, "batch": B, "us_per_iteration": it_ms * 1e3,
+                     "bytes_per_unknown": bpu, "achieved_gbs": gbs, "frac": gbs / hbm,
+                     "unknown_iterations_per_s": B * N / (it_ms * 1e-3)})
+        del prob, solver, plain
+        torch.cuda.empty_cache()
+    clocks = sampler.stop()
+    print(json.dumps({"metric": "HBM bandwidth of the stencil / reduction / FCG kernels (fraction of measured peak)",
+                      "unit": "GB/s", "peak_gbs": hbm, "l2_bytes": L2, "sweep": rows, "clocks": clocks,
+                      "data": "synthetic (seeded lognormal k, N(0,1) f)"}), flush=True)
+
+
 def main(argv=None):
     args = parse_args(argv)
+    if args.sweep:
+        run_sweep(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:
