@@ -20,6 +20,27 @@ constexpr int kModes = 20;             // K
 constexpr int kModes2 = kModes * kModes;
 constexpr int kMmax = 64;              // FCGNO_MMAX
 constexpr int kDotChunk = 6;           // window dots reduced together
+constexpr int kStR = 16;               // rows of a 2-D stencil tile
+constexpr int kStC = 128;              // columns of a 2-D stencil tile
+constexpr int kStThreads = 256;        // block size of the stencil-tile kernels
+
+// 2-D stencil tiles (fcg_device.cuh): C = min(n, kStC) columns, kStR rows, CTAs per system.
+__host__ __device__ __forceinline__ int st_cols(int n) { return n < kStC ? n : kStC; }
+__host__ __device__ __forceinline__ int st_tiles(int n) {
+  return ((n + kStR - 1) / kStR) * ((n + st_cols(n) - 1) / st_cols(n));
+}
+// Elements per thread of the element-wise kernels: kPerThread for small batches (more CTAs, lower
+// latency), kEptWide once a batch has >= 2^21 unknowns (fewer, fatter CTAs amortise the per-CTA
+// double-double reduction and keep more loads in flight).
+constexpr int kEptWide = 16;
+__host__ __device__ __forceinline__ bool ew_wide(int n, int B) { return (size_t)n * n * B >= ((size_t)1 << 21); }
+constexpr int kEptUpdate = 8;          // k_update streams four vectors: fewer elements per thread
+__host__ __device__ __forceinline__ int ew_blocks(int n, int ept) { return (n * n + kThreads * ept - 1) / (kThreads * ept); }
+// Capacity of the per-system partial arrays: the most CTAs any kernel launches per system.
+__host__ __device__ __forceinline__ int part_cap(int n) {
+  const int a = (n * n + kTile - 1) / kTile, b = st_tiles(n);
+  return a > b ? a : b;
+}
 
 enum : int { SYS_RUNNING = 0, SYS_CONVERGED = 1, SYS_MAXIT = 2, SYS_BREAKDOWN = 3, SYS_NONFINITE = 4 };
 enum : int { FLAG_NONFINITE = 1, FLAG_BREAKDOWN = 2 };

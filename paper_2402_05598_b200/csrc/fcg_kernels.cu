@@ -1,14 +1,13 @@
 // fcg_kernels.cu — matrix-free stencil, inner products and the FCG(m) step kernels.
 //
-// One FCG iteration (Algorithm 1) is split into five launches, each one
-// HBM sweep over the vectors it touches; every reduction finishes inside the producing kernel
-// (last CTA of a system reduces its partials in a fixed order), so the only scalar launch is
-// k_finalize:
+// One FCG iteration (Algorithm 1) is three launches, each one HBM sweep over
+// the vectors it touches; every reduction finishes inside the producing kernel (the last CTA of a
+// system reduces its partials in a fixed order), so there is no scalar-only launch:
 //   [NO output or k_window_dots]  (w, s_k) for the m_i window      -> beta_k = (w,s_k)/(p_k,s_k)
-//   k_pform                        p = w - sum beta_k p_k            (newest -> oldest)
-//   k_stencil_dots                 s = A p ; (p,s), (p,r)            -> alpha, breakdown
-//   k_update                       u += alpha p ; r -= alpha s ; (r,r)
-//   k_finalize                     ||r||/||r0||, status, iteration counter
+//   k_pform_stencil                p = w - sum beta_k p_k (newest -> oldest); s = A p;
+//                                  (p,s), (p,r) -> alpha, breakdown
+//   k_update                       u += alpha p ; r -= alpha s ; (r,r); ||r||/||r0||, status,
+//                                  iteration counter
 // All arithmetic is fp64 in the oracle's operation order (R5, R6, R13) so identity
 // runs reproduce the oracle's residual histories bit for bit.
 #include "internal.h"
@@ -30,63 +29,92 @@ bool pdl_enabled() {
   return v == 1;
 }
 
-static inline dim3 sys_grid(int nblk, int B) { return dim3((unsigned)nblk, (unsigned)B, 1); }
 
 
 // ------------------------------------------------------------------ apply_A
-__global__ void __launch_bounds__(kThreads) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
-                                                      double* __restrict__ y, int n, int N, double scale) {
+// 2-D tiles (fcg_device.cuh st_fill / st_walk): x and k staged once with a one-cell halo, every
+// face computed once.  Grid (st_tiles(n), B), kStThreads threads, RG = st_rg(n) rows per thread.
+#define ST_SMEM                                                   \
+  __shared__ __align__(16) double sx[(kStR + 2) * (kStC + 2)];    \
+  __shared__ __align__(16) double sk[(kStR + 2) * (kStC + 2)];    \
+  __shared__ double sbnd[kStR * (kStThreads / 32 + 1)]
+
+// launch KERNEL<RG> for the row-group size of n
+#define ST_LAUNCH(err, n, KERNEL, grid, s, ...)                                                      \
+  switch (st_rg(n)) {                                                                               \
+    case 1: err = launch_k(KERNEL<1>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
+    case 2: err = launch_k(KERNEL<2>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
+    case 4: err = launch_k(KERNEL<4>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
+    default: err = launch_k(KERNEL<8>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;           \
+  }
+
+template <int RG>
+__global__ void __launch_bounds__(kStThreads, 3) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
+                                                           double* __restrict__ y, int n, double scale) {
   pdl_wait();
   pdl_trigger();
+  ST_SMEM;
   const int b = blockIdx.y;
-  const double* kb = k + (size_t)b * N;
-  const double* xb = x + (size_t)b * N;
-  double* yb = y + (size_t)b * N;
-#pragma unroll
-  for (int q = 0; q < kPerThread; ++q) {
-    const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
-    if (e < N) {
-      const int i = e / n, j = e - i * n;
-      yb[e] = stencil_at(kb, xb, n, i, j, scale);
-    }
-  }
+  const size_t N = (size_t)n * n;
+  const StGeo g = st_geo(n);
+  const double* xb = x + b * N;
+  double* yb = y + b * N;
+  const bool fast = st_fill(g, n, k + b * N, sx, sk, [&](const StCells& cl, double (&xv)[kStCpt]) { st_load(cl, xb, xv); });
+  const StWalk<RG> w(g);
+  const double none[RG] = {};
+  st_walk_any<RG>(fast, g, w, n, scale, sx, sk, sbnd, none, [&](bool ok, int e, double, double v, double) {
+    if (ok) yb[e] = v;
+  });
 }
 
 cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, cudaStream_t s) {
-  const int N = n * n, nblk = (N + kTile - 1) / kTile;
-  cudaError_t e = launch_k(k_apply_A, sys_grid(nblk, B), dim3(kThreads), 0, s, k, x, y, n, N, double(n + 1) * double(n + 1));
+  cudaError_t e;
+  ST_LAUNCH(e, n, k_apply_A, dim3((unsigned)st_tiles(n), (unsigned)B), s, k, x, y, n, double(n + 1) * double(n + 1));
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ batched dot
+template <int EPT>
 __global__ void __launch_bounds__(kThreads) k_dot(const double* __restrict__ x, const double* __restrict__ y,
-                                                  double* __restrict__ out, dd* part, unsigned* cnt, int N,
-                                                  int nblk) {
+                                                  double* __restrict__ out, dd* part, unsigned* cnt, int N, int cap) {
   pdl_wait();
   pdl_trigger();
   __shared__ dd sm[8];
   const int b = blockIdx.y;
+  const double* xb = x + (size_t)b * N;
+  const double* yb = y + (size_t)b * N;
+  double xv[EPT], yv[EPT];
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
+    xv[q] = e < N ? xb[e] : 0.0;
+    yv[q] = e < N ? yb[e] : 0.0;
+  }
   double s = 0.0, c = 0.0;
 #pragma unroll
-  for (int q = 0; q < kPerThread; ++q) {
-    const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
-    if (e < N) dot2_acc(x[(size_t)b * N + e], y[(size_t)b * N + e], s, c);
-  }
+  for (int q = 0; q < EPT; ++q) dot2_acc(xv[q], yv[q], s, c);
   dd v[1] = {dot2_finish(s, c)};
   block_reduce_dd<1>(v, sm);
-  if (threadIdx.x == 0) part[(size_t)b * nblk + blockIdx.x] = v[0];
-  if (arrive_last(cnt + b, nblk)) {
-    const dd t = block_reduce_partials(part + (size_t)b * nblk, nblk, 1, sm);
+  if (threadIdx.x == 0) part[(size_t)b * cap + blockIdx.x] = v[0];
+  const int nb = gridDim.x;
+  if (arrive_last(cnt + b, nb)) {
+    const dd t = block_reduce_partials(part + (size_t)b * cap, nb, 1, sm);
     if (threadIdx.x == 0) out[b] = dd_round(t);
   }
 }
 
 cudaError_t launch_dot(const double* x, const double* y, double* out, dd* part, unsigned* cnt, int n, int B,
                        cudaStream_t s) {
-  const int N = n * n, nblk = (N + kTile - 1) / kTile;
-  cudaError_t e = launch_k(k_dot, sys_grid(nblk, B), dim3(kThreads), 0, s, x, y, out, part, cnt, N, nblk);
+  const int N = n * n, cap = part_cap(n);
+  cudaError_t e;
+  if (ew_wide(n, B))
+    e = launch_k(k_dot<kEptWide>, dim3((unsigned)ew_blocks(n, kEptWide), (unsigned)B), dim3(kThreads), 0, s, x, y,
+                 out, part, cnt, N, cap);
+  else
+    e = launch_k(k_dot<kPerThread>, dim3((unsigned)ew_blocks(n, kPerThread), (unsigned)B), dim3(kThreads), 0, s, x,
+                 y, out, part, cnt, N, cap);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
@@ -111,29 +139,33 @@ cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t
 }
 
 // ------------------------------------------------------------------ r0 = f - A u0
-__global__ void __launch_bounds__(kThreads) k_init_residual(FcgDev d) {
+template <int RG>
+__global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   pdl_wait();
   pdl_trigger();
+  ST_SMEM;
   __shared__ dd sm[8];
-  const int b = blockIdx.y, N = d.N;
-  const double* kb = d.k + (size_t)b * N;
-  const double* ub = d.u + (size_t)b * N;
+  const int b = blockIdx.y, n = d.n;
+  const size_t N = (size_t)d.N;
+  const StGeo g = st_geo(n);
+  const double* ub = d.u + b * N;
+  double* rb = d.r + b * N;
+  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl, double (&xv)[kStCpt]) { st_load(cl, ub, xv); });
+  const StWalk<RG> w(g);
+  double fx[RG];
+  st_rows(g, w, n, d.f + b * N, fx);
   double s = 0.0, c = 0.0;
-#pragma unroll
-  for (int q = 0; q < kPerThread; ++q) {
-    const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
-    if (e < N) {
-      const int i = e / d.n, j = e - i * d.n;
-      const double rv = __dsub_rn(d.f[(size_t)b * N + e], stencil_at(kb, ub, d.n, i, j, d.scale));
-      d.r[(size_t)b * N + e] = rv;
-      dot2_acc(rv, rv, s, c);
-    }
-  }
+  st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, fx, [&](bool ok, int e, double, double v, double fv) {
+    const double rv = ok ? __dsub_rn(fv, v) : 0.0;
+    if (ok) rb[e] = rv;
+    dot2_acc(rv, rv, s, c);
+  });
   dd v[1] = {dot2_finish(s, c)};
   block_reduce_dd<1>(v, sm);
   if (threadIdx.x == 0) d.part_rr[(size_t)b * d.nblk + blockIdx.x] = v[0];
-  if (arrive_last(d.cnt + 2 * d.B + b, d.nblk)) {
-    const dd t = block_reduce_partials(d.part_rr + (size_t)b * d.nblk, d.nblk, 1, sm);
+  const int nb = gridDim.x;
+  if (arrive_last(d.cnt + 2 * d.B + b, nb)) {
+    const dd t = block_reduce_partials(d.part_rr + (size_t)b * d.nblk, nb, 1, sm);
     if (threadIdx.x == 0) {
       const double rr = dd_round(t);
       const double rho0 = __dsqrt_rn(rr);
@@ -149,13 +181,16 @@ __global__ void __launch_bounds__(kThreads) k_init_residual(FcgDev d) {
 }
 
 cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e = launch_k(k_init_residual, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  cudaError_t e;
+  ST_LAUNCH(e, d.n, k_init_residual, dim3((unsigned)st_tiles(d.n), (unsigned)d.B), s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
-__global__ void __launch_bounds__(kThreads) k_window_dots(FcgDev d) {
+// ------------------------------------------------------------------ (w, s_k) window dots (identity B)
+template <int EPT>
+__global__ void __launch_bounds__(kThreads, 2) k_window_dots(FcgDev d) {
   pdl_wait();
   pdl_trigger();
   const int b = blockIdx.y;
@@ -163,112 +198,117 @@ __global__ void __launch_bounds__(kThreads) k_window_dots(FcgDev d) {
   const int i = *d.iter;
   const int mi = m_schedule(i, d.m, d.schedule);
   if (mi == 0) return;
-  double wv[kPerThread];
+  double wv[EPT];
 #pragma unroll
-  for (int q = 0; q < kPerThread; ++q) {
-    const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
+  for (int q = 0; q < EPT; ++q) {
+    const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
     wv[q] = e < d.N ? d.w[(size_t)b * d.N + e] : 0.0;
   }
-  window_dots_beta(d, b, blockIdx.x, i, mi, wv);
+  window_dots_beta<EPT>(d, b, blockIdx.x, i, mi, wv);
 }
 
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e = launch_k(k_window_dots, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  cudaError_t e;
+  if (ew_wide(d.n, d.B))
+    e = launch_k(k_window_dots<kEptWide>, dim3((unsigned)ew_blocks(d.n, kEptWide), (unsigned)d.B), dim3(kThreads), 0,
+                 s, d);
+  else
+    e = launch_k(k_window_dots<kPerThread>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B), dim3(kThreads),
+                 0, s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ p = w - sum beta_k p_k ; s = A p ; (p,s), (p,r)
-// One CTA per (tile of kTile elements, system).  p is formed for the tile plus a one-row halo on
-// each side (the halo values are recomputed here, bit-identical to the owning CTA's), kept in
-// shared memory for the stencil, and written to the ring for the tile only.
-__global__ void __launch_bounds__(kThreads) k_pform_stencil(FcgDev d) {
+// One CTA per 2-D tile of one system.  Phase 1 forms p over the tile and its one-cell halo (halo
+// values recomputed, bit-identical to the owning CTA's) into shared memory and writes the tile's
+// p to the ring; phase 2 applies the stencil from shared memory, writes s and accumulates (p,s)
+// and (p,r).  The system's last CTA forms gamma = (p,s), alpha = (p,r)/gamma and flags breakdown.
+template <int RG>
+__global__ void __launch_bounds__(kStThreads, 2) k_pform_stencil(FcgDev d) {
   pdl_wait();
   pdl_trigger();
-  extern __shared__ __align__(16) double sp[];   // p over [lo, hi)
+  ST_SMEM;
   __shared__ dd sm[16];
   __shared__ double sbeta[kMmax];
-  __shared__ int sslot[kMmax];
+  __shared__ const double* sptr[kMmax];
   const int b = blockIdx.y;
   if (d.status[b] != SYS_RUNNING) return;
   const int i = *d.iter;
   const int mi = m_schedule(i, d.m, d.schedule);
-  const int N = d.N, n = d.n, slot = ring_slot(i, d.m);
-  const int e0 = blockIdx.x * kTile, e1 = min(N, e0 + kTile);
-  const int lo = max(0, e0 - n), hi = min(N, e1 + n);
+  const int n = d.n, slot = ring_slot(i, d.m);
+  const size_t N = (size_t)d.N;
   for (int q = threadIdx.x; q < mi; q += blockDim.x) {
     sbeta[q] = d.beta[(size_t)b * kMmax + q];
-    sslot[q] = ring_slot(i - mi + q, d.m);
+    sptr[q] = d.ring_p + ((size_t)ring_slot(i - mi + q, d.m) * d.B + b) * N;
   }
   __syncthreads();
+  const StGeo g = st_geo(n);
   double* pout = d.ring_p + ((size_t)slot * d.B + b) * N;
-  const double* wb = d.w + (size_t)b * N;
+  const double* wb = d.w + b * N;
   int bad = 0;
-  for (int e = lo + threadIdx.x; e < hi; e += blockDim.x) {
-    const double wv = wb[e];
-    double p = wv;
-    for (int t = mi - 1; t >= 0; --t)   // newest -> oldest (R13)
-      p = __dsub_rn(p, __dmul_rn(sbeta[t], d.ring_p[((size_t)sslot[t] * d.B + b) * N + e]));
-    sp[e - lo] = p;
-    if (e >= e0 && e < e1) {
-      if (!isfinite(wv)) bad = 1;
-      pout[e] = p;
-    }
-  }
-  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d.flags + b, FLAG_NONFINITE);
-  const double* kb = d.k + (size_t)b * N;
-  double* sb = d.ring_s + ((size_t)slot * d.B + b) * N;
-  double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
+  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl, double (&xv)[kStCpt]) {
+    // w and then the window vectors newest -> oldest (R13), each a batch of kStCpt loads; these
+    // vectors are read-only here, so the loads may pass the ring stores below
+    st_load(cl, wb, xv);
 #pragma unroll
-  for (int q = 0; q < kPerThread; ++q) {
-    const int e = e0 + q * kThreads + threadIdx.x;
-    if (e < N) {
-      const int ii = e / n, j = e - ii * n;
-      const double sv = stencil_at(kb, sp, n, ii, j, d.scale, lo);
-      sb[e] = sv;
-      const double pv = sp[e - lo];
-      dot2_acc(pv, sv, s0, c0);
-      dot2_acc(pv, d.r[(size_t)b * N + e], s1, c1);
+    for (int u = 0; u < kStCpt; ++u)
+      if ((cl.own >> u & 1u) && !isfinite(xv[u])) bad = 1;
+    for (int t = mi - 1; t >= 0; --t) {
+      double pv[kStCpt];
+      st_load(cl, sptr[t], pv);
+      const double bt = sbeta[t];
+#pragma unroll
+      for (int u = 0; u < kStCpt; ++u)
+        if (cl.in >> u & 1u) xv[u] = __dsub_rn(xv[u], __dmul_rn(bt, pv[u]));   // outside stays 0
     }
-  }
+#pragma unroll
+    for (int u = 0; u < kStCpt; ++u)
+      if (cl.own >> u & 1u) pout[cl.e[u]] = xv[u];
+  });
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d.flags + b, FLAG_NONFINITE);
+  const StWalk<RG> w(g);
+  double rx[RG];
+  st_rows(g, w, n, d.r + b * N, rx);
+  double* sout = d.ring_s + ((size_t)slot * d.B + b) * N;
+  double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
+  st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, rx, [&](bool ok, int e, double pv, double sv, double rv) {
+    if (ok) sout[e] = sv;
+    const double p = ok ? pv : 0.0, q = ok ? sv : 0.0;
+    dot2_acc(p, q, s0, c0);
+    dot2_acc(p, rv, s1, c1);
+  });
   dd v[2] = {dot2_finish(s0, c0), dot2_finish(s1, c1)};
   block_reduce_dd<2>(v, sm);
   if (threadIdx.x == 0) {
     d.part_step[((size_t)b * d.nblk + blockIdx.x) * 2 + 0] = v[0];
     d.part_step[((size_t)b * d.nblk + blockIdx.x) * 2 + 1] = v[1];
   }
-  if (arrive_last(d.cnt + d.B + b, d.nblk)) {
-    dd g, p;
-    if (d.nblk <= kSerialPartials) {
+  const int nb = gridDim.x;
+  if (arrive_last(d.cnt + d.B + b, nb)) {
+    dd gsum, psum;
+    if (nb <= kSerialPartials) {
       if (threadIdx.x == 0) {
-        g = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, d.nblk, 2);
-        p = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, d.nblk, 2);
+        gsum = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, nb, 2);
+        psum = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, nb, 2);
       }
     } else {
-      g = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, d.nblk, 2, sm);
-      p = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, d.nblk, 2, sm);
+      gsum = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, nb, 2, sm);
+      psum = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, nb, 2, sm);
     }
     if (threadIdx.x == 0) {
-      const double gamma = dd_round(g);
+      const double gamma = dd_round(gsum);
       d.gamma[(size_t)slot * d.B + b] = gamma;
       if (!(gamma > 0.0) || !isfinite(gamma)) atomicOr(d.flags + b, FLAG_BREAKDOWN);
-      d.alpha[b] = __ddiv_rn(dd_round(p), gamma);
+      d.alpha[b] = __ddiv_rn(dd_round(psum), gamma);
     }
   }
 }
 
-size_t pform_stencil_smem(int n) { return (size_t)(kTile + 2 * n) * sizeof(double); }
-
 cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s) {
-  static size_t set = 0;
-  const size_t smem = pform_stencil_smem(d.n);
-  if (smem > 48 * 1024 && smem > set) {   // never during graph capture of a smaller size
-    const cudaError_t e = cudaFuncSetAttribute((const void*)k_pform_stencil, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    set = smem;
-  }
-  cudaError_t e = launch_k(k_pform_stencil, sys_grid(d.nblk, d.B), dim3(kThreads), smem, s, d);
+  cudaError_t e;
+  ST_LAUNCH(e, d.n, k_pform_stencil, dim3((unsigned)st_tiles(d.n), (unsigned)d.B), s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
@@ -279,6 +319,7 @@ cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s) {
 // bookkeeping (Algorithm 1's stopping test); the last system to arrive publishes the number of
 // systems still running and advances the iteration counter.  Systems flagged this iteration
 // skip the vector update but still take part in the arrival protocol.
+template <int EPT>
 __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -293,29 +334,42 @@ __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
     const double alpha = d.alpha[b];
     const double* pb = d.ring_p + ((size_t)slot * d.B + b) * N;
     const double* sb = d.ring_s + ((size_t)slot * d.B + b) * N;
+    double* ub = d.u + (size_t)b * N;
+    double* rb = d.r + (size_t)b * N;
+    double uv[EPT], pv[EPT], rv[EPT], sv[EPT];
 #pragma unroll
-    for (int q = 0; q < kPerThread; ++q) {
-      const int e = blockIdx.x * kTile + q * kThreads + threadIdx.x;
+    for (int q = 0; q < EPT; ++q) {   // all loads first: EPT x 4 in flight
+      const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
+      const bool ok = e < N;
+      uv[q] = ok ? ub[e] : 0.0;
+      pv[q] = ok ? __ldg(pb + e) : 0.0;
+      rv[q] = ok ? rb[e] : 0.0;
+      sv[q] = ok ? __ldg(sb + e) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) {
+      const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
+      rv[q] = __dsub_rn(rv[q], __dmul_rn(alpha, sv[q]));
       if (e < N) {
-        const size_t g = (size_t)b * N + e;
-        d.u[g] = __dadd_rn(d.u[g], __dmul_rn(alpha, pb[e]));
-        const double rv = __dsub_rn(d.r[g], __dmul_rn(alpha, sb[e]));
-        d.r[g] = rv;
-        dot2_acc(rv, rv, s, c);
+        ub[e] = __dadd_rn(uv[q], __dmul_rn(alpha, pv[q]));
+        rb[e] = rv[q];
       }
     }
+#pragma unroll
+    for (int q = 0; q < EPT; ++q) dot2_acc(rv[q], rv[q], s, c);
   }
   dd v[1] = {dot2_finish(s, c)};
   block_reduce_dd<1>(v, sm);
   if (threadIdx.x == 0) d.part_rr[(size_t)b * d.nblk + blockIdx.x] = v[0];
-  if (!arrive_last(d.cnt + 2 * d.B + b, d.nblk)) return;
+  const int nb = gridDim.x;
+  if (!arrive_last(d.cnt + 2 * d.B + b, nb)) return;
   bool running = false;
   if (fl == 0) {
     dd t;
-    if (d.nblk <= kSerialPartials) {
-      if (threadIdx.x == 0) t = serial_partials(d.part_rr + (size_t)b * d.nblk, d.nblk, 1);
+    if (nb <= kSerialPartials) {
+      if (threadIdx.x == 0) t = serial_partials(d.part_rr + (size_t)b * d.nblk, nb, 1);
     } else {
-      t = block_reduce_partials(d.part_rr + (size_t)b * d.nblk, d.nblk, 1, sm);
+      t = block_reduce_partials(d.part_rr + (size_t)b * d.nblk, nb, 1, sm);
     }
     if (threadIdx.x == 0) {
       const double rr = dd_round(t);
@@ -345,7 +399,13 @@ __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
 }
 
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e = launch_k(k_update, sys_grid(d.nblk, d.B), dim3(kThreads), 0, s, d);
+  cudaError_t e;
+  if (ew_wide(d.n, d.B))
+    e = launch_k(k_update<kEptUpdate>, dim3((unsigned)ew_blocks(d.n, kEptUpdate), (unsigned)d.B), dim3(kThreads), 0, s,
+                 d);
+  else
+    e = launch_k(k_update<kPerThread>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B), dim3(kThreads), 0,
+                 s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();

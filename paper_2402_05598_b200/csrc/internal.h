@@ -119,7 +119,6 @@ cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s);
-size_t pform_stencil_smem(int n);
 
 cudaError_t launch_twiddles(float* F32, double* F64, int n, cudaStream_t s);
 template <typename T>

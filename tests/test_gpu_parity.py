@@ -51,6 +51,16 @@ def test_apply_A_bitwise(lib, n, B, kind):
     assert np.array_equal(y, ref), np.max(np.abs(y - ref))
 
 
+@pytest.mark.parametrize("n,B", [(17, 3), (257, 2), (300, 2)])
+def test_apply_A_bitwise_ragged_tiles(lib, n, B):
+    # 2-D stencil tiles (16 rows x min(n, 256) columns): ragged last tile row (n = 17), ragged
+    # last tile column (n = 257: one column; n = 300: 44 columns), halos across tile borders.
+    k = sy.lognormal_k(n, B, 0.05, 4.0, seed=9)
+    x = sy.normal_field(n, B, seed=10)
+    y = host(lib.Problem(dev(k)).apply_A(dev(x)))
+    assert np.array_equal(y, orc.apply_A(k, x))
+
+
 @pytest.mark.parametrize("cfg_id", [3, 4, 5])
 def test_apply_A_full_configs(lib, cfg_id):
     cfg = sy.CONFIGS[cfg_id]
@@ -238,6 +248,15 @@ def test_identity_ragged(lib, n, B, m):
     k = sy.lognormal_k(n, B, 0.1, 1.0, 61)
     f = sy.normal_field(n, B, 62)
     _check_identity(lib, k, f, m, 1e-8, 3000, range(B))
+
+
+@pytest.mark.parametrize("n,B,m,maxit,systems", [(300, 2, 10, 40, [0, 1]), (512, 8, 10, 24, [0, 7])])
+def test_identity_prefix_wide_tiles(lib, n, B, m, maxit, systems):
+    # multi-column stencil tiles (n = 300) and the wide element-wise kernels (B*N >= 2^21 at
+    # n = 512, B = 8): residual histories and iterates bit-identical to the oracle over maxit steps
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 63)
+    f = sy.normal_field(n, B, 64)
+    _check_identity(lib, k, f, m, 1e-14, maxit, systems)
 
 
 @pytest.mark.parametrize("n", [4, 8])
