@@ -49,7 +49,7 @@ bool pdl_enabled() {
   }
 
 template <int RG>
-__global__ void __launch_bounds__(kStThreads, 3) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
+__global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
                                                            double* __restrict__ y, int n, double scale) {
   pdl_wait();
   pdl_trigger();
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k_apply_A(const double* __restr
   const StGeo g = st_geo(n);
   const double* xb = x + b * N;
   double* yb = y + b * N;
-  const bool fast = st_fill(g, n, k + b * N, sx, sk, [&](const StCells& cl, double (&xv)[kStCpt]) { st_load(cl, xb, xv); });
+  const bool fast = st_fill(g, n, k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, xb, sx); });
   const StWalk<RG> w(g);
   const double none[RG] = {};
   st_walk_any<RG>(fast, g, w, n, scale, sx, sk, sbnd, none, [&](bool ok, int e, double, double v, double) {
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   const StGeo g = st_geo(n);
   const double* ub = d.u + b * N;
   double* rb = d.r + b * N;
-  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl, double (&xv)[kStCpt]) { st_load(cl, ub, xv); });
+  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, ub, sx); });
   const StWalk<RG> w(g);
   double fx[RG];
   st_rows(g, w, n, d.f + b * N, fx);
@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_window_dots(FcgDev d) {
     const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
     wv[q] = e < d.N ? d.w[(size_t)b * d.N + e] : 0.0;
   }
-  window_dots_beta<EPT>(d, b, blockIdx.x, i, mi, wv);
+  window_dots_pairs<EPT>(d, b, blockIdx.x, i, mi, wv);
 }
 
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
@@ -248,24 +248,38 @@ __global__ void __launch_bounds__(kStThreads, 2) k_pform_stencil(FcgDev d) {
   double* pout = d.ring_p + ((size_t)slot * d.B + b) * N;
   const double* wb = d.w + b * N;
   int bad = 0;
-  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl, double (&xv)[kStCpt]) {
-    // w and then the window vectors newest -> oldest (R13), each a batch of kStCpt loads; these
-    // vectors are read-only here, so the loads may pass the ring stores below
+  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) {
+    // w and then the window vectors newest -> oldest (R13), two vectors per batch of 2*kStCpt
+    // loads; these vectors are read-only here, so the loads may pass the ring stores below
+    double xv[kStCpt];
     st_load(cl, wb, xv);
 #pragma unroll
     for (int u = 0; u < kStCpt; ++u)
       if ((cl.own >> u & 1u) && !isfinite(xv[u])) bad = 1;
-    for (int t = mi - 1; t >= 0; --t) {
-      double pv[kStCpt];
-      st_load(cl, sptr[t], pv);
-      const double bt = sbeta[t];
+    int t = mi - 1;
+    for (; t >= 1; t -= 2) {
+      double pa[kStCpt], pb[kStCpt];
+      st_load(cl, sptr[t], pa);
+      st_load(cl, sptr[t - 1], pb);
+      const double ba = sbeta[t], bb = sbeta[t - 1];
 #pragma unroll
       for (int u = 0; u < kStCpt; ++u)
-        if (cl.in >> u & 1u) xv[u] = __dsub_rn(xv[u], __dmul_rn(bt, pv[u]));   // outside stays 0
+        if (cl.in >> u & 1u) xv[u] = __dsub_rn(__dsub_rn(xv[u], __dmul_rn(ba, pa[u])), __dmul_rn(bb, pb[u]));
+    }
+    if (t == 0) {
+      double pa[kStCpt];
+      st_load(cl, sptr[0], pa);
+      const double ba = sbeta[0];
+#pragma unroll
+      for (int u = 0; u < kStCpt; ++u)
+        if (cl.in >> u & 1u) xv[u] = __dsub_rn(xv[u], __dmul_rn(ba, pa[u]));   // outside stays 0
     }
 #pragma unroll
-    for (int u = 0; u < kStCpt; ++u)
+    for (int u = 0; u < kStCpt; ++u) {
+      const int c = threadIdx.x + u * kStThreads;
+      if (c < cl.cells) sx[c] = xv[u];
       if (cl.own >> u & 1u) pout[cl.e[u]] = xv[u];
+    }
   });
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d.flags + b, FLAG_NONFINITE);
   const StWalk<RG> w(g);
