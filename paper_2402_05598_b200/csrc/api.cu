@@ -28,6 +28,7 @@ struct fcgno_problem {
   float* khat32;
   double* khat64;
   bool no_ok;
+  bool kfast;   // every k in [2^-400, 2^400]: stencil faces by the branch-free division (fcg_device.cuh)
 };
 
 namespace {
@@ -225,14 +226,14 @@ int fcgno_assemble(fcgno_grid g, const double* k, void* ws, size_t ws_bytes, voi
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, w.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  if (bad) return fail(FCGNO_ENONPOS_K, "assemble: k has a non-positive or non-finite entry");
+  if (bad & 1) return fail(FCGNO_ENONPOS_K, "assemble: k has a non-positive or non-finite entry");
   CK(launch_twiddles(w.F32, w.F64, g.n, s));
   const bool no_ok = no_grid_ok(g.n);
   if (no_ok) {
     CK(launch_khat<double>(k, w.F64, w.part, w.khat64, g.n, g.batch, ngroups_of(g.n), s));
     CK(launch_khat<float>(k, w.F32, reinterpret_cast<float*>(w.part), w.khat32, g.n, g.batch, ngroups_of(g.n), s));
   }
-  fcgno_problem* p = new fcgno_problem{g.n, g.batch, k, w.F32, w.F64, w.khat32, w.khat64, no_ok};
+  fcgno_problem* p = new fcgno_problem{g.n, g.batch, k, w.F32, w.F64, w.khat32, w.khat64, no_ok, (bad & 2) == 0};
   *out = p;
   return FCGNO_OK;
 }
@@ -242,7 +243,7 @@ void fcgno_problem_destroy(fcgno_problem* p) { delete p; }
 int fcgno_apply_A(const fcgno_problem* p, const double* x, double* y, void* stream) {
   if (!p || !x || !y) return fail(FCGNO_EINVAL, "apply_A: NULL argument");
   if (x == y) return fail(FCGNO_EINVAL, "apply_A: y must not alias x");
-  CK(launch_apply_A(p->k, x, y, p->n, p->B, static_cast<cudaStream_t>(stream)));
+  CK(launch_apply_A(p->k, x, y, p->n, p->B, p->kfast, static_cast<cudaStream_t>(stream)));
   return FCGNO_OK;
 }
 
@@ -671,7 +672,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     d.n = p->n; d.B = nb; d.N = p->n * p->n; d.nblk = nblk_of(p->n);
     d.m = o.m; d.maxit = o.maxit; d.schedule = o.schedule; d.tol = o.tol;
     d.scale = double(p->n + 1) * double(p->n + 1);
-    d.k = ln.p.k; d.f = f + b0 * N; d.u = u + b0 * N; d.w = nd ? ln.sw.wvec : d.r;
+    d.k = ln.p.k; d.kfast = p->kfast ? 1 : 0; d.f = f + b0 * N; d.u = u + b0 * N; d.w = nd ? ln.sw.wvec : d.r;
     d.status = status + b0; d.iters = iters + b0;
     d.hist = history ? history + (size_t)b0 * (o.maxit + 1) : nullptr;
   }

@@ -50,7 +50,7 @@ bool pdl_enabled() {
 
 template <int RG>
 __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
-                                                           double* __restrict__ y, int n, double scale) {
+                                                           double* __restrict__ y, int n, double scale, int fast) {
   pdl_wait();
   pdl_trigger();
   ST_SMEM;
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restr
   const StGeo g = st_geo(n);
   const double* xb = x + b * N;
   double* yb = y + b * N;
-  const bool fast = st_fill(g, n, k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, xb, sx); });
+  st_fill(g, n, k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, xb, sx); });
   const StWalk<RG> w(g);
   const double none[RG] = {};
   st_walk_any<RG>(fast, g, w, n, scale, sx, sk, sbnd, none, [&](bool ok, int e, double, double v, double) {
@@ -67,9 +67,10 @@ __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restr
   });
 }
 
-cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, cudaStream_t s) {
+cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, bool kfast, cudaStream_t s) {
   cudaError_t e;
-  ST_LAUNCH(e, n, k_apply_A, dim3((unsigned)st_tiles(n), (unsigned)B), s, k, x, y, n, double(n + 1) * double(n + 1));
+  ST_LAUNCH(e, n, k_apply_A, dim3((unsigned)st_tiles(n), (unsigned)B), s, k, x, y, n, double(n + 1) * double(n + 1),
+            kfast ? 1 : 0);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
@@ -127,9 +128,11 @@ __global__ void k_check_k(const double* __restrict__ k, size_t count, int* bad) 
   int local = 0;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < count; t += (size_t)gridDim.x * blockDim.x) {
     const double v = k[t];
-    if (!(v > 0.0) || !isfinite(v)) local = 1;
+    if (!(v > 0.0) || !isfinite(v)) local |= 1;
+    if (!k_inrange(v)) local |= 2;   // outside the branch-free division's range (fcg_device.cuh)
   }
-  if (__syncthreads_or(local) && threadIdx.x == 0) atomicOr(bad, 1);
+  const int any1 = __syncthreads_or(local & 1), any2 = __syncthreads_or(local & 2);
+  if (threadIdx.x == 0 && (any1 || any2)) atomicOr(bad, (any1 ? 1 : 0) | (any2 ? 2 : 0));
 }
 
 cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t s) {
@@ -150,7 +153,8 @@ __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   const StGeo g = st_geo(n);
   const double* ub = d.u + b * N;
   double* rb = d.r + b * N;
-  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, ub, sx); });
+  const bool fast = d.kfast != 0;
+  st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, ub, sx); });
   const StWalk<RG> w(g);
   double fx[RG];
   st_rows(g, w, n, d.f + b * N, fx);
@@ -226,7 +230,7 @@ cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
 // p to the ring; phase 2 applies the stencil from shared memory, writes s and accumulates (p,s)
 // and (p,r).  The system's last CTA forms gamma = (p,s), alpha = (p,r)/gamma and flags breakdown.
 template <int RG>
-__global__ void __launch_bounds__(kStThreads, 2) k_pform_stencil(FcgDev d) {
+__global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   pdl_wait();
   pdl_trigger();
   ST_SMEM;
@@ -248,7 +252,8 @@ __global__ void __launch_bounds__(kStThreads, 2) k_pform_stencil(FcgDev d) {
   double* pout = d.ring_p + ((size_t)slot * d.B + b) * N;
   const double* wb = d.w + b * N;
   int bad = 0;
-  const bool fast = st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) {
+  const bool fast = d.kfast != 0;
+  st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) {
     // w and then the window vectors newest -> oldest (R13), two vectors per batch of 2*kStCpt
     // loads; these vectors are read-only here, so the loads may pass the ring stores below
     double xv[kStCpt];

@@ -16,6 +16,7 @@ struct FcgDev {
   int m, maxit, schedule;
   double tol, scale;          // scale = (n+1)^2
   const double* k;            // [B][N]
+  int kfast;                  // problem's k all in [2^-400, 2^400] (branch-free face division)
   const double* f;            // [B][N]
   double* u;                  // [B][N]  caller's iterate
   double* r;                  // [B][N]  residual
@@ -111,7 +112,7 @@ struct ProfHook {
 };
 
 // Launch helpers (defined in fcg_kernels.cu / no_kernels.cu).  All return cudaGetLastError().
-cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, cudaStream_t s);
+cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, bool kfast, cudaStream_t s);
 cudaError_t launch_dot(const double* x, const double* y, double* out, dd* part, unsigned* cnt, int n, int B,
                        cudaStream_t s);
 cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t s);

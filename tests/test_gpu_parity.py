@@ -61,6 +61,18 @@ def test_apply_A_bitwise_ragged_tiles(lib, n, B):
     assert np.array_equal(y, orc.apply_A(k, x))
 
 
+def test_apply_A_bitwise_wide_range_k(lib):
+    # k outside [2^-400, 2^400]: the faces take the guarded IEEE division path (assemble clears
+    # the problem's fast-division flag); inside it, the branch-free path.  Both bitwise.
+    rng = np.random.default_rng(11)
+    n, B = 150, 2
+    x = sy.normal_field(n, B, seed=12)
+    for lo, hi in ((-150.0, 150.0), (-100.0, 100.0)):
+        k = 10.0 ** rng.uniform(lo, hi, size=(B, n, n))
+        y = host(lib.Problem(dev(k)).apply_A(dev(x)))
+        assert np.array_equal(y, orc.apply_A(k, x))
+
+
 @pytest.mark.parametrize("cfg_id", [3, 4, 5])
 def test_apply_A_full_configs(lib, cfg_id):
     cfg = sy.CONFIGS[cfg_id]
