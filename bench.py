@@ -126,6 +126,8 @@ class ClockSampler:
     def start(self, settle_s: float = 15.0):
         """Start sampling and wait (bounded) for the first sample: NVML initialisation inside
         nvidia-smi briefly stalls the GPU and must not overlap a timed step."""
+        if os.environ.get("BENCH_NO_SMI"):   # A/B of the sampler's own effect on step times
+            return
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
                                           "--format=csv,noheader,nounits", "-lms", "200"],
@@ -443,12 +445,11 @@ def run_reference(args):
 SWEEP_SEEDS = {1024: 110, 2048: 111}
 
 
-def sweep_window_sizes(m, check_every, maxit):
-    """m_i of the iterations the in-graph profiler samples (the first of every graph chunk)."""
-    out = []
-    for i in range(0, maxit, check_every):
-        out.append(min(i, max(1, i % (m + 1))))
-    return out
+def sweep_samples(m, check_every, maxit):
+    """(i, m_i, m_{i+1}) of the iterations the in-graph profiler samples (the first of every graph
+    chunk)."""
+    sched = lambda i: min(i, max(1, i % (m + 1)))
+    return [(i, sched(i), sched(i + 1)) for i in range(0, maxit, check_every)]
 
 
 def run_sweep(args):
@@ -463,8 +464,8 @@ def run_sweep(args):
       launches of one sampled iteration per chunk; check_every = 12 makes the sampled iterations'
       windows m_i cycle through 1, 2, ..., 10 like the run's own.
     Algorithmic bytes per unknown (fp64): apply_A 24 (x, k read; y written); dot 16;
-    window dots (1 + m_i) 8; p-form + stencil (5 + m_i) 8 (w, m_i p_k, k, r read; p, s written);
-    update 48 (u, p, r, s read; u, r written)."""
+    p-form + stencil (6 + m_i) 8 (w = r, m_i p_k, k, u read; u (lazy x update), p, s written;
+    4 * 8 at i = 0); window dots (1 + m_i) 8; update 3 * 8 (r, s read; r written)."""
     import torch
 
     import synthetic as sy
@@ -544,14 +545,14 @@ def run_sweep(args):
         solver.solve(f, u)
         torch.cuda.synchronize()
         prof = F.profile_read()
-        mis = sweep_window_sizes(m, ce, maxit)
-        for name, per_mi in (("k_window_dots", lambda mi: (1 + mi) * 8 if mi else 0),
-                             ("k_pform_stencil", lambda mi: (5 + mi) * 8),
-                             ("k_update", lambda mi: 48)):
+        samp = sweep_samples(m, ce, maxit)
+        for name, per_it in (("k_window_dots", lambda i, mi, mi1: (1 + mi) * 8 if mi else 0),
+                             ("k_pform_stencil", lambda i, mi, mi1: (6 + mi) * 8 if i else 4 * 8),
+                             ("k_update", lambda i, mi, mi1: 3 * 8)):
             ms, cnt = prof.get(name, (0.0, 0))
             if not cnt:
                 continue
-            nb = sum(per_mi(mi) for mi in mis) * B * N
+            nb = sum(per_it(*x) for x in samp) * B * N
             gbs = nb / (ms * 1e-3) / 1e9
             rows.append({"kernel": name, "n": n, "batch": B, "us_per_launch": ms * 1e3 / cnt,
                          "bytes_per_unknown": nb / (B * N * cnt), "achieved_gbs": gbs, "frac": gbs / hbm,
@@ -568,7 +569,7 @@ def run_sweep(args):
         e1.synchronize()
         it_ms = e0.elapsed_time(e1) / maxit
         m_bar = mean_window(m, maxit)
-        bpu = (12 + 2 * m_bar) * 8
+        bpu = (10 + 2 * m_bar) * 8   # window (1 + m_i) 8 + p-form (6 + m_i) 8 + update 3 * 8
         gbs = bpu * B * N / (it_ms * 1e-3) / 1e9
         rows.append({"kernel": "identity FCG iteration", "n": n, "batch": B, "us_per_iteration": it_ms * 1e3,
                      "bytes_per_unknown": bpu, "achieved_gbs": gbs, "frac": gbs / hbm,

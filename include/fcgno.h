@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FCGNO_ABI_VERSION 2
+#define FCGNO_ABI_VERSION 3
 #define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
 #define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
 #define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
@@ -107,9 +107,9 @@ typedef enum {
   FCGNO_PROF_NO_INPUT = 3,   /* k_dft_rows + k_lift_mix: DFT of r/||r|| and layer-1 mixing */
   FCGNO_PROF_WINDOW = 4,     /* k_window_dots (identity preconditioner only) */
   FCGNO_PROF_PFORM = 5,      /* unused since ABI 2 (p is formed inside k_pform_stencil) */
-  FCGNO_PROF_STENCIL = 6,    /* k_pform_stencil: p = w - sum beta p, s = A p, (p,s), (p,r); one launch
+  FCGNO_PROF_STENCIL = 6,    /* k_pform_stencil: lazy u += alpha p, p = w - sum beta p, s = A p, (p,s), (p,r); one launch
                                 per iteration */
-  FCGNO_PROF_UPDATE = 7,     /* k_update: u, r update, (r,r), convergence bookkeeping */
+  FCGNO_PROF_UPDATE = 7,     /* k_update: r update, (r,r), convergence bookkeeping (u is updated lazily) */
   FCGNO_PROF_FINALIZE = 8,   /* unused since ABI 2 (folded into k_update) */
   FCGNO_PROF_NO_YDIR = 9,    /* k_yan + k_ysyn: y-direction DFTs of the tensor-core NO path */
   FCGNO_PROF_NCLASS = 10

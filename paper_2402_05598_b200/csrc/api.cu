@@ -625,6 +625,62 @@ int build_chunk(Chunk& c, int iters, int mask, const fcgno_no_desc* nd, const vo
   if (e != cudaSuccess) return cuda_fail(e, "graph instantiate");
   return FCGNO_OK;
 }
+// Device-side iteration loop: one graph whose WHILE node replays a body of `chunk` unrolled
+// iterations followed by k_loop_cond (condition: a system is still running), so a solve is one
+// graph launch and the GPU never waits for the host.  Returns FCGNO_OK, or -1 when the graph could
+// not be built (the caller then uses the host-polled chunk loop).
+struct DeviceLoop {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  int kernels = 0;   // kernels of one body replay
+  void destroy() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr; graph = nullptr;
+  }
+};
+
+int build_device_loop(DeviceLoop& L, int chunk, const fcgno_no_desc* nd, const void* packed, const Lane& ln,
+                      cudaStream_t s) {
+  const uint64_t before = launch_counter();
+  cudaGraphConditionalHandle h;
+  cudaGraphNode_t node;
+  cudaGraphNodeParams np{};
+  if (cudaGraphCreate(&L.graph, 0) != cudaSuccess) return -1;
+  if (cudaGraphConditionalHandleCreate(&h, L.graph, 1, cudaGraphCondAssignDefault) != cudaSuccess) return -1;
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  if (cudaGraphAddNode(&node, L.graph, nullptr, 0, &np) != cudaSuccess) return -1;
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return -1;
+  int per = 0, total = 0;
+  for (int t = 0; t < chunk && per >= 0; ++t) {
+    per = enqueue_iteration(ln.sw.d, nd, packed, &ln.p, ln.sw, s, nullptr);
+    total += per;
+  }
+  const cudaError_t ec = (per >= 0) ? launch_loop_cond(ln.sw.d.active, h, s) : cudaErrorUnknown;
+  cudaGraph_t out = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(s, &out);
+  launch_counter() = before;   // captured, not launched
+  if (per < 0 || ec != cudaSuccess || ee != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -1;
+  }
+  L.kernels = total + 1;
+  if (cudaGraphInstantiate(&L.exec, L.graph, 0) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return -1;
+  }
+  return FCGNO_OK;
+}
+
+bool host_loop_forced() {
+  const char* e = getenv("FCGNO_HOSTLOOP");
+  return e && e[0] == '1';
+}
 }  // namespace
 
 size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd, fcgno_solve_opts o) {
@@ -717,6 +773,29 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     if ((rc = build_chunk(full[0], chunk, mask, nd, packed, lanes, nl, st, ev_fj)) != FCGNO_OK) break;
     if (mask && (rc = build_chunk(full[1], chunk, mask, nd, packed, lanes, nl, st, ev_fj)) != FCGNO_OK) break;
     if (o.maxit % chunk && (rc = build_chunk(tail, o.maxit % chunk, mask, nd, packed, lanes, nl, st, ev_fj)) != FCGNO_OK) break;
+    // default: the whole iteration loop on the device (one graph launch); the host-polled chunk
+    // loop below is kept for in-graph profiling (event nodes are not allowed in conditional
+    // bodies), batch lanes, and as a fallback
+    DeviceLoop dl;
+    bool device_loop = false;
+    if (nl == 1 && mask == 0 && !host_loop_forced()) {
+      device_loop = build_device_loop(dl, chunk, nd, packed, lanes[0], s) == FCGNO_OK;
+      if (!device_loop) dl.destroy();
+    }
+    if (device_loop) {
+      if ((e = cudaGraphLaunch(dl.exec, s)) != cudaSuccess) rc = cuda_fail(e, "graph launch");
+      int it = 0;
+      if (rc == FCGNO_OK && (e = cudaMemcpyAsync(h_active, lanes[0].sw.d.iter, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+        rc = cuda_fail(e, "iteration count");
+      if (rc == FCGNO_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) rc = cuda_fail(e, "solve");
+      if (rc == FCGNO_OK) {
+        it = h_active[0];
+        launch_counter() += (uint64_t)dl.kernels * (uint64_t)((it + chunk - 1) / chunk > 0 ? (it + chunk - 1) / chunk : 1);
+      }
+      dl.destroy();
+      if (rc == FCGNO_OK && (e = launch_flush_x(lanes[0].sw.d, s)) != cudaSuccess) rc = cuda_fail(e, "flush_x");
+      break;
+    }
     int launched = 0, k = 0;
     Chunk* prev = nullptr;
     while (launched < o.maxit) {
@@ -742,6 +821,8 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
       if (done) break;
     }
     if (rc == FCGNO_OK && (e = cudaStreamSynchronize(s)) == cudaSuccess && mask && prev) prev->harvest();
+    for (int l = 0; l < nl && rc == FCGNO_OK; ++l)   // last lazy x update of the stopped systems
+      if ((e = launch_flush_x(lanes[l].sw.d, s)) != cudaSuccess) rc = cuda_fail(e, "flush_x");
   } while (false);
   cudaError_t e_end = cudaStreamSynchronize(s);
   for (int l = 1; l < nl; ++l) {

@@ -34,7 +34,7 @@ __host__ __device__ __forceinline__ int st_tiles(int n) {
 // double-double reduction and keep more loads in flight).
 constexpr int kEptWide = 16;
 __host__ __device__ __forceinline__ bool ew_wide(int n, int B) { return (size_t)n * n * B >= ((size_t)1 << 21); }
-constexpr int kEptUpdate = 8;          // k_update streams four vectors: fewer elements per thread
+constexpr int kEptUpdate = 16;         // k_update streams two vectors (u is updated lazily)
 __host__ __device__ __forceinline__ int ew_blocks(int n, int ept) { return (n * n + kThreads * ept - 1) / (kThreads * ept); }
 // Capacity of the per-system partial arrays: the most CTAs any kernel launches per system.
 __host__ __device__ __forceinline__ int part_cap(int n) {

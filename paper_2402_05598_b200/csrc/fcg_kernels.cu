@@ -1,13 +1,15 @@
 // fcg_kernels.cu — matrix-free stencil, inner products and the FCG(m) step kernels.
 //
-// One FCG iteration (Algorithm 1) is three launches, each one HBM sweep over
-// the vectors it touches; every reduction finishes inside the producing kernel (the last CTA of a
-// system reduces its partials in a fixed order), so there is no scalar-only launch:
-//   [NO output or k_window_dots]  (w, s_k) for the m_i window      -> beta_k = (w,s_k)/(p_k,s_k)
-//   k_pform_stencil                p = w - sum beta_k p_k (newest -> oldest); s = A p;
-//                                  (p,s), (p,r) -> alpha, breakdown
-//   k_update                       u += alpha p ; r -= alpha s ; (r,r); ||r||/||r0||, status,
-//                                  iteration counter
+// One FCG iteration (Algorithm 1) is two launches after the preconditioner, each
+// one HBM sweep over the vectors it touches; every reduction finishes inside the producing kernel
+// (the last CTA of a system reduces its partials in a fixed order), so there is no scalar-only
+// launch:
+//   [k_no_out* | k_window_dots]  w = B(r); (w, s_k) for the m_i window -> beta_k = (w,s_k)/(p_k,s_k)
+//   k_pform_stencil           u += alpha_{i-1} p_{i-1} (lazy x update); p = w - sum beta_k p_k
+//                             (newest -> oldest); s = A p; (p,s), (p,r) -> alpha, breakdown
+//   k_update                  r -= alpha s; (r,r); ||r||/||r0||, status, iteration counter
+//
+//   k_flush_x (once, after the solve)  the last lazy x update of the stopped systems
 // All arithmetic is fp64 in the oracle's operation order (R5, R6, R13) so identity
 // runs reproduce the oracle's residual histories bit for bit.
 #include "internal.h"
@@ -298,6 +300,25 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
     dot2_acc(p, q, s0, c0);
     dot2_acc(p, rv, s1, c1);
   });
+  if (i > 0) {
+    // lazy x update of the previous iteration, u += alpha_{i-1} p_{i-1}:
+    // the same single rounding as in k_update's place, one sweep of u fewer.  alpha[b] still holds
+    // alpha_{i-1}: this launch's last CTA overwrites it only after every CTA has passed here.
+    const double* pprev = sptr[mi - 1];   // newest window vector = p_{i-1}
+    double* ub = d.u + b * N;
+    const double al = d.alpha[b];
+    double uv[RG], pv[RG];
+#pragma unroll
+    for (int s = 0; s < RG; ++s) {
+      const int e = (g.i0 + w.r0 + s) * n + g.j0 + w.c;
+      const bool ok = w.valid(g, s);
+      uv[s] = ok ? ub[e] : 0.0;
+      pv[s] = ok ? __ldg(pprev + e) : 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < RG; ++s)
+      if (w.valid(g, s)) ub[(g.i0 + w.r0 + s) * n + g.j0 + w.c] = __dadd_rn(uv[s], __dmul_rn(al, pv[s]));
+  }
   dd v[2] = {dot2_finish(s0, c0), dot2_finish(s1, c1)};
   block_reduce_dd<2>(v, sm);
   if (threadIdx.x == 0) {
@@ -333,13 +354,14 @@ cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ u += alpha p ; r -= alpha s ; (r,r) ; bookkeeping
-// The last CTA of each system reduces (r, r) and applies the system's convergence / breakdown
-// bookkeeping (Algorithm 1's stopping test); the last system to arrive publishes the number of
-// systems still running and advances the iteration counter.  Systems flagged this iteration
-// skip the vector update but still take part in the arrival protocol.
+// ------------------------------------------------------------------ r -= alpha s ; (r,r) ; bookkeeping
+// u += alpha p is applied lazily by the next k_pform_stencil (or by k_flush_x after the solve), so
+// this kernel streams r and s only.  The last CTA of each system reduces (r, r) and applies the system's
+// convergence / breakdown bookkeeping (Algorithm 1's stopping test); the last system to arrive
+// publishes the number of systems still running and advances the iteration counter.  Systems
+// flagged this iteration skip the vector update but still take part in the arrival protocol.
 template <int EPT>
-__global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
+__global__ void __launch_bounds__(kThreads, 2) k_update(FcgDev d) {
   pdl_wait();
   pdl_trigger();
   __shared__ dd sm[8];
@@ -351,17 +373,13 @@ __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
   double s = 0.0, c = 0.0;
   if (fl == 0) {
     const double alpha = d.alpha[b];
-    const double* pb = d.ring_p + ((size_t)slot * d.B + b) * N;
     const double* sb = d.ring_s + ((size_t)slot * d.B + b) * N;
-    double* ub = d.u + (size_t)b * N;
     double* rb = d.r + (size_t)b * N;
-    double uv[EPT], pv[EPT], rv[EPT], sv[EPT];
+    double rv[EPT], sv[EPT];
 #pragma unroll
-    for (int q = 0; q < EPT; ++q) {   // all loads first: EPT x 4 in flight
+    for (int q = 0; q < EPT; ++q) {   // all loads first: EPT x 2 in flight
       const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
       const bool ok = e < N;
-      uv[q] = ok ? ub[e] : 0.0;
-      pv[q] = ok ? __ldg(pb + e) : 0.0;
       rv[q] = ok ? rb[e] : 0.0;
       sv[q] = ok ? __ldg(sb + e) : 0.0;
     }
@@ -369,10 +387,7 @@ __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
     for (int q = 0; q < EPT; ++q) {
       const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
       rv[q] = __dsub_rn(rv[q], __dmul_rn(alpha, sv[q]));
-      if (e < N) {
-        ub[e] = __dadd_rn(uv[q], __dmul_rn(alpha, pv[q]));
-        rb[e] = rv[q];
-      }
+      if (e < N) rb[e] = rv[q];
     }
 #pragma unroll
     for (int q = 0; q < EPT; ++q) dot2_acc(rv[q], rv[q], s, c);
@@ -415,6 +430,47 @@ __global__ void __launch_bounds__(kThreads) k_update(FcgDev d) {
       *d.iter = i + 1;
     }
   }
+}
+
+// Condition of the device-side iteration loop (a CUDA-graph WHILE node, api.cu): run another chunk
+// of iterations while any system of the batch is still running.
+__global__ void k_loop_cond(const int* __restrict__ active, cudaGraphConditionalHandle h) {
+  pdl_wait();
+  cudaGraphSetConditional(h, *active > 0 ? 1u : 0u);
+}
+
+cudaError_t launch_loop_cond(const int* active, cudaGraphConditionalHandle h, cudaStream_t s) {
+  cudaError_t e = launch_k(k_loop_cond, dim3(1), dim3(1), 0, s, active, h);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+// After the solve: the last lazy x update of every system that stopped in k_update (converged or
+// at maxit after >= 1 iteration), u += alpha_{iters-1} p_{iters-1}.
+template <int EPT>
+__global__ void __launch_bounds__(kThreads) k_flush_x(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.y;
+  const int st = d.status[b], it = d.iters[b];
+  if (!((st == SYS_CONVERGED || st == SYS_MAXIT) && it >= 1)) return;
+  const int N = d.N;
+  const double al = d.alpha[b];
+  const double* pb = d.ring_p + ((size_t)ring_slot(it - 1, d.m) * d.B + b) * N;
+  double* ub = d.u + (size_t)b * N;
+#pragma unroll
+  for (int q = 0; q < EPT; ++q) {
+    const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
+    if (e < N) ub[e] = __dadd_rn(ub[e], __dmul_rn(al, pb[e]));
+  }
+}
+
+cudaError_t launch_flush_x(const FcgDev& d, cudaStream_t s) {
+  cudaError_t e = launch_k(k_flush_x<kPerThread>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B),
+                           dim3(kThreads), 0, s, d);
+  if (e != cudaSuccess) return e;
+  ++launch_counter();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s) {

@@ -120,6 +120,8 @@ cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_flush_x(const FcgDev& d, cudaStream_t s);
+cudaError_t launch_loop_cond(const int* active, cudaGraphConditionalHandle h, cudaStream_t s);
 
 cudaError_t launch_twiddles(float* F32, double* F64, int n, cudaStream_t s);
 template <typename T>
