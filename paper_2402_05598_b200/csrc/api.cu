@@ -11,6 +11,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -677,6 +678,36 @@ int build_device_loop(DeviceLoop& L, int chunk, const fcgno_no_desc* nd, const v
   return FCGNO_OK;
 }
 
+// Instantiated device-loop graphs, reused across solves whose captured kernel arguments are
+// identical (same problem arrays, workspace carve, NO weights, options): a repeated solve is then
+// one graph launch with no capture / instantiation on the host.  Kernel arguments are captured by
+// value, so an identical key means an identical graph whatever allocation the pointers belong to.
+struct LoopKey {
+  FcgDev d;
+  fcgno_no_desc nd;
+  int has_nd, chunk;
+  const void* packed;
+  const void* pf[4];
+  int n, B, no_ok, kfast;   // the NO buffers are carved from the workspace after d.r (d) at
+};                          // offsets fixed by (n, B, nd, m): covered by the fields above
+struct LoopEntry { LoopKey key; DeviceLoop loop; uint64_t used; };
+std::vector<LoopEntry>& loop_cache() { static std::vector<LoopEntry> c; return c; }
+std::mutex& loop_cache_mutex() { static std::mutex m; return m; }   // held from lookup to launch
+// (an evicted exec still in flight is freed by CUDA when it completes)
+constexpr size_t kLoopCacheMax = 4;
+
+LoopKey loop_key(const Lane& ln, const fcgno_no_desc* nd, const void* packed, int chunk) {
+  LoopKey k;
+  std::memset(&k, 0, sizeof(k));   // padding bytes too: the key is compared with memcmp
+  k.d = ln.sw.d;
+  if (nd) { k.nd = *nd; k.has_nd = 1; }
+  k.chunk = chunk;
+  k.packed = packed;
+  k.pf[0] = ln.p.F32; k.pf[1] = ln.p.F64; k.pf[2] = ln.p.khat32; k.pf[3] = ln.p.khat64;
+  k.n = ln.p.n; k.B = ln.p.B; k.no_ok = ln.p.no_ok; k.kfast = ln.p.kfast;
+  return k;
+}
+
 bool host_loop_forced() {
   const char* e = getenv("FCGNO_HOSTLOOP");
   return e && e[0] == '1';
@@ -776,23 +807,44 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     // default: the whole iteration loop on the device (one graph launch); the host-polled chunk
     // loop below is kept for in-graph profiling (event nodes are not allowed in conditional
     // bodies), batch lanes, and as a fallback
-    DeviceLoop dl;
-    bool device_loop = false;
+    DeviceLoop* dlp = nullptr;
+    std::unique_lock<std::mutex> cache_lock(loop_cache_mutex(), std::defer_lock);
     if (nl == 1 && mask == 0 && !host_loop_forced()) {
-      device_loop = build_device_loop(dl, chunk, nd, packed, lanes[0], s) == FCGNO_OK;
-      if (!device_loop) dl.destroy();
+      cache_lock.lock();
+      static uint64_t tick = 0;
+      const LoopKey key = loop_key(lanes[0], nd, packed, chunk);
+      auto& cache = loop_cache();
+      for (auto& ent : cache)
+        if (std::memcmp(&ent.key, &key, sizeof(key)) == 0) { dlp = &ent.loop; ent.used = ++tick; break; }
+      if (!dlp) {
+        DeviceLoop dl;
+        if (build_device_loop(dl, chunk, nd, packed, lanes[0], s) == FCGNO_OK) {
+          if (cache.size() >= kLoopCacheMax) {   // evict the least recently used
+            size_t victim = 0;
+            for (size_t t = 1; t < cache.size(); ++t) if (cache[t].used < cache[victim].used) victim = t;
+            cache[victim].loop.destroy();
+            cache.erase(cache.begin() + victim);
+          }
+          cache.push_back(LoopEntry{key, dl, ++tick});
+          dlp = &cache.back().loop;
+        } else {
+          dl.destroy();
+        }
+      }
     }
-    if (device_loop) {
+    if (dlp) {
+      DeviceLoop& dl = *dlp;
       if ((e = cudaGraphLaunch(dl.exec, s)) != cudaSuccess) rc = cuda_fail(e, "graph launch");
+      const int kernels = dl.kernels;
+      cache_lock.unlock();
       int it = 0;
       if (rc == FCGNO_OK && (e = cudaMemcpyAsync(h_active, lanes[0].sw.d.iter, sizeof(int), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
         rc = cuda_fail(e, "iteration count");
       if (rc == FCGNO_OK && (e = cudaStreamSynchronize(s)) != cudaSuccess) rc = cuda_fail(e, "solve");
       if (rc == FCGNO_OK) {
         it = h_active[0];
-        launch_counter() += (uint64_t)dl.kernels * (uint64_t)((it + chunk - 1) / chunk > 0 ? (it + chunk - 1) / chunk : 1);
+        launch_counter() += (uint64_t)kernels * (uint64_t)((it + chunk - 1) / chunk > 0 ? (it + chunk - 1) / chunk : 1);
       }
-      dl.destroy();
       if (rc == FCGNO_OK && (e = launch_flush_x(lanes[0].sw.d, s)) != cudaSuccess) rc = cuda_fail(e, "flush_x");
       break;
     }

@@ -37,20 +37,26 @@ bool pdl_enabled() {
 // 2-D tiles (fcg_device.cuh st_fill / st_walk): x and k staged once with a one-cell halo, every
 // face computed once.  Grid (st_tiles(n), B), kStThreads threads, RG = st_rg(n) rows per thread.
 #define ST_SMEM                                                   \
-  __shared__ __align__(16) double sx[(kStR + 2) * (kStC + 2)];    \
-  __shared__ __align__(16) double sk[(kStR + 2) * (kStC + 2)];    \
+  __shared__ __align__(16) double sx[(kStR + 2) * kStSP];        \
+  __shared__ __align__(16) double sk[(kStR + 2) * kStSP];        \
   __shared__ double sbnd[kStR * (kStThreads / 32 + 1)]
 
-// launch KERNEL<RG> for the row-group size of n
-#define ST_LAUNCH(err, n, KERNEL, grid, s, ...)                                                      \
-  switch (st_rg(n)) {                                                                               \
-    case 1: err = launch_k(KERNEL<1>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
-    case 2: err = launch_k(KERNEL<2>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
-    case 4: err = launch_k(KERNEL<4>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
-    default: err = launch_k(KERNEL<8>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;           \
+// launch KERNEL<RG, PAIRS> for the row-group size of n; PAIRS (16-byte column pairs) when n is even
+#define ST_LAUNCH2(err, PAIRS, n, KERNEL, grid, s, ...)                                                       \
+  switch (st_rg(n)) {                                                                                         \
+    case 1: err = launch_k(KERNEL<1, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;               \
+    case 2: err = launch_k(KERNEL<2, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;               \
+    case 4: err = launch_k(KERNEL<4, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;               \
+    default: err = launch_k(KERNEL<8, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;              \
+  }
+#define ST_LAUNCH(err, n, KERNEL, grid, s, ...)                          \
+  if ((n) % 2 == 0) {                                                   \
+    ST_LAUNCH2(err, true, n, KERNEL, grid, s, __VA_ARGS__)              \
+  } else {                                                              \
+    ST_LAUNCH2(err, false, n, KERNEL, grid, s, __VA_ARGS__)             \
   }
 
-template <int RG>
+template <int RG, bool PAIRS>
 __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
                                                            double* __restrict__ y, int n, double scale, int fast) {
   pdl_wait();
@@ -61,7 +67,9 @@ __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restr
   const StGeo g = st_geo(n);
   const double* xb = x + b * N;
   double* yb = y + b * N;
-  st_fill(g, n, k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, xb, sx); });
+  st_copy<PAIRS>(g, n, k + b * N, sk);
+  st_copy<PAIRS>(g, n, xb, sx);
+  st_fill_end();
   const StWalk<RG> w(g);
   const double none[RG] = {};
   st_walk_any<RG>(fast, g, w, n, scale, sx, sk, sbnd, none, [&](bool ok, int e, double, double v, double) {
@@ -144,7 +152,7 @@ cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t
 }
 
 // ------------------------------------------------------------------ r0 = f - A u0
-template <int RG>
+template <int RG, bool PAIRS>
 __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -156,7 +164,9 @@ __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   const double* ub = d.u + b * N;
   double* rb = d.r + b * N;
   const bool fast = d.kfast != 0;
-  st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) { st_copy(cl, ub, sx); });
+  st_copy<PAIRS>(g, n, d.k + b * N, sk);
+  st_copy<PAIRS>(g, n, ub, sx);
+  st_fill_end();
   const StWalk<RG> w(g);
   double fx[RG];
   st_rows(g, w, n, d.f + b * N, fx);
@@ -231,7 +241,7 @@ cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
 // values recomputed, bit-identical to the owning CTA's) into shared memory and writes the tile's
 // p to the ring; phase 2 applies the stencil from shared memory, writes s and accumulates (p,s)
 // and (p,r).  The system's last CTA forms gamma = (p,s), alpha = (p,r)/gamma and flags breakdown.
-template <int RG>
+template <int RG, bool PAIRS>
 __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -253,41 +263,10 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   const StGeo g = st_geo(n);
   double* pout = d.ring_p + ((size_t)slot * d.B + b) * N;
   const double* wb = d.w + b * N;
-  int bad = 0;
   const bool fast = d.kfast != 0;
-  st_fill(g, n, d.k + b * N, sx, sk, [&](const StCells& cl) {
-    // w and then the window vectors newest -> oldest (R13), two vectors per batch of 2*kStCpt
-    // loads; these vectors are read-only here, so the loads may pass the ring stores below
-    double xv[kStCpt];
-    st_load(cl, wb, xv);
-#pragma unroll
-    for (int u = 0; u < kStCpt; ++u)
-      if ((cl.own >> u & 1u) && !isfinite(xv[u])) bad = 1;
-    int t = mi - 1;
-    for (; t >= 1; t -= 2) {
-      double pa[kStCpt], pb[kStCpt];
-      st_load(cl, sptr[t], pa);
-      st_load(cl, sptr[t - 1], pb);
-      const double ba = sbeta[t], bb = sbeta[t - 1];
-#pragma unroll
-      for (int u = 0; u < kStCpt; ++u)
-        if (cl.in >> u & 1u) xv[u] = __dsub_rn(__dsub_rn(xv[u], __dmul_rn(ba, pa[u])), __dmul_rn(bb, pb[u]));
-    }
-    if (t == 0) {
-      double pa[kStCpt];
-      st_load(cl, sptr[0], pa);
-      const double ba = sbeta[0];
-#pragma unroll
-      for (int u = 0; u < kStCpt; ++u)
-        if (cl.in >> u & 1u) xv[u] = __dsub_rn(xv[u], __dmul_rn(ba, pa[u]));   // outside stays 0
-    }
-#pragma unroll
-    for (int u = 0; u < kStCpt; ++u) {
-      const int c = threadIdx.x + u * kStThreads;
-      if (c < cl.cells) sx[c] = xv[u];
-      if (cl.own >> u & 1u) pout[cl.e[u]] = xv[u];
-    }
-  });
+  st_copy<PAIRS>(g, n, d.k + b * N, sk);
+  const int bad = st_pform<PAIRS>(g, n, wb, sptr, sbeta, mi, sx, pout);
+  st_fill_end();
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d.flags + b, FLAG_NONFINITE);
   const StWalk<RG> w(g);
   double rx[RG];
