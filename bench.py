@@ -15,6 +15,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -27,6 +28,7 @@ sys.path.insert(0, ROOT)
 METRIC = "batched FCG-NO unknown-iterations/s on 1 B200; % of HBM roofline per iteration"
 UNIT = "unknown-iterations/s"
 K_MODES = 20
+CONVERGE_MAXIT = {1: 500, 2: 5000, 3: 30000, 4: 30000, 5: 2000}   # SURVEY §8(d) D.2 identity maxit
 FP32_ALU_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # SMs x FP32 lanes x FMA x max SM clock
 
 
@@ -44,6 +46,9 @@ def parse_args(argv=None):
                     help="BASELINE configs[4] second half: isolated HBM bandwidth sweep of apply_A, the batched "
                          "dot and the FCG kernels at 1024^2 and 2048^2, batch 4 (one JSON line)")
     ap.add_argument("--sweep-n", type=int, nargs="*", default=[1024, 2048])
+    ap.add_argument("--precond", choices=["no", "identity", "structured"], default="no",
+                    help="no: the config's random-init SNO (the BASELINE workload, default); identity: FCG(I); "
+                         "structured: the convergent structured SNO of SURVEY C.2 #30 (solves/s and iterations)")
     return ap.parse_args(argv)
 
 
@@ -171,9 +176,10 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle)
-def cpu_oracle_rate(cfg, budget_s=12.0, max_iters=400):
+def cpu_oracle_rate(cfg, budget_s=12.0, max_iters=400, precond="no"):
     """The oracle as it stands: FCG-NO (fp64 NO, exact dots) on system 0 of the workload, on one
-    host thread, for as many iterations as fit ~budget_s.  Returns (unknown-iterations/s, sample)."""
+    host thread, for as many iterations as fit ~budget_s.  Returns (unknown-iterations/s, sample).
+    precond: "no" (the config's random-init SNO), "identity", or "structured" (SURVEY C.2 #30)."""
     import numpy as np
     from threadpoolctl import threadpool_limits
 
@@ -182,9 +188,10 @@ def cpu_oracle_rate(cfg, budget_s=12.0, max_iters=400):
     with threadpool_limits(limits=1):
         k = sy.make_k(cfg, systems=[0])[0]
         f = sy.make_f(cfg, systems=[0])[0]
-        params = orc.unpack_weights(sy.make_weights(cfg), cfg["width"])
+        blob = sy.make_weights(cfg) if precond == "no" else sy.structured_no_weights(cfg["width"], cfg["n"])
+        params = orc.unpack_weights(blob, cfg["width"])
         A = lambda x: orc.apply_A(k, x)
-        P = lambda r: orc.no_forward(params, r, k)
+        P = None if precond == "identity" else (lambda r: orc.no_forward(params, r, k))
         t0 = time.perf_counter()
         orc.fcg(A, f, np.zeros_like(f), cfg["m"], cfg["tol"], 3, precond=P)
         per_it = (time.perf_counter() - t0) / 3
@@ -194,7 +201,15 @@ def cpu_oracle_rate(cfg, budget_s=12.0, max_iters=400):
         dt = time.perf_counter() - t0
     N = cfg["n"] ** 2
     done = res["iters"]
-    return N * done / dt, f"system 0 of the workload, {done} FCG-NO iterations (fp64 NO, exact dots), {dt:.1f} s"
+    host = platform.processor() or platform.machine()
+    try:
+        host = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    kind = {"no": "FCG-NO (fp64 NO, exact dots)", "identity": "FCG(I) (exact dots)",
+            "structured": "FCG with the structured SNO (fp64, exact dots)"}[precond]
+    return N * done / dt, (f"system 0 of the workload, {done} {kind} iterations, {dt:.1f} s on 1 thread of "
+                           f"{host} ({os.cpu_count()} logical CPUs)")
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -211,6 +226,8 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = dict(sy.CONFIGS[args.config])
+    if args.precond != "no":   # converging runs: the iteration cap of SURVEY D.2's identity column
+        cfg["maxit"] = CONVERGE_MAXIT[args.config]
     if args.maxit:
         cfg["maxit"] = args.maxit
     n, B, w, m = cfg["n"], cfg["batch"], cfg["width"], cfg["m"]
@@ -218,11 +235,12 @@ def run_ours(args):
     systems = shard_systems(B, rank)
     k = sy.make_k(cfg, systems=systems)
     f = sy.make_f(cfg, systems=systems)
-    blob = sy.make_weights(cfg)
+    blob = sy.make_weights(cfg) if args.precond == "no" else sy.structured_no_weights(w, n)
     dk = torch.from_numpy(k).cuda()
     df = torch.from_numpy(f).cuda()
     prob = F.Problem(dk)
-    no = F.NeuralOperator(w, blob, precision=F.FP32 if cfg["no_precision"] == "fp32" else F.FP64)
+    no = None if args.precond == "identity" else \
+        F.NeuralOperator(w, blob, precision=F.FP32 if cfg["no_precision"] == "fp32" else F.FP64)
     solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False)
     u = torch.zeros_like(df)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
@@ -271,8 +289,12 @@ def run_ours(args):
     # dominant-kernel timing: a second timed pass of the same workload whose graphs carry CUDA
     # events around the layer launches of one sampled iteration per chunk (kept out of the pass
     # above: event nodes break programmatic-dependent-launch overlap and perturb the step time)
-    psolver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False,
-                       profile_mask=1 << F.PROF_NO_LAYER)
+    # (converging runs: a prefix short enough that every system is still running, so the bytes of
+    # every timed launch are known; identity: the dominant kernel is k_pform_stencil)
+    prof_maxit = {"no": cfg["maxit"], "structured": min(cfg["maxit"], 48), "identity": min(cfg["maxit"], 132)}[args.precond]
+    prof_every = 12 if args.precond == "identity" else 16
+    psolver = F.Solver(prob, m, cfg["tol"], prof_maxit, no=no, history=False, check_every=prof_every,
+                       profile_mask=1 << (F.PROF_STENCIL if no is None else F.PROF_NO_LAYER))
     u.zero_()
     psolver.solve(df, u)
     F.profile_reset()
@@ -296,7 +318,7 @@ def run_ours(args):
     ms_per_iter = (local_ms / args.steps) / max(iters_step, 1)
 
     # dominant kernel: the SNO layer kernel (3 launches per iteration), timed in-graph
-    layer_ms, layer_n = prof["k_no_layer"]
+    layer_ms, layer_n = prof["k_no_layer"] if no is not None else prof["k_pform_stencil"]
     avg_layer_ms = layer_ms / max(layer_n, 1)
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {"hbm_gbs": 6650.0}
@@ -309,7 +331,20 @@ def run_ours(args):
         except (ValueError, OSError):
             traffic = None
     tc_path = cfg["no_precision"] == "fp32" and 64 <= n <= 128 and n % 16 == 0 and w <= 128
-    if tc_path:
+    if no is None:
+        # identity FCG: k_pform_stencil, (6 + m_i) 8 B per unknown at the sampled iterations (w = r;
+        # 4 * 8 at i = 0), every system running
+        samp = [(i, min(i, max(1, i % (m + 1)))) for i in range(0, prof_maxit, prof_every)]
+        alg = sum(((6 + mi) * 8 if i else 32) for i, mi in samp) / len(samp) * B * N
+        achieved = alg / (avg_layer_ms * 1e-3) / 1e9
+        roofline = {"kernel": "k_pform_stencil", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved / hbm, "traffic": None, "algorithmic_bytes_per_launch": alg,
+                    "avg_launch_ms": avg_layer_ms, "launches_timed": layer_n,
+                    "share_of_step": avg_layer_ms / ms_per_iter,
+                    "timing": f"CUDA events inside the solve graphs, one sampled iteration per {prof_every} of a "
+                              f"{prof_maxit}-iteration prefix (all systems running)",
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, measured on this pool)"}
+    elif tc_path:
         # tcgen05 3xBF16 layer (k_tc_layer): activations stream through HBM; the MMA work (3 split
         # passes, padding included) needs < 1/3 of the HBM time, so the bound is HBM.
         alg = layer_bytes(B, n, w)
@@ -333,15 +368,20 @@ def run_ours(args):
                     "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (FFMA path; DESIGN.md §6)"}
 
     # per-iteration HBM roofline (the metric's second half)
-    m_bar = mean_window(m, cfg["maxit"])
-    bytes_iter = fcg_no_bytes_per_unknown(m_bar, w) * N * B
+    m_bar = mean_window(m, int(max(iters_step, 1)))
+    if no is None:   # identity FCG, fused-minimal: (7 + 2 m̄) 8 + 8 B per unknown
+        bytes_iter = ((7 + 2 * m_bar) * 8 + 8) * N * B
+    else:
+        bytes_iter = fcg_no_bytes_per_unknown(m_bar, w) * N * B
     hbm_frac = (bytes_iter / (hbm * 1e9)) / (ms_per_iter * 1e-3)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "bf16x3 split (NO tensor cores, fp32 accumulate) + f64 (FCG vectors, dots)",
-           "data": "synthetic (seeded; BASELINE configs[1] recipe, random-init NO weights)",
-           "config": {"workload": f"config{args.config}", "n": n, "batch": B, "m": m, "tol": cfg["tol"],
+           "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64" if no is None else "bf16x3 split (NO tensor cores, fp32 accumulate) + f64 (FCG vectors, dots)",
+           "data": "synthetic (seeded; BASELINE configs recipe, " + {"no": "random-init NO weights)", "identity":
+                   "identity preconditioner)", "structured": "structured SNO weights, SURVEY C.2 #30)"}[args.precond],
+           "config": {"workload": f"config{args.config}", "precond": args.precond, "n": n, "batch": B, "m": m, "tol": cfg["tol"],
                       "maxit": cfg["maxit"], "no_width": w, "no_precision": cfg["no_precision"],
                       "k_field": cfg["k"], "rhs": cfg["rhs"], "l2": "flushed (256 MiB write) before every step",
                       "parallelism": f"batch replicas x{world} (weak)"},
@@ -350,13 +390,19 @@ def run_ours(args):
            "hbm_roofline_per_iteration": {"algorithmic_bytes_per_iter": bytes_iter, "peak_gbs": hbm,
                                           "frac": hbm_frac},
            "roofline": roofline, "gpu_launches": int(launches), "clocks": clocks}
+    if args.precond != "no":   # converging runs: solves/s and iteration counts
+        it_host = solver.iters.cpu().numpy()
+        st_host = solver.status.cpu().numpy()
+        out["solves_per_s"] = B * world / (max_ms / args.steps / 1e3)
+        out["iterations"] = {"mean": float(it_host.mean()), "min": int(it_host.min()), "max": int(it_host.max()),
+                             "converged": int((st_host == F.CONVERGED).sum()), "of": int(B)}
 
     if not args.no_split and rank == 0:
         out["time_split_ms_per_iter"] = time_split(F, prob, no, cfg, df)
     if rank == 0:
         out["e2e"] = e2e_measure(F, no, cfg, k, f, args.steps)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, sample = cpu_oracle_rate(cfg)
+        rate, sample = cpu_oracle_rate(cfg, precond=args.precond)
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
     if world > 1:
         dist.barrier()
@@ -427,7 +473,7 @@ def run_reference(args):
         cfg["maxit"] = args.maxit
     rates, samples = [], []
     for step in range(args.warmup + args.steps):
-        rate, sample = cpu_oracle_rate(cfg, budget_s=4.0, max_iters=100)
+        rate, sample = cpu_oracle_rate(cfg, budget_s=4.0, max_iters=100, precond=args.precond)
         if step >= args.warmup:
             rates.append(rate); samples.append(sample)
     value = statistics.mean(rates)

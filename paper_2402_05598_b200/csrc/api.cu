@@ -112,7 +112,7 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
   r.rpart = c.take<T>((size_t)B * ngroups_of(n) * kModes2 * 2);
   r.v0 = c.take<T>((size_t)B * w * N);
   r.v1 = c.take<T>((size_t)B * w * N);
-  r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
+  r.chat = c.take<T>((size_t)kRowSplitMax * kModes2 * B * w * 2);   // row-split partials (FFMA layer)
   r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
   if (sizeof(T) == sizeof(float) && tc_layer_supported_host(n, w)) {
     const TcGeom g(n, w);

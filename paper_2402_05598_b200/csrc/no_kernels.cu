@@ -329,6 +329,10 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   const int b = blockIdx.y, og = blockIdx.x * GO;
   if (a.status && a.status[b] != SYS_RUNNING) return;
   const int n = a.n, N = a.N, cin = a.cin, w = a.w, RC = a.rows;
+  // row split (gridDim.z parts): this CTA's rows [ia, ib); its y-analysis is partial z of chat,
+  // summed by k_mix in a fixed order
+  const int nrc = (n + RC - 1) / RC, z = blockIdx.z, nz = gridDim.z;
+  const int ia = (int)(((long long)nrc * z / nz)) * RC, ib = min(n, (int)(((long long)nrc * (z + 1) / nz)) * RC);
   const int go = min(GO, w - og);
   const int nbuf = a.nbuf;
   const LayerSmem<T, GO> L(n, cin, RC, nbuf);
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
     }
     cp_async_commit();
   };
-  if (!FIRST && nbuf == 2) stage(0, 0);
+  if (!FIRST && nbuf == 2 && ia < ib) stage(ia, 0);
 
   for (int t = threadIdx.x; t < cin * GO; t += blockDim.x) {
     const int c = t / GO, o = t - c * GO;
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   __syncthreads();
 
   int it = 0;
-  for (int i0 = 0; i0 < n; i0 += RC, ++it) {
+  for (int i0 = ia; i0 < ib; i0 += RC, ++it) {
     const int rows = min(RC, n - i0), npix = rows * n;
     const size_t base = (size_t)i0 * n;
     T* Vin = VinB + (size_t)((FIRST || nbuf == 1) ? 0 : (it & 1)) * cin * CH;
@@ -403,7 +407,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
         Vin[npix + t] = (T)kb[t];
       }
     } else if (nbuf == 2) {
-      if (i0 + RC < n) { stage(i0 + RC, (it + 1) & 1); cp_async_wait<1>(); }
+      if (i0 + RC < ib) { stage(i0 + RC, (it + 1) & 1); cp_async_wait<1>(); }
       else cp_async_wait<0>();
     } else {
       stage(i0, 0);
@@ -490,7 +494,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
     const int e = threadIdx.x + q * 256;
     if (e < GO * kModes2) {
       const int o = e % GO, kk = e / GO;
-      if (o < go) a.chat[((size_t)kk * a.B + b) * w + og + o] = T2{accr[q], acci[q]};
+      if (o < go) a.chat[(((size_t)z * kModes2 + kk) * a.B + b) * w + og + o] = T2{accr[q], acci[q]};
     }
   }
 }
@@ -705,6 +709,25 @@ size_t no_max_smem(int n, int w) {
 template size_t no_max_smem<float>(int, int);
 template size_t no_max_smem<double>(int, int);
 
+// Row split of the FFMA layer kernel: parts per system such that (CTAs x parts) fills the SMs
+// once at the kernel's occupancy, at most kRowSplitMax and one row chunk per part.
+static int layer_row_split(const void* fn, size_t smem, int ctas, int row_chunks) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess || per_sm < 1) {
+    (void)cudaGetLastError();
+    per_sm = 1;
+  }
+  int nz = (sms * per_sm) / (ctas > 0 ? ctas : 1);
+  nz = nz < 1 ? 1 : (nz > kRowSplitMax ? kRowSplitMax : nz);
+  return nz < row_chunks ? nz : row_chunks;
+}
+
 // The tensor-core path keeps the mixed spectra mode-major ([400][B][cout]); the FFMA path [B][cout][400].
 template <typename T>
 static bool tc_layout_modes(const NoDev<T>& no) {
@@ -752,6 +775,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     launches += 1;
   }
   unsigned char* vblob[2] = {no.vb0, no.vb1};
+  int nparts = 1;
   for (int l = 0; l < 3; ++l) {
     if (tc_path) {
       TcLayerArgsHost h{};
@@ -787,11 +811,17 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
         la.cin = w; la.W = pk + no.L.W[l - 1]; la.bias = pk + no.L.b[l - 1]; la.vin = vbuf[(l - 1) & 1];
       }
       const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, nbuf).total * sizeof(T);
+      // split the rows of each system over gridDim.z CTAs until the grid fills the SMs once
+      // (large n, few systems: config 5 has 6 x 8 CTAs of one per SM otherwise)
+      const void* fn = l == 0 ? (const void*)k_no_layer<T, true, GO> : (const void*)k_no_layer<T, false, GO>;
+      const int nz = layer_row_split(fn, smem, (int)(lgrid.x * lgrid.y), (n + rows - 1) / rows);
+      nparts = nz;
+      const dim3 g3(lgrid.x, lgrid.y, nz);
       pb(PROF_NO_LAYER);
       if (l == 0) {
-        launch_k(k_no_layer<T, true, GO>, lgrid, dim3(256), smem, s, la);
+        launch_k(k_no_layer<T, true, GO>, g3, dim3(256), smem, s, la);
       } else {
-        launch_k(k_no_layer<T, false, GO>, lgrid, dim3(256), smem, s, la);
+        launch_k(k_no_layer<T, false, GO>, g3, dim3(256), smem, s, la);
       }
       pe(PROF_NO_LAYER);
       ++launches;
@@ -806,7 +836,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
                     (float)inv_n2, status, s);
     else
       launch_k(k_mix<T>, dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), dim3(256), msmem, s,
-               (const T2*)chat, Rm, ghat, B, w, cout, inv_n2, status, 1);
+               (const T2*)chat, Rm, ghat, B, w, cout, inv_n2, status, nparts);
     pe(PROF_NO_MIX);
     ++launches;
     if (tc_path && l < 2) {
