@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256) k_mix(const typename Cplx<T>::type* __res
 // ------------------------------------------------------------------ operator layer (layers 1-3)
 template <typename T>
 struct LayerArgs {
-  int n, N, w, cin, B, rows, nbuf, use_gelu;
+  int n, N, w, cin, B, rows, nbuf, use_gelu, fsm;
   const double* r; const double* rr; const double* k;   // FIRST layer inputs
   const T* vin;                                          // [B][cin][N] (layers 2, 3)
   const T* W;                                            // [w][cin]
@@ -268,14 +268,13 @@ struct LayerArgs {
   const int* status;
 };
 
-constexpr int kFsmemMaxN = 128;   // stage the twiddle table in shared memory up to this n
 
 template <typename T, int GO>
 struct LayerSmem {
   // element offsets (in T) of each region; complex regions are 2 T per entry
   size_t Wsm, bsm, gh, Fs, Vin, Vout, Gs, Tx, total;
   int nbuf;
-  __host__ __device__ LayerSmem(int n, int cin, int rows, int nbuf_) {
+  __host__ __device__ LayerSmem(int n, int cin, int rows, int nbuf_, int fs) {
     const int CH = rows * n;
     nbuf = nbuf_;                               // 2: double-buffered input rows (cp.async)
     size_t o = 0;
@@ -283,7 +282,7 @@ struct LayerSmem {
     Wsm = o; o = al(o + (size_t)cin * GO);
     bsm = o; o = al(o + GO);
     gh = o; o = al(o + (size_t)2 * GO * kGhStride);
-    Fs = o; o = al(o + (n <= kFsmemMaxN ? (size_t)2 * n * kModes : 0));
+    Fs = o; o = al(o + (fs ? (size_t)2 * n * kModes : 0));
     Vin = o; o = al(o + (size_t)nbuf * cin * CH);
     Vout = o; o = al(o + (size_t)GO * CH);
     Gs = o; o = al(o + (size_t)2 * rows * kModes * GO);
@@ -296,15 +295,19 @@ template <typename T> constexpr int layer_go() { return sizeof(T) == 4 ? 8 : 4; 
 
 // Rows per chunk (up to 256 pixels) and input buffering: halve the rows, then drop the second
 // buffer, until the CTA's shared memory fits the opt-in limit.
+// The twiddle table is staged in shared memory whenever it fits (dropped last): for n >= 256 its
+// global reads sat on the dependent x-analysis / y-synthesis loops.
 template <typename T>
-void layer_config(int n, int cin, bool first, size_t limit, int* rows_out, int* nbuf_out) {
-  int nbuf = first ? 1 : 2;
+void layer_config(int n, int cin, bool first, size_t limit, int* rows_out, int* nbuf_out, int* fs_out) {
+  int nbuf = first ? 1 : 2, fs = 1;
   int rows = n >= 256 ? 1 : 256 / n;
-  auto bytes = [&]() { return LayerSmem<T, layer_go<T>()>(n, cin, rows, nbuf).total * sizeof(T); };
+  auto bytes = [&]() { return LayerSmem<T, layer_go<T>()>(n, cin, rows, nbuf, fs).total * sizeof(T); };
   while (rows > 1 && bytes() > limit) rows = (rows + 1) / 2;
   if (bytes() > limit) nbuf = 1;
+  if (bytes() > limit) fs = 0;
   *rows_out = rows;
   *nbuf_out = nbuf;
+  *fs_out = fs;
 }
 
 __device__ __forceinline__ void cp_async_bytes16(void* sdst, const void* gsrc) {
@@ -335,7 +338,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   const int ia = (int)(((long long)nrc * z / nz)) * RC, ib = min(n, (int)(((long long)nrc * (z + 1) / nz)) * RC);
   const int go = min(GO, w - og);
   const int nbuf = a.nbuf;
-  const LayerSmem<T, GO> L(n, cin, RC, nbuf);
+  const LayerSmem<T, GO> L(n, cin, RC, nbuf, a.fsm);
   extern __shared__ __align__(16) unsigned char smraw[];
   T* sm = reinterpret_cast<T*>(smraw);
   T* Wsm = sm + L.Wsm;           // [cin][GO]
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(256) k_no_layer(const LayerArgs<T> a) {
   T2* Tx = reinterpret_cast<T2*>(sm + L.Tx);      // [GO][RC*20+1]
   const int TXS = RC * kModes + 1;
   const int CH = RC * n;
-  const bool fsm = n <= kFsmemMaxN;
+  const bool fsm = a.fsm != 0;
   T2* Fsm = reinterpret_cast<T2*>(sm + L.Fs);
   const T2* Ft = fsm ? Fsm : a.F;                 // twiddles exp(-2 pi i kappa j / n), [n][20]
 
@@ -700,9 +703,9 @@ template <typename T>
 size_t no_max_smem(int n, int w) {
   constexpr int GO = layer_go<T>();
   const size_t lim = (size_t)optin_smem() - 2048;
-  int rows1, nbuf1;
-  layer_config<T>(n, w, false, lim, &rows1, &nbuf1);
-  size_t m = LayerSmem<T, GO>(n, w, rows1, nbuf1).total * sizeof(T);
+  int rows1, nbuf1, fs1;
+  layer_config<T>(n, w, false, lim, &rows1, &nbuf1, &fs1);
+  size_t m = LayerSmem<T, GO>(n, w, rows1, nbuf1, fs1).total * sizeof(T);
   const size_t msmem = ((size_t)w * w + (size_t)kMixBatch * w) * 2 * sizeof(T);
   return m > msmem ? m : msmem;
 }
@@ -799,9 +802,9 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       launches += 2;
     } else {
       LayerArgs<T> la{};
-      int rows, nbuf;
-      layer_config<T>(n, l == 0 ? 2 : w, l == 0, lim, &rows, &nbuf);
-      la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.nbuf = nbuf; la.use_gelu = no.use_gelu;
+      int rows, nbuf, fs;
+      layer_config<T>(n, l == 0 ? 2 : w, l == 0, lim, &rows, &nbuf, &fs);
+      la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.nbuf = nbuf; la.use_gelu = no.use_gelu; la.fsm = fs;
       la.r = r; la.rr = rr; la.k = no.k;
       la.ghat = ghat; la.F = F; la.chat = chat; la.status = status;
       la.vout = vbuf[l & 1];
@@ -810,7 +813,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       } else {
         la.cin = w; la.W = pk + no.L.W[l - 1]; la.bias = pk + no.L.b[l - 1]; la.vin = vbuf[(l - 1) & 1];
       }
-      const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, nbuf).total * sizeof(T);
+      const size_t smem = LayerSmem<T, GO>(n, la.cin, rows, nbuf, fs).total * sizeof(T);
       // split the rows of each system over gridDim.z CTAs until the grid fills the SMs once
       // (large n, few systems: config 5 has 6 x 8 CTAs of one per SM otherwise)
       const void* fn = l == 0 ? (const void*)k_no_layer<T, true, GO> : (const void*)k_no_layer<T, false, GO>;
