@@ -20,7 +20,8 @@ Readings:
       the system stops with iters = i;
   R6  inner products are correctly rounded (oracle/dots.py);
   R15 u0 is an input (BASELINE configs use u0 = 0; P:102's u0 ~ N(0,1) is used for the
-      Table 1 pin).
+      Table 1 pin);
+  R21 optional fp32 storage of r, w, p, s (vec32, BASELINE configs[2] "fp32 or fp64 FCG").
 """
 from __future__ import annotations
 
@@ -42,19 +43,30 @@ def m_schedule(i: int, m_max: int, schedule: str = "paper") -> int:
     raise ValueError(schedule)
 
 
-def fcg(apply_A, f, u0, m_max, tol, maxit, precond=None, schedule="paper"):
+def _round32(x):
+    """Store a vector in fp32 (round to nearest) and read it back as fp64 (exact)."""
+    return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def fcg(apply_A, f, u0, m_max, tol, maxit, precond=None, schedule="paper", vec32=False):
     """Algorithm 1 for one system.  apply_A(x) -> A x; precond(r) -> w (None = identity).
 
+    vec32 (reading R21, SURVEY C.2 #28 "vectors and ring in fp32, dots accumulated in fp64"): the
+    residual r, the preconditioned residual w and the stored directions p, s are kept in fp32; each
+    is computed in fp64 from the stored values exactly as below and rounded once when stored; the
+    iterate u, the inner products (correctly rounded, R6) and the scalars stay fp64.
+
     Returns dict(u, r, hist, iters, status)."""
+    st = _round32 if vec32 else (lambda x: x)
     u = np.array(u0, dtype=np.float64, copy=True)
-    r = np.asarray(f, dtype=np.float64) - apply_A(u)
+    r = st(np.asarray(f, dtype=np.float64) - apply_A(u))
     rho0 = math.sqrt(dot(r, r))
     hist = [1.0]
     if rho0 == 0.0:
         return dict(u=u, r=r, hist=np.array(hist), iters=0, status=CONVERGED)
     P, S, G = [], [], []          # stored p_k, s_k, (p_k, s_k); newest last
     for i in range(maxit):
-        w = r.copy() if precond is None else np.asarray(precond(r), dtype=np.float64)
+        w = r.copy() if precond is None else st(np.asarray(precond(r), dtype=np.float64))
         if not np.all(np.isfinite(w)):
             return dict(u=u, r=r, hist=np.array(hist), iters=i, status=NONFINITE)
         mi = m_schedule(i, m_max, schedule)
@@ -63,13 +75,14 @@ def fcg(apply_A, f, u0, m_max, tol, maxit, precond=None, schedule="paper"):
         p = w.copy()
         for kk in reversed(window):
             p = p - betas[kk] * P[kk]
-        s = apply_A(p)
+        p = st(p)
+        s = st(apply_A(p))
         gamma = dot(p, s)
         if not (gamma > 0.0 and math.isfinite(gamma)):
             return dict(u=u, r=r, hist=np.array(hist), iters=i, status=BREAKDOWN)
         alpha = dot(p, r) / gamma
         u = u + alpha * p
-        r = r - alpha * s
+        r = st(r - alpha * s)
         hist.append(math.sqrt(dot(r, r)) / rho0)
         P.append(p); S.append(s); G.append(gamma)
         if len(P) > m_max:                      # windows never reach further back

@@ -188,3 +188,43 @@ def test_breakdown_and_nonfinite_status():
     assert res["status"] == orc.BREAKDOWN and res["iters"] == 0
     res = orc.fcg(A, np.zeros_like(f), np.zeros_like(f), 5, 1e-8, 10)
     assert res["status"] == orc.CONVERGED and res["iters"] == 0
+
+
+# ----------------------------------------------------------------------------- fp32 vector storage (R21)
+def test_vec32_stored_vectors_are_fp32_and_history_consistent():
+    # R21: r, w, p, s stored in fp32; the history is ||r||/||r0|| of the stored residuals.
+    k = sy.lognormal_k(12, 1, 0.1, 1.0, 41)[0]
+    f = np.random.default_rng(42).normal(size=(12, 12))
+    A = lambda x: orc.apply_A(k, x)
+    res = orc.fcg(A, f, np.zeros_like(f), 5, 1e-6, 400, vec32=True)
+    r = res["r"]
+    assert np.array_equal(r, r.astype(np.float32).astype(np.float64))
+    r0 = f.astype(np.float32).astype(np.float64)   # u0 = 0: r0 = fl32(f)
+    assert res["hist"][-1] == np.sqrt(orc.dot(r, r)) / np.sqrt(orc.dot(r0, r0))
+    assert res["status"] == orc.CONVERGED
+
+
+def test_vec32_poisson_prefix_matches_fp64_to_fp32_rounding():
+    # k = 1, n = 8: the fp32-stored run is FCG up to fp32 rounding (first 15 relative residuals
+    # within 1e-6 of the fp64 run) and converges to 1e-10 within +-3 iterations of it.
+    n = 8
+    k = np.ones((n, n))
+    f = np.random.default_rng(3).normal(size=(n, n))
+    A = lambda x: orc.apply_A(k, x)
+    a = orc.fcg(A, f, np.zeros_like(f), 5, 1e-10, 200, vec32=True)
+    b = orc.fcg(A, f, np.zeros_like(f), 5, 1e-10, 200)
+    assert np.max(np.abs(a["hist"][:15] / b["hist"][:15] - 1.0)) < 1e-6
+    assert a["status"] == orc.CONVERGED and abs(a["iters"] - b["iters"]) <= 3
+
+
+def test_vec32_exact_inverse_one_step():
+    # SPEC.md:194 with fp32 storage: B = A^{-1} (dense, n = 6) leaves a residual at fp32 rounding.
+    n = 6
+    k = sy.lognormal_k(n, 1, 0.1, 1.0, 43)[0]
+    N = n * n
+    Ad = np.stack([orc.apply_A(k, e.reshape(n, n)).ravel() for e in np.eye(N)], axis=1)
+    Ainv = np.linalg.inv(Ad)
+    f = np.random.default_rng(44).normal(size=(n, n))
+    res = orc.fcg(lambda x: orc.apply_A(k, x), f, np.zeros_like(f), 5, 1e-5, 5,
+                  precond=lambda r: (Ainv @ r.ravel()).reshape(n, n), vec32=True)
+    assert res["iters"] == 1 and res["hist"][1] < 1e-5
