@@ -46,6 +46,8 @@ def parse_args(argv=None):
                     help="BASELINE configs[4] second half: isolated HBM bandwidth sweep of apply_A, the batched "
                          "dot and the FCG kernels at 1024^2 and 2048^2, batch 4 (one JSON line)")
     ap.add_argument("--sweep-n", type=int, nargs="*", default=[1024, 2048])
+    ap.add_argument("--vec32", action="store_true",
+                    help="FCG vectors and ring stored in fp32 (BASELINE configs[2] variant, DESIGN.md R21)")
     ap.add_argument("--precond", choices=["no", "identity", "structured"], default="no",
                     help="no: the config's random-init SNO (the BASELINE workload, default); identity: FCG(I); "
                          "structured: the convergent structured SNO of SURVEY C.2 #30 (solves/s and iterations)")
@@ -107,11 +109,10 @@ def mean_window(m, iters):
     return tot / max(iters, 1)
 
 
-def fcg_no_bytes_per_unknown(m_bar, w):
+def fcg_no_bytes_per_unknown(m_bar, w, S=8):
     """Algorithmic HBM bytes per unknown per FCG-NO iteration (fused-minimal
-    FCG part with fp64 vectors, plus the NO's input/output and materialised fp32 activations
+    FCG part with S-byte vectors, plus the NO's input/output and materialised fp32 activations
     v1..v3 written and read once)."""
-    S = 8
     fcg = (9 + 2 * m_bar) * S + 8
     no = S + 8 + S + 6 * w * 4
     return fcg + no
@@ -241,7 +242,7 @@ def run_ours(args):
     prob = F.Problem(dk)
     no = None if args.precond == "identity" else \
         F.NeuralOperator(w, blob, precision=F.FP32 if cfg["no_precision"] == "fp32" else F.FP64)
-    solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False)
+    solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False, vec_fp32=args.vec32)
     u = torch.zeros_like(df)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     # clock sampler first: nvidia-smi's start-up stalls the GPU briefly, so it must land in the
@@ -294,7 +295,7 @@ def run_ours(args):
     prof_maxit = {"no": cfg["maxit"], "structured": min(cfg["maxit"], 48), "identity": min(cfg["maxit"], 132)}[args.precond]
     prof_every = 12 if args.precond == "identity" else 16
     psolver = F.Solver(prob, m, cfg["tol"], prof_maxit, no=no, history=False, check_every=prof_every,
-                       profile_mask=1 << (F.PROF_STENCIL if no is None else F.PROF_NO_LAYER))
+                       profile_mask=1 << (F.PROF_STENCIL if no is None else F.PROF_NO_LAYER), vec_fp32=args.vec32)
     u.zero_()
     psolver.solve(df, u)
     F.profile_reset()
@@ -369,10 +370,11 @@ def run_ours(args):
 
     # per-iteration HBM roofline (the metric's second half)
     m_bar = mean_window(m, int(max(iters_step, 1)))
-    if no is None:   # identity FCG, fused-minimal: (7 + 2 m̄) 8 + 8 B per unknown
-        bytes_iter = ((7 + 2 * m_bar) * 8 + 8) * N * B
+    S = 4 if args.vec32 else 8
+    if no is None:   # identity FCG, fused-minimal: (7 + 2 m̄) S + 8 B per unknown
+        bytes_iter = ((7 + 2 * m_bar) * S + 8) * N * B
     else:
-        bytes_iter = fcg_no_bytes_per_unknown(m_bar, w) * N * B
+        bytes_iter = fcg_no_bytes_per_unknown(m_bar, w, S) * N * B
     hbm_frac = (bytes_iter / (hbm * 1e9)) / (ms_per_iter * 1e-3)
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -381,7 +383,8 @@ def run_ours(args):
            "dtype": "f64" if no is None else "bf16x3 split (NO tensor cores, fp32 accumulate) + f64 (FCG vectors, dots)",
            "data": "synthetic (seeded; BASELINE configs recipe, " + {"no": "random-init NO weights)", "identity":
                    "identity preconditioner)", "structured": "structured SNO weights, SURVEY C.2 #30)"}[args.precond],
-           "config": {"workload": f"config{args.config}", "precond": args.precond, "n": n, "batch": B, "m": m, "tol": cfg["tol"],
+           "config": {"workload": f"config{args.config}", "precond": args.precond,
+                      "fcg_vectors": "fp32" if args.vec32 else "fp64", "n": n, "batch": B, "m": m, "tol": cfg["tol"],
                       "maxit": cfg["maxit"], "no_width": w, "no_precision": cfg["no_precision"],
                       "k_field": cfg["k"], "rhs": cfg["rhs"], "l2": "flushed (256 MiB write) before every step",
                       "parallelism": f"batch replicas x{world} (weak)"},
@@ -398,9 +401,9 @@ def run_ours(args):
                              "converged": int((st_host == F.CONVERGED).sum()), "of": int(B)}
 
     if not args.no_split and rank == 0:
-        out["time_split_ms_per_iter"] = time_split(F, prob, no, cfg, df)
+        out["time_split_ms_per_iter"] = time_split(F, prob, no, cfg, df, vec32=args.vec32)
     if rank == 0:
-        out["e2e"] = e2e_measure(F, no, cfg, k, f, args.steps)
+        out["e2e"] = e2e_measure(F, no, cfg, k, f, args.steps, args.vec32)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sample = cpu_oracle_rate(cfg, precond=args.precond)
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
@@ -411,10 +414,11 @@ def run_ours(args):
         print(json.dumps(out), flush=True)
 
 
-def time_split(F, prob, no, cfg, df, iters=64):
+def time_split(F, prob, no, cfg, df, iters=64, vec32=False):
     """Instrumented solve (every kernel class timed in-graph) -> ms per iteration per phase."""
     import torch
-    s = F.Solver(prob, cfg["m"], cfg["tol"], iters, no=no, history=False, profile_mask=(1 << F.PROF_NCLASS) - 1)
+    s = F.Solver(prob, cfg["m"], cfg["tol"], iters, no=no, history=False, profile_mask=(1 << F.PROF_NCLASS) - 1,
+                 vec_fp32=vec32)
     u = torch.zeros_like(df)
     s.solve(df, u)
     F.profile_reset()
@@ -432,13 +436,13 @@ def time_split(F, prob, no, cfg, df, iters=64):
                     "(instrumented run, 64 iterations; per sampled iteration)"}
 
 
-def e2e_measure(F, no, cfg, k, f, steps):
+def e2e_measure(F, no, cfg, k, f, steps, vec32=False):
     """Same metric through the host-buffer C-ABI entry point: H2D of k, f, u0 from pinned memory,
     assemble, solve, D2H of u, iters, status, all inside the timed region."""
     import numpy as np
     import torch
     n, B = cfg["n"], cfg["batch"]
-    hs = F.HostSolver(n, B, cfg["m"], cfg["tol"], cfg["maxit"], no=no)
+    hs = F.HostSolver(n, B, cfg["m"], cfg["tol"], cfg["maxit"], no=no, vec_fp32=vec32)
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
     kh, fh = pin(k), pin(f)
     uh = torch.zeros((B, n, n), dtype=torch.float64).pin_memory().numpy()

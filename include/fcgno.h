@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FCGNO_ABI_VERSION 3
+#define FCGNO_ABI_VERSION 4
 #define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
 #define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
 #define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
@@ -97,6 +97,11 @@ typedef struct {
                            first unrolled iteration of every graph chunk (one sampled iteration
                            per check_every) with CUDA events recorded inside the solve's graphs;
                            0 = no instrumentation */
+  int32_t vec_fp32;     /* 0: r, w and the (p_k, s_k) ring in fp64 (default).  1: stored in fp32
+                           (BASELINE configs[2] "fp32 or fp64 FCG variants"; R21): every
+                           vector operation is computed in fp64 from the stored values and rounded
+                           once when stored; u, the inner products (correctly rounded) and the
+                           scalars stay fp64. */
 } fcgno_solve_opts;
 
 /* Kernel classes for in-graph CUDA-event profiling (diagnostics; bench.py). */

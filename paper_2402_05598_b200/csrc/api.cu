@@ -436,10 +436,15 @@ SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgn
   const size_t N = (size_t)n * n;
   const int nblk = nblk_of(n);
   FcgDev& d = s.d;
-  d.r = c.take<double>(B * N);
-  s.wvec = nd ? c.take<double>(B * N) : nullptr;
-  d.ring_p = c.take<double>((size_t)(o.m + 1) * B * N);
-  d.ring_s = c.take<double>((size_t)(o.m + 1) * B * N);
+  // r, w and the ring in fp64, or fp32 with opts.vec_fp32 (reading R21; the FcgDev fields then
+  // point at float arrays), plus an fp64 copy of r for the NO input
+  const size_t es = o.vec_fp32 ? sizeof(float) : sizeof(double);
+  d.vec32 = o.vec_fp32 ? 1 : 0;
+  d.r = reinterpret_cast<double*>(c.take<unsigned char>(es * B * N));
+  s.wvec = nd ? reinterpret_cast<double*>(c.take<unsigned char>(es * B * N)) : nullptr;
+  d.r64 = (nd && o.vec_fp32) ? c.take<double>(B * N) : nullptr;
+  d.ring_p = reinterpret_cast<double*>(c.take<unsigned char>(es * (o.m + 1) * B * N));
+  d.ring_s = reinterpret_cast<double*>(c.take<unsigned char>(es * (o.m + 1) * B * N));
   d.gamma = c.take<double>((size_t)(o.m + 1) * B);
   d.beta = c.take<double>((size_t)B * kMmax);
   d.alpha = c.take<double>(B);
@@ -461,6 +466,7 @@ int check_opts(const fcgno_solve_opts& o) {
   if (o.m < 1 || o.m > FCGNO_MMAX) return fail(FCGNO_EINVAL, "m=%d outside [1, %d]", o.m, FCGNO_MMAX);
   if (o.maxit < 0) return fail(FCGNO_EINVAL, "maxit < 0");
   if (o.schedule != FCGNO_SCHEDULE_PAPER && o.schedule != FCGNO_SCHEDULE_SLIDING) return fail(FCGNO_EINVAL, "bad schedule");
+  if (o.vec_fp32 != 0 && o.vec_fp32 != 1) return fail(FCGNO_EINVAL, "vec_fp32 must be 0 or 1");
   if (!(o.tol >= 0.0) && !std::isnan(o.tol)) return fail(FCGNO_EINVAL, "tol < 0");
   return FCGNO_OK;
 }
@@ -535,10 +541,10 @@ int enqueue_iteration(const FcgDev& d, const fcgno_no_desc* nd, const void* pack
     cudaError_t e;
     if (nd->precision == FCGNO_FP64) {
       NoDev<double> no = make_nodev<double>(p, *nd, packed, sw.n64, p->F64, p->khat64);
-      e = launch_no_forward<double>(no, d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
+      e = launch_no_forward<double>(no, d.vec32 ? d.r64 : d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
     } else {
       NoDev<float> no = make_nodev<float>(p, *nd, packed, sw.n32, p->F32, p->khat32);
-      e = launch_no_forward<float>(no, d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
+      e = launch_no_forward<float>(no, d.vec32 ? d.r64 : d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
     }
     if (e != cudaSuccess) return -1;
     count += nl;

@@ -41,22 +41,29 @@ bool pdl_enabled() {
   __shared__ __align__(16) double sk[(kStR + 2) * kStSP];        \
   __shared__ double sbnd[kStR * (kStThreads / 32 + 1)]
 
-// launch KERNEL<RG, PAIRS> for the row-group size of n; PAIRS (16-byte column pairs) when n is even
-#define ST_LAUNCH2(err, PAIRS, n, KERNEL, grid, s, ...)                                                       \
+// launch KERNEL<RG, PAIRS, V> for the row-group size of n; PAIRS (column pairs) when n is even; V
+// the storage type of the FCG vectors (double, or float with opts.vec_fp32, reading R21)
+#define ST_LAUNCH2(err, PAIRS, V, n, KERNEL, grid, s, ...)                                                    \
   switch (st_rg(n)) {                                                                                         \
-    case 1: err = launch_k(KERNEL<1, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;               \
-    case 2: err = launch_k(KERNEL<2, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;               \
-    case 4: err = launch_k(KERNEL<4, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;               \
-    default: err = launch_k(KERNEL<8, PAIRS>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;              \
+    case 1: err = launch_k(KERNEL<1, PAIRS, V>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
+    case 2: err = launch_k(KERNEL<2, PAIRS, V>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
+    case 4: err = launch_k(KERNEL<4, PAIRS, V>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;            \
+    default: err = launch_k(KERNEL<8, PAIRS, V>, grid, dim3(kStThreads), 0, s, __VA_ARGS__); break;           \
   }
-#define ST_LAUNCH(err, n, KERNEL, grid, s, ...)                          \
+#define ST_LAUNCH(err, n, V, KERNEL, grid, s, ...)                       \
   if ((n) % 2 == 0) {                                                   \
-    ST_LAUNCH2(err, true, n, KERNEL, grid, s, __VA_ARGS__)              \
+    ST_LAUNCH2(err, true, V, n, KERNEL, grid, s, __VA_ARGS__)           \
   } else {                                                              \
-    ST_LAUNCH2(err, false, n, KERNEL, grid, s, __VA_ARGS__)             \
+    ST_LAUNCH2(err, false, V, n, KERNEL, grid, s, __VA_ARGS__)          \
+  }
+#define ST_LAUNCH_VEC(err, d, KERNEL, grid, s, ...)                     \
+  if ((d).vec32) {                                                      \
+    ST_LAUNCH(err, (d).n, float, KERNEL, grid, s, __VA_ARGS__)          \
+  } else {                                                              \
+    ST_LAUNCH(err, (d).n, double, KERNEL, grid, s, __VA_ARGS__)         \
   }
 
-template <int RG, bool PAIRS>
+template <int RG, bool PAIRS, typename V>   // V unused: apply_A works on caller fp64 vectors
 __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restrict__ k, const double* __restrict__ x,
                                                            double* __restrict__ y, int n, double scale, int fast) {
   pdl_wait();
@@ -79,7 +86,7 @@ __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restr
 
 cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, int B, bool kfast, cudaStream_t s) {
   cudaError_t e;
-  ST_LAUNCH(e, n, k_apply_A, dim3((unsigned)st_tiles(n), (unsigned)B), s, k, x, y, n, double(n + 1) * double(n + 1),
+  ST_LAUNCH(e, n, double, k_apply_A, dim3((unsigned)st_tiles(n), (unsigned)B), s, k, x, y, n, double(n + 1) * double(n + 1),
             kfast ? 1 : 0);
   if (e != cudaSuccess) return e;
   ++launch_counter();
@@ -152,7 +159,7 @@ cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t
 }
 
 // ------------------------------------------------------------------ r0 = f - A u0
-template <int RG, bool PAIRS>
+template <int RG, bool PAIRS, typename V>
 __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -162,7 +169,8 @@ __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   const size_t N = (size_t)d.N;
   const StGeo g = st_geo(n);
   const double* ub = d.u + b * N;
-  double* rb = d.r + b * N;
+  V* rb = reinterpret_cast<V*>(d.r) + b * N;
+  double* r64 = d.r64 ? d.r64 + b * N : nullptr;   // fp64 copy of an fp32 r for the NO input
   const bool fast = d.kfast != 0;
   st_copy<PAIRS>(g, n, d.k + b * N, sk);
   st_copy<PAIRS>(g, n, ub, sx);
@@ -172,8 +180,11 @@ __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   st_rows(g, w, n, d.f + b * N, fx);
   double s = 0.0, c = 0.0;
   st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, fx, [&](bool ok, int e, double, double v, double fv) {
-    const double rv = ok ? __dsub_rn(fv, v) : 0.0;
-    if (ok) rb[e] = rv;
+    const double rv = ok ? rnd<V>(__dsub_rn(fv, v)) : 0.0;   // stored value (R21)
+    if (ok) {
+      rb[e] = (V)rv;
+      if (r64) r64[e] = rv;
+    }
     dot2_acc(rv, rv, s, c);
   });
   dd v[1] = {dot2_finish(s, c)};
@@ -198,14 +209,14 @@ __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
 
 cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s) {
   cudaError_t e;
-  ST_LAUNCH(e, d.n, k_init_residual, dim3((unsigned)st_tiles(d.n), (unsigned)d.B), s, d);
+  ST_LAUNCH_VEC(e, d, k_init_residual, dim3((unsigned)st_tiles(d.n), (unsigned)d.B), s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ (w, s_k) window dots (identity B)
-template <int EPT>
+template <int EPT, typename V>
 __global__ void __launch_bounds__(kThreads, 2) k_window_dots(FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -218,19 +229,22 @@ __global__ void __launch_bounds__(kThreads, 2) k_window_dots(FcgDev d) {
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {
     const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
-    wv[q] = e < d.N ? d.w[(size_t)b * d.N + e] : 0.0;
+    wv[q] = e < d.N ? (double)reinterpret_cast<const V*>(d.w)[(size_t)b * d.N + e] : 0.0;
   }
-  window_dots_pairs<EPT>(d, b, blockIdx.x, i, mi, wv);
+  window_dots_pairs<EPT, V>(d, b, blockIdx.x, i, mi, wv);
+}
+
+template <typename V>
+static cudaError_t launch_window_dots_t(const FcgDev& d, cudaStream_t s) {
+  if (ew_wide(d.n, d.B))
+    return launch_k(k_window_dots<kEptWide, V>, dim3((unsigned)ew_blocks(d.n, kEptWide), (unsigned)d.B), dim3(kThreads),
+                    0, s, d);
+  return launch_k(k_window_dots<kPerThread, V>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B),
+                  dim3(kThreads), 0, s, d);
 }
 
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e;
-  if (ew_wide(d.n, d.B))
-    e = launch_k(k_window_dots<kEptWide>, dim3((unsigned)ew_blocks(d.n, kEptWide), (unsigned)d.B), dim3(kThreads), 0,
-                 s, d);
-  else
-    e = launch_k(k_window_dots<kPerThread>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B), dim3(kThreads),
-                 0, s, d);
+  const cudaError_t e = d.vec32 ? launch_window_dots_t<float>(d, s) : launch_window_dots_t<double>(d, s);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
@@ -241,14 +255,14 @@ cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s) {
 // values recomputed, bit-identical to the owning CTA's) into shared memory and writes the tile's
 // p to the ring; phase 2 applies the stencil from shared memory, writes s and accumulates (p,s)
 // and (p,r).  The system's last CTA forms gamma = (p,s), alpha = (p,r)/gamma and flags breakdown.
-template <int RG, bool PAIRS>
+template <int RG, bool PAIRS, typename V>
 __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   pdl_wait();
   pdl_trigger();
   ST_SMEM;
   __shared__ dd sm[16];
   __shared__ double sbeta[kMmax];
-  __shared__ const double* sptr[kMmax];
+  __shared__ const V* sptr[kMmax];
   const int b = blockIdx.y;
   if (d.status[b] != SYS_RUNNING) return;
   const int i = *d.iter;
@@ -257,25 +271,26 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   const size_t N = (size_t)d.N;
   for (int q = threadIdx.x; q < mi; q += blockDim.x) {
     sbeta[q] = d.beta[(size_t)b * kMmax + q];
-    sptr[q] = d.ring_p + ((size_t)ring_slot(i - mi + q, d.m) * d.B + b) * N;
+    sptr[q] = reinterpret_cast<const V*>(d.ring_p) + ((size_t)ring_slot(i - mi + q, d.m) * d.B + b) * N;
   }
   __syncthreads();
   const StGeo g = st_geo(n);
-  double* pout = d.ring_p + ((size_t)slot * d.B + b) * N;
-  const double* wb = d.w + b * N;
+  V* pout = reinterpret_cast<V*>(d.ring_p) + ((size_t)slot * d.B + b) * N;
+  const V* wb = reinterpret_cast<const V*>(d.w) + b * N;
   const bool fast = d.kfast != 0;
   st_copy<PAIRS>(g, n, d.k + b * N, sk);
-  const int bad = st_pform<PAIRS>(g, n, wb, sptr, sbeta, mi, sx, pout);
+  const int bad = st_pform<PAIRS, V>(g, n, wb, sptr, sbeta, mi, sx, pout);
   st_fill_end();
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d.flags + b, FLAG_NONFINITE);
   const StWalk<RG> w(g);
   double rx[RG];
-  st_rows(g, w, n, d.r + b * N, rx);
-  double* sout = d.ring_s + ((size_t)slot * d.B + b) * N;
+  st_rows<RG, V>(g, w, n, reinterpret_cast<const V*>(d.r) + b * N, rx);
+  V* sout = reinterpret_cast<V*>(d.ring_s) + ((size_t)slot * d.B + b) * N;
   double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
   st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, rx, [&](bool ok, int e, double pv, double sv, double rv) {
-    if (ok) sout[e] = sv;
-    const double p = ok ? pv : 0.0, q = ok ? sv : 0.0;
+    const double sr = rnd<V>(sv);   // s as stored (R21)
+    if (ok) sout[e] = (V)sr;
+    const double p = ok ? pv : 0.0, q = ok ? sr : 0.0;
     dot2_acc(p, q, s0, c0);
     dot2_acc(p, rv, s1, c1);
   });
@@ -283,7 +298,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
     // lazy x update of the previous iteration, u += alpha_{i-1} p_{i-1}:
     // the same single rounding as in k_update's place, one sweep of u fewer.  alpha[b] still holds
     // alpha_{i-1}: this launch's last CTA overwrites it only after every CTA has passed here.
-    const double* pprev = sptr[mi - 1];   // newest window vector = p_{i-1}
+    const V* pprev = sptr[mi - 1];        // newest window vector = p_{i-1}
     double* ub = d.u + b * N;
     const double al = d.alpha[b];
     double uv[RG], pv[RG];
@@ -292,7 +307,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
       const int e = (g.i0 + w.r0 + s) * n + g.j0 + w.c;
       const bool ok = w.valid(g, s);
       uv[s] = ok ? ub[e] : 0.0;
-      pv[s] = ok ? __ldg(pprev + e) : 0.0;
+      pv[s] = ok ? (double)__ldg(pprev + e) : 0.0;
     }
 #pragma unroll
     for (int s = 0; s < RG; ++s)
@@ -327,7 +342,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
 
 cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s) {
   cudaError_t e;
-  ST_LAUNCH(e, d.n, k_pform_stencil, dim3((unsigned)st_tiles(d.n), (unsigned)d.B), s, d);
+  ST_LAUNCH_VEC(e, d, k_pform_stencil, dim3((unsigned)st_tiles(d.n), (unsigned)d.B), s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
@@ -339,7 +354,7 @@ cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s) {
 // convergence / breakdown bookkeeping (Algorithm 1's stopping test); the last system to arrive
 // publishes the number of systems still running and advances the iteration counter.  Systems
 // flagged this iteration skip the vector update but still take part in the arrival protocol.
-template <int EPT>
+template <int EPT, typename V>
 __global__ void __launch_bounds__(kThreads, 2) k_update(FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -352,21 +367,25 @@ __global__ void __launch_bounds__(kThreads, 2) k_update(FcgDev d) {
   double s = 0.0, c = 0.0;
   if (fl == 0) {
     const double alpha = d.alpha[b];
-    const double* sb = d.ring_s + ((size_t)slot * d.B + b) * N;
-    double* rb = d.r + (size_t)b * N;
+    const V* sb = reinterpret_cast<const V*>(d.ring_s) + ((size_t)slot * d.B + b) * N;
+    V* rb = reinterpret_cast<V*>(d.r) + (size_t)b * N;
+    double* r64 = d.r64 ? d.r64 + (size_t)b * N : nullptr;
     double rv[EPT], sv[EPT];
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {   // all loads first: EPT x 2 in flight
       const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
       const bool ok = e < N;
-      rv[q] = ok ? rb[e] : 0.0;
-      sv[q] = ok ? __ldg(sb + e) : 0.0;
+      rv[q] = ok ? (double)rb[e] : 0.0;
+      sv[q] = ok ? (double)__ldg(sb + e) : 0.0;
     }
 #pragma unroll
     for (int q = 0; q < EPT; ++q) {
       const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
-      rv[q] = __dsub_rn(rv[q], __dmul_rn(alpha, sv[q]));
-      if (e < N) rb[e] = rv[q];
+      rv[q] = rnd<V>(__dsub_rn(rv[q], __dmul_rn(alpha, sv[q])));   // stored value (R21)
+      if (e < N) {
+        rb[e] = (V)rv[q];
+        if (r64) r64[e] = rv[q];
+      }
     }
 #pragma unroll
     for (int q = 0; q < EPT; ++q) dot2_acc(rv[q], rv[q], s, c);
@@ -426,7 +445,7 @@ cudaError_t launch_loop_cond(const int* active, cudaGraphConditionalHandle h, cu
 
 // After the solve: the last lazy x update of every system that stopped in k_update (converged or
 // at maxit after >= 1 iteration), u += alpha_{iters-1} p_{iters-1}.
-template <int EPT>
+template <int EPT, typename V>
 __global__ void __launch_bounds__(kThreads) k_flush_x(FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -435,31 +454,35 @@ __global__ void __launch_bounds__(kThreads) k_flush_x(FcgDev d) {
   if (!((st == SYS_CONVERGED || st == SYS_MAXIT) && it >= 1)) return;
   const int N = d.N;
   const double al = d.alpha[b];
-  const double* pb = d.ring_p + ((size_t)ring_slot(it - 1, d.m) * d.B + b) * N;
+  const V* pb = reinterpret_cast<const V*>(d.ring_p) + ((size_t)ring_slot(it - 1, d.m) * d.B + b) * N;
   double* ub = d.u + (size_t)b * N;
 #pragma unroll
   for (int q = 0; q < EPT; ++q) {
     const int e = (blockIdx.x * EPT + q) * kThreads + threadIdx.x;
-    if (e < N) ub[e] = __dadd_rn(ub[e], __dmul_rn(al, pb[e]));
+    if (e < N) ub[e] = __dadd_rn(ub[e], __dmul_rn(al, (double)pb[e]));
   }
 }
 
 cudaError_t launch_flush_x(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e = launch_k(k_flush_x<kPerThread>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B),
-                           dim3(kThreads), 0, s, d);
+  const dim3 grid((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B);
+  cudaError_t e = d.vec32 ? launch_k(k_flush_x<kPerThread, float>, grid, dim3(kThreads), 0, s, d)
+                          : launch_k(k_flush_x<kPerThread, double>, grid, dim3(kThreads), 0, s, d);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
 }
 
-cudaError_t launch_update(const FcgDev& d, cudaStream_t s) {
-  cudaError_t e;
+template <typename V>
+static cudaError_t launch_update_t(const FcgDev& d, cudaStream_t s) {
   if (ew_wide(d.n, d.B))
-    e = launch_k(k_update<kEptUpdate>, dim3((unsigned)ew_blocks(d.n, kEptUpdate), (unsigned)d.B), dim3(kThreads), 0, s,
-                 d);
-  else
-    e = launch_k(k_update<kPerThread>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B), dim3(kThreads), 0,
-                 s, d);
+    return launch_k(k_update<kEptUpdate, V>, dim3((unsigned)ew_blocks(d.n, kEptUpdate), (unsigned)d.B), dim3(kThreads),
+                    0, s, d);
+  return launch_k(k_update<kPerThread, V>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B), dim3(kThreads),
+                  0, s, d);
+}
+
+cudaError_t launch_update(const FcgDev& d, cudaStream_t s) {
+  const cudaError_t e = d.vec32 ? launch_update_t<float>(d, s) : launch_update_t<double>(d, s);
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();

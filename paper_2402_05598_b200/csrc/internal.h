@@ -17,6 +17,9 @@ struct FcgDev {
   double tol, scale;          // scale = (n+1)^2
   const double* k;            // [B][N]
   int kfast;                  // problem's k all in [2^-400, 2^400] (branch-free face division)
+  int vec32;                  // r, w, ring_p, ring_s stored as float (opts.vec_fp32, reading R21);
+                              // the double* fields below then point at float arrays
+  double* r64;                // vec32 with a NO: fp64 copy of r (the NO's input), else nullptr
   const double* f;            // [B][N]
   double* u;                  // [B][N]  caller's iterate
   double* r;                  // [B][N]  residual

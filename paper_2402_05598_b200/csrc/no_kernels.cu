@@ -584,13 +584,21 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
         z += Gr[k2].x * f.x + Gr[k2].y * f.y;
       }
       wv[q] = s * (double)z;
-      a.wout[(size_t)b * N + e] = wv[q];
+      if (d.vec32) {   // w stored in fp32 (R21): the window dots see the stored value
+        wv[q] = (double)(float)wv[q];
+        reinterpret_cast<float*>(a.wout)[(size_t)b * N + e] = (float)wv[q];
+      } else {
+        a.wout[(size_t)b * N + e] = wv[q];
+      }
     }
   }
   if (a.use_dots) {
     const int i = *d.iter;
     const int mi = m_schedule(i, d.m, d.schedule);
-    if (mi > 0) window_dots_beta(d, b, blk, i, mi, wv);
+    if (mi > 0) {
+      if (d.vec32) window_dots_beta<kPerThread, float>(d, b, blk, i, mi, wv);
+      else window_dots_beta<kPerThread, double>(d, b, blk, i, mi, wv);
+    }
   }
 }
 
@@ -615,7 +623,10 @@ __global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float
   const int it = a.use_dots ? *d.iter : 0;
   const int mi = a.use_dots ? m_schedule(it, d.m, d.schedule) : 0;
   double rv[kWinPre][kPerThread];
-  if (mi > 0) window_prefetch(d, b, blk, it, mi, rv);
+  if (mi > 0) {
+    if (d.vec32) window_prefetch<float>(d, b, blk, it, mi, rv);
+    else window_prefetch<double>(d, b, blk, it, mi, rv);
+  }
   for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)t * a.B + b];   // mode-major
   for (int t = threadIdx.x; t < kModes * n; t += blockDim.x) {
     const int j = t / kModes, k = t - j * kModes;
@@ -654,10 +665,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float
         z += Gr[k2].x * f.x + Gr[k2].y * f.y;
       }
       wv[q] = s * (double)z;
-      a.wout[(size_t)b * N + e] = wv[q];
+      if (d.vec32) {   // w stored in fp32 (R21): the window dots see the stored value
+        wv[q] = (double)(float)wv[q];
+        reinterpret_cast<float*>(a.wout)[(size_t)b * N + e] = (float)wv[q];
+      } else {
+        a.wout[(size_t)b * N + e] = wv[q];
+      }
     }
   }
-  if (mi > 0) window_dots_beta<true>(d, b, blk, it, mi, wv, rv);
+  if (mi > 0) {
+    if (d.vec32) window_dots_beta<true, kPerThread, float>(d, b, blk, it, mi, wv, rv);
+    else window_dots_beta<true, kPerThread, double>(d, b, blk, it, mi, wv, rv);
+  }
 }
 
 // ------------------------------------------------------------------ launcher

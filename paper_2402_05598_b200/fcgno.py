@@ -45,7 +45,7 @@ class NoDesc(ctypes.Structure):
 class SolveOpts(ctypes.Structure):
     _fields_ = [("m", ctypes.c_int32), ("maxit", ctypes.c_int32), ("tol", ctypes.c_double),
                 ("schedule", ctypes.c_int32), ("check_every", ctypes.c_int32),
-                ("profile_mask", ctypes.c_int32)]
+                ("profile_mask", ctypes.c_int32), ("vec_fp32", ctypes.c_int32)]
 
 
 _vp, _sz, _i = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
@@ -220,9 +220,10 @@ class Solver:
 
     def __init__(self, problem: Problem, m: int, tol: float, maxit: int, no: NeuralOperator | None = None,
                  schedule: int = SCHEDULE_PAPER, check_every: int = 16, history: bool = True,
-                 profile_mask: int = 0):
+                 profile_mask: int = 0, vec_fp32: bool = False):
         self.problem, self.no = problem, no
-        self.opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), int(profile_mask))
+        self.opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), int(profile_mask),
+                              int(bool(vec_fp32)))
         self._desc = ctypes.byref(no.desc) if no is not None else None
         nbytes = _lib.fcgno_solve_workspace_bytes(problem.grid, self._desc, self.opts)
         if nbytes == 0:
@@ -247,9 +248,9 @@ class Solver:
 
 def fcg_solve(problem: Problem, f: torch.Tensor, u0: torch.Tensor | None = None, *, m: int, tol: float, maxit: int,
               no: NeuralOperator | None = None, schedule: int = SCHEDULE_PAPER, history: bool = True,
-              check_every: int = 16) -> SolveResult:
+              check_every: int = 16, vec_fp32: bool = False) -> SolveResult:
     u = torch.zeros_like(f) if u0 is None else u0.clone()
-    return Solver(problem, m, tol, maxit, no, schedule, check_every, history).solve(f, u)
+    return Solver(problem, m, tol, maxit, no, schedule, check_every, history, vec_fp32=vec_fp32).solve(f, u)
 
 
 class HostSolver:
@@ -257,10 +258,10 @@ class HostSolver:
     and D2H copies inside one call."""
 
     def __init__(self, n: int, batch: int, m: int, tol: float, maxit: int, no: NeuralOperator | None = None,
-                 schedule: int = SCHEDULE_PAPER, check_every: int = 16, device="cuda"):
+                 schedule: int = SCHEDULE_PAPER, check_every: int = 16, device="cuda", vec_fp32: bool = False):
         self.grid = Grid(int(n), int(batch))
         self.no = no
-        self.opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), 0)
+        self.opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), 0, int(bool(vec_fp32)))
         self._desc = ctypes.byref(no.desc) if no is not None else None
         self.ws = _workspace(_lib.fcgno_solve_host_workspace_bytes(self.grid, self._desc, self.opts), device)
         self.n, self.B = int(n), int(batch)

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(built):
 def test_binding_covers_every_declared_symbol(built):
     from paper_2402_05598_b200 import fcgno
     assert set(declared_functions()) <= set(fcgno.EXPORTS)
-    assert fcgno.abi_version() == 3
+    assert fcgno.abi_version() == 4
 
 
 def test_sizes_and_validation(built):
@@ -60,6 +60,10 @@ def test_sizes_and_validation(built):
                 F.SolveOpts(5, -1, 1e-6, 0, 16, 0), F.SolveOpts(5, 10, 1e-6, 7, 16, 0)):
         assert F._lib.fcgno_solve_workspace_bytes(g, None, bad) == 0
     # solve workspace grows with m (ring of m+1 (p, s) pairs)
+    v32 = F._lib.fcgno_solve_workspace_bytes(g, None, F.SolveOpts(5, 10, 1e-6, 0, 16, 0, 1))
+    v64 = F._lib.fcgno_solve_workspace_bytes(g, None, F.SolveOpts(5, 10, 1e-6, 0, 16, 0, 0))
+    assert 0 < v32 < v64                                  # fp32 vectors and ring (R21)
+    assert F._lib.fcgno_solve_workspace_bytes(g, None, F.SolveOpts(5, 10, 1e-6, 0, 16, 0, 2)) == 0
     a = F._lib.fcgno_solve_workspace_bytes(g, None, F.SolveOpts(5, 10, 1e-6, 0, 16, 0))
     b = F._lib.fcgno_solve_workspace_bytes(g, None, F.SolveOpts(10, 10, 1e-6, 0, 16, 0))
     assert b - a >= 2 * 5 * 4 * 64 * 64 * 8

@@ -230,12 +230,13 @@ def _oracle_fcg(k, f, m, tol, maxit, precond=None, schedule="paper"):
                    schedule=schedule)
 
 
-def _check_identity(lib, k, f, m, tol, maxit, systems, schedule=0):
+def _check_identity(lib, k, f, m, tol, maxit, systems, schedule=0, vec32=False):
     prob = lib.Problem(dev(k))
-    res = lib.fcg_solve(prob, dev(f), m=m, tol=tol, maxit=maxit, schedule=schedule)
+    res = lib.fcg_solve(prob, dev(f), m=m, tol=tol, maxit=maxit, schedule=schedule, vec_fp32=vec32)
     iters, status, hist, u = host(res.iters), host(res.status), host(res.history), host(res.u)
     for b in systems:
-        ref = _oracle_fcg(k[b], f[b], m, tol, maxit, schedule="sliding" if schedule else "paper")
+        ref = orc.fcg(lambda x: orc.apply_A(k[b], x), f[b], np.zeros_like(f[b]), m, tol, maxit,
+                      schedule="sliding" if schedule else "paper", vec32=vec32)
         it = ref["iters"]
         assert iters[b] == it and status[b] == ref["status"]
         assert np.array_equal(hist[b, :it + 1], ref["hist"]), "identity histories must agree bit for bit"
@@ -269,6 +270,44 @@ def test_identity_prefix_wide_tiles(lib, n, B, m, maxit, systems):
     k = sy.lognormal_k(n, B, 0.1, 1.0, 63)
     f = sy.normal_field(n, B, 64)
     _check_identity(lib, k, f, m, 1e-14, maxit, systems)
+
+
+# ----------------------------------------------------------------------------- fp32 vectors (R21)
+@pytest.mark.parametrize("cfg_id,systems,maxit", [(1, [0], None), (2, [0, 63], 5000)])
+def test_identity_vec32_configs_bitwise(lib, cfg_id, systems, maxit):
+    # opts.vec_fp32: r, w, p, s stored in fp32, every vector operation in fp64 rounded once on
+    # store; histories, iterates and counts bit-identical to the oracle's fp32-storage variant.
+    cfg = sy.CONFIGS[cfg_id]
+    k, f = sy.make_k(cfg), sy.make_f(cfg)
+    _check_identity(lib, k, f, cfg["m"], cfg["tol"], maxit or cfg["maxit"], systems, vec32=True)
+
+
+@pytest.mark.parametrize("n,B,m,maxit,systems", [(45, 2, 10, 3000, [0, 1]), (512, 8, 10, 24, [0, 7])])
+def test_identity_vec32_ragged_and_wide(lib, n, B, m, maxit, systems):
+    # odd n (single-cell tile fills) and the wide element-wise kernels with fp32 column pairs
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 65)
+    f = sy.normal_field(n, B, 66)
+    _check_identity(lib, k, f, m, 1e-6 if n < 100 else 1e-14, maxit, systems, vec32=True)
+
+
+def test_fcg_no_fp32_vec32_config3_first_step(lib):
+    # BASELINE configs[2]: fp32 NO with fp32 FCG vectors.  As for the fp64-vector variant, the
+    # fp32 NO is compared over one NO application + one FCG update from identical state.
+    cfg = sy.CONFIGS[3]
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    w = cfg["width"]
+    params = orc.unpack_weights(blob, w)
+    maxit = 6
+    prob = lib.Problem(dev(k))
+    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit,
+                        no=lib.NeuralOperator(w, blob, precision=lib.FP32), vec_fp32=True)
+    assert np.all(host(res.status) == lib.MAXIT)
+    for b in (0, cfg["batch"] - 1):
+        ref = orc.fcg(lambda x: orc.apply_A(k[b], x), f[b], np.zeros_like(f[b]), cfg["m"], cfg["tol"], maxit,
+                      precond=lambda r: orc.no_forward(params, r, k[b]), vec32=True)
+        h = host(res.history)[b]
+        assert abs(h[1] - ref["hist"][1]) / ref["hist"][1] <= 1e-4
+        assert np.all(np.isfinite(h[:maxit + 1]))
 
 
 @pytest.mark.parametrize("n", [4, 8])
