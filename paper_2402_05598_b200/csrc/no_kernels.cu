@@ -519,7 +519,8 @@ struct OutArgs {
 };
 
 
-template <typename T>
+// V: storage type of the FCG vectors (w written, ring read; R21), fixed per launch.
+template <typename T, typename V>
 __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -583,28 +584,21 @@ __global__ void __launch_bounds__(kThreads) k_no_out(const OutArgs<T> a, const F
         const T2 f = __ldg(a.F + (size_t)j * kModes + k2);
         z += Gr[k2].x * f.x + Gr[k2].y * f.y;
       }
-      wv[q] = s * (double)z;
-      if (d.vec32) {   // w stored in fp32 (R21): the window dots see the stored value
-        wv[q] = (double)(float)wv[q];
-        reinterpret_cast<float*>(a.wout)[(size_t)b * N + e] = (float)wv[q];
-      } else {
-        a.wout[(size_t)b * N + e] = wv[q];
-      }
+      wv[q] = rnd<V>(s * (double)z);   // w as stored (R21): the window dots see the stored value
+      reinterpret_cast<V*>(a.wout)[(size_t)b * N + e] = (V)wv[q];
     }
   }
   if (a.use_dots) {
     const int i = *d.iter;
     const int mi = m_schedule(i, d.m, d.schedule);
-    if (mi > 0) {
-      if (d.vec32) window_dots_beta<kPerThread, float>(d, b, blk, i, mi, wv);
-      else window_dots_beta<kPerThread, double>(d, b, blk, i, mi, wv);
-    }
+    if (mi > 0) window_dots_beta<kPerThread, V>(d, b, blk, i, mi, wv);
   }
 }
 
 // Tensor-core path variant: the layer-4 bypass sum_o (D W4)[o] v3[o] arrives as one fp32 field
 // reduced by layer 3's epilogue; this kernel adds cst + the 1-channel synthesis, scales by ||r||
 // and computes the FCG window dots.
+template <typename V>
 __global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float> a, const FcgDev d) {
   pdl_wait();
   pdl_trigger();
@@ -623,10 +617,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float
   const int it = a.use_dots ? *d.iter : 0;
   const int mi = a.use_dots ? m_schedule(it, d.m, d.schedule) : 0;
   double rv[kWinPre][kPerThread];
-  if (mi > 0) {
-    if (d.vec32) window_prefetch<float>(d, b, blk, it, mi, rv);
-    else window_prefetch<double>(d, b, blk, it, mi, rv);
-  }
+  if (mi > 0) window_prefetch<V>(d, b, blk, it, mi, rv);
   for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)t * a.B + b];   // mode-major
   for (int t = threadIdx.x; t < kModes * n; t += blockDim.x) {
     const int j = t / kModes, k = t - j * kModes;
@@ -664,19 +655,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float
         const float2 f = Fs[k2 * n + j];
         z += Gr[k2].x * f.x + Gr[k2].y * f.y;
       }
-      wv[q] = s * (double)z;
-      if (d.vec32) {   // w stored in fp32 (R21): the window dots see the stored value
-        wv[q] = (double)(float)wv[q];
-        reinterpret_cast<float*>(a.wout)[(size_t)b * N + e] = (float)wv[q];
-      } else {
-        a.wout[(size_t)b * N + e] = wv[q];
-      }
+      wv[q] = rnd<V>(s * (double)z);   // w as stored (R21): the window dots see the stored value
+      reinterpret_cast<V*>(a.wout)[(size_t)b * N + e] = (V)wv[q];
     }
   }
-  if (mi > 0) {
-    if (d.vec32) window_dots_beta<true, kPerThread, float>(d, b, blk, it, mi, wv, rv);
-    else window_dots_beta<true, kPerThread, double>(d, b, blk, it, mi, wv, rv);
-  }
+  if (mi > 0) window_dots_beta<true, kPerThread, V>(d, b, blk, it, mi, wv, rv);
 }
 
 // ------------------------------------------------------------------ launcher
@@ -708,8 +691,10 @@ cudaError_t prepare_no_kernels() {
   if ((e = set_smem((const void*)k_no_layer<T, true, GO>)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_no_layer<T, false, GO>)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_mix<T>)) != cudaSuccess) return e;
-  if ((e = set_smem((const void*)k_no_out<T>)) != cudaSuccess) return e;
-  if ((e = set_smem((const void*)k_no_out_blob)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_no_out<T, double>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_no_out<T, float>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_no_out_blob<double>)) != cudaSuccess) return e;
+  if ((e = set_smem((const void*)k_no_out_blob<float>)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_dft_rows<T, true>)) != cudaSuccess) return e;
   if ((e = set_smem((const void*)k_dft_rows<T, false>)) != cudaSuccess) return e;
   done = true;
@@ -878,17 +863,21 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   const int nr_max = kTile / n + 2;
   const size_t osmem = (size_t)(kModes2 + (size_t)nr_max * kModes) * sizeof(T2) + (size_t)((w + 3) & ~3) * sizeof(T);
   FcgDev dummy{};
+  const bool v32 = fcg && fcg->vec32;
   pb(PROF_NO_OUT);
   if constexpr (sizeof(T) == sizeof(float)) {
     if (tc_path) {
       oa.p3 = no.p3;
       const size_t bsmem = (size_t)(kModes2 + (size_t)nr_max * kModes + (size_t)kModes * n) * sizeof(float2) + kTile * sizeof(float);
-      launch_k(k_no_out_blob, dim3(nblk, B), dim3(kThreads), bsmem, s, oa, fcg ? *fcg : dummy);
+      if (v32) launch_k(k_no_out_blob<float>, dim3(nblk, B), dim3(kThreads), bsmem, s, oa, *fcg);
+      else launch_k(k_no_out_blob<double>, dim3(nblk, B), dim3(kThreads), bsmem, s, oa, fcg ? *fcg : dummy);
     } else {
-      launch_k(k_no_out<T>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);
+      if (v32) launch_k(k_no_out<T, float>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, *fcg);
+      else launch_k(k_no_out<T, double>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);
     }
   } else {
-    launch_k(k_no_out<T>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);
+    if (v32) launch_k(k_no_out<T, float>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, *fcg);
+    else launch_k(k_no_out<T, double>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, fcg ? *fcg : dummy);
   }
   pe(PROF_NO_OUT);
   ++launches;
