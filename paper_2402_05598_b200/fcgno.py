@@ -275,3 +275,22 @@ class HostSolver:
         _check(_lib.fcgno_solve_host(self.grid, _ptr(k), _ptr(f), _ptr(u), self._desc,
                                      _ptr(self.no.packed) if self.no else None, self.opts, _ptr(iters),
                                      _ptr(status), None, _ptr(self.ws), self.ws.numel(), _stream(stream)))
+
+
+def notay_ratio(problem: Problem, r: torch.Tensor, e: torch.Tensor, no: NeuralOperator | None = None,
+                stream=None, optimal_scale: bool = False) -> torch.Tensor:
+    """Theorem-1 / Notay diagnostic (PAPER.md Eq. final_loss):
+    eps_b = ||B(r_b) - e_b||_A / ||e_b||_A with e = A^{-1} r supplied by the caller.
+
+    Composed from the library's entry points: w = apply_NO(r) (identity: w = r), A w and A e
+    (apply_A), and the correctly rounded dots (w, Aw), (w, Ae), (e, Ae) (batched_dot), so that
+    ||w - e||_A^2 = (w, Aw) - 2 (w, Ae) + (e, Ae); only that scalar combination of B numbers is done
+    here.  optimal_scale: min over c of ||c B(r) - e||_A / ||e||_A = sqrt(1 - (w,Ae)^2 / ((w,Aw)(e,Ae))),
+    the scale-free form (FCG's iterates do not depend on the scale of B)."""
+    w = no.apply(problem, r, stream) if no is not None else r
+    Aw = problem.apply_A(w, stream=stream)
+    Ae = problem.apply_A(e, stream=stream)
+    ww, we, ee = problem.dot(w, Aw, stream), problem.dot(w, Ae, stream), problem.dot(e, Ae, stream)
+    if optimal_scale:
+        return torch.sqrt(torch.clamp(1.0 - we * we / (ww * ee), min=0.0))
+    return torch.sqrt(torch.clamp(ww - 2.0 * we + ee, min=0.0) / ee)

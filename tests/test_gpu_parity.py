@@ -527,3 +527,29 @@ def test_opt_in_paths_match_default(lib):
     assert np.isfinite(u0).all() and h0.shape == h1.shape == h2.shape
     assert np.array_equal(u0, u1) and np.array_equal(h0, h1, equal_nan=True)
     assert np.array_equal(u0, u2) and np.array_equal(h0, h2, equal_nan=True)
+
+
+# ----------------------------------------------------------------------------- Notay ratio (NEXT-2)
+@pytest.mark.parametrize("kind", ["identity", "no64", "no32"])
+def test_notay_ratio_matches_oracle(lib, kind):
+    # eps = ||B(r) - A^{-1} r||_A / ||A^{-1} r||_A (Eq. final_loss) through the library's kernels vs
+    # the oracle's direct definition, e = A^{-1} r from a dense library solve on both sides.
+    n, B, w = 32, 2, 8
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 95)
+    r = sy.normal_field(n, B, 96)
+    e = np.stack([np.linalg.solve(orc.dense_A(k[b]), r[b].ravel()).reshape(n, n) for b in range(B)])
+    blob = sy.structured_no_weights(w, n) if kind != "identity" else None
+    no = None
+    if kind != "identity":
+        no = lib.NeuralOperator(w, blob, precision=lib.FP64 if kind == "no64" else lib.FP32)
+    prob = lib.Problem(dev(k))
+    eps = host(lib.notay_ratio(prob, dev(r), dev(e), no))
+    eps_s = host(lib.notay_ratio(prob, dev(r), dev(e), no, optimal_scale=True))
+    params = orc.unpack_weights(blob, w) if blob is not None else None
+    for b in range(B):
+        wb = r[b] if params is None else orc.no_forward(params, r[b], k[b])
+        ref = orc.notay_ratio(lambda x: orc.apply_A(k[b], x), wb, e[b])
+        tol = {"identity": 1e-11, "no64": 1e-9, "no32": 1e-3}[kind]
+        assert abs(eps[b] - ref) <= tol * ref, (eps[b], ref)
+        ref_s = orc.notay_ratio_scaled(lambda x: orc.apply_A(k[b], x), wb, e[b])
+        assert abs(eps_s[b] - ref_s) <= max(tol, 1e-9) * ref_s, (eps_s[b], ref_s)
