@@ -125,7 +125,8 @@ class ClockSampler:
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index: int):
-        self.path = tempfile.mktemp(suffix=".csv")
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
         self.proc = None
         self.gpu = gpu_index
 
@@ -397,6 +398,9 @@ def run_ours(args):
         it_host = solver.iters.cpu().numpy()
         st_host = solver.status.cpu().numpy()
         out["solves_per_s"] = B * world / (max_ms / args.steps / 1e3)
+        # SURVEY D.1 "swept" variant: N * B * max_b(iters_b) / T, the work the kernels touch were
+        # converged systems not skipped
+        out["swept_unknown_iterations_per_s"] = N * B * world * float(it_host.max()) / (max_ms / args.steps / 1e3)
         out["iterations"] = {"mean": float(it_host.mean()), "min": int(it_host.min()), "max": int(it_host.max()),
                              "converged": int((st_host == F.CONVERGED).sum()), "of": int(B)}
 
