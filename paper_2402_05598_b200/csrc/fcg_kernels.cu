@@ -234,11 +234,44 @@ __global__ void __launch_bounds__(kThreads, 2) k_window_dots(FcgDev d) {
   window_dots_pairs<EPT, V>(d, b, blockIdx.x, i, mi, wv);
 }
 
+// Wide batches: 32 elements per thread, w kept in (dynamic) shared memory by its own thread.
+constexpr int kEptWin = 32;
+template <typename V>
+__global__ void __launch_bounds__(kThreads, 2) k_window_dots_smem(FcgDev d) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ __align__(16) double wsm[];   // [kEptWin][kThreads]
+  const int b = blockIdx.y;
+  if (d.status[b] != SYS_RUNNING) return;
+  const int i = *d.iter;
+  const int mi = m_schedule(i, d.m, d.schedule);
+  if (mi == 0) return;
+  const V* wb = reinterpret_cast<const V*>(d.w) + (size_t)b * d.N;
+#pragma unroll 8
+  for (int q = 0; q < kEptWin; ++q) {
+    const int e = (blockIdx.x * kEptWin + q) * kThreads + threadIdx.x;
+    wsm[q * kThreads + threadIdx.x] = e < d.N ? (double)__ldg(wb + e) : 0.0;
+  }
+  window_dots_pairs_smem<kEptWin, V>(d, b, blockIdx.x, i, mi, wsm);
+}
+
 template <typename V>
 static cudaError_t launch_window_dots_t(const FcgDev& d, cudaStream_t s) {
-  if (ew_wide(d.n, d.B))
-    return launch_k(k_window_dots<kEptWide, V>, dim3((unsigned)ew_blocks(d.n, kEptWide), (unsigned)d.B), dim3(kThreads),
-                    0, s, d);
+  if (ew_wide(d.n, d.B)) {
+    static bool attr = false;
+    const int smem = kEptWin * kThreads * (int)sizeof(double);
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute((const void*)k_window_dots_smem<float>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute((const void*)k_window_dots_smem<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 smem);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    return launch_k(k_window_dots_smem<V>, dim3((unsigned)ew_blocks(d.n, kEptWin), (unsigned)d.B), dim3(kThreads),
+                    (size_t)smem, s, d);
+  }
   return launch_k(k_window_dots<kPerThread, V>, dim3((unsigned)ew_blocks(d.n, kPerThread), (unsigned)d.B),
                   dim3(kThreads), 0, s, d);
 }
