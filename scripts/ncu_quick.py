@@ -10,8 +10,10 @@ M = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
      "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
      "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum",
      "launch__registers_per_thread", "launch__occupancy_limit_registers", "launch__occupancy_limit_shared_mem",
-     "l1tex__throughput.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active"]
-SHORT = ["us", "dramR", "dramW", "dram%", "sm%", "warps%", "inst", "fp64%", "L2B", "regs", "occR", "occS", "l1%", "issue%"]
+     "l1tex__throughput.avg.pct_of_peak_sustained_active", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+     "lts__t_sector_hit_rate.pct", "dram__throughput.avg.pct_of_peak_sustained_elapsed"]
+SHORT = ["us", "dramR", "dramW", "dram%", "sm%", "warps%", "inst", "fp64%", "L2B", "regs", "occR", "occS", "l1%", "issue%",
+         "L2hit%", "dramBW%"]
 out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv", "--metrics", ",".join(M)],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
