@@ -5,8 +5,9 @@
 //    all but astronomically rare ties (reading R6);
 //  * deterministic block reductions and the "last CTA of a system reduces the partials"
 //    protocol, so no scalar-only kernel launch is needed per reduction;
-//  * the canonical fp64 stencil op order (R1-R5) written with explicit _rn
-//    intrinsics so that nvcc cannot contract it into fma.
+//  * the harmonic face mean of the stencil (R1); the stencil itself (canonical op
+//    order R5, explicit _rn intrinsics so nvcc cannot contract it into fma) is st_walk in
+//    fcg_device.cuh.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -163,27 +164,6 @@ __device__ __forceinline__ int m_schedule(int i, int m, int schedule) {
 // ------------------------------------------------------------------ stencil (fp64, canonical order)
 __device__ __forceinline__ double harmonic(double a, double b) {
   return __ddiv_rn(2.0 * __dmul_rn(a, b), __dadd_rn(a, b));
-}
-
-// y(i,j) of one system; k points at the system's [n][n] array, x holds the system's field from
-// element xoff on (x[e - xoff]; xoff = 0 for the whole field, > 0 for a shared-memory halo tile).
-__device__ __forceinline__ double stencil_at(const double* __restrict__ k, const double* __restrict__ x,
-                                             int n, int i, int j, double scale, int xoff = 0) {
-  const int e = i * n + j, ex = e - xoff;
-  const double kc = __ldg(k + e);
-  const double xc = x[ex];
-  double kW = kc, kE = kc, kS = kc, kN = kc, xW = 0.0, xE = 0.0, xS = 0.0, xN = 0.0;
-  if (j > 0)     { kW = harmonic(kc, __ldg(k + e - 1)); xW = x[ex - 1]; }
-  if (j < n - 1) { kE = harmonic(kc, __ldg(k + e + 1)); xE = x[ex + 1]; }
-  if (i > 0)     { kS = harmonic(kc, __ldg(k + e - n)); xS = x[ex - n]; }
-  if (i < n - 1) { kN = harmonic(kc, __ldg(k + e + n)); xN = x[ex + n]; }
-  const double d = __dadd_rn(__dadd_rn(kW, kE), __dadd_rn(kS, kN));
-  double t = __dmul_rn(d, xc);
-  t = __dsub_rn(t, __dmul_rn(kW, xW));
-  t = __dsub_rn(t, __dmul_rn(kE, xE));
-  t = __dsub_rn(t, __dmul_rn(kS, xS));
-  t = __dsub_rn(t, __dmul_rn(kN, xN));
-  return __dmul_rn(t, scale);
 }
 
 }  // namespace fcgno
