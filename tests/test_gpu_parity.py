@@ -553,3 +553,48 @@ def test_notay_ratio_matches_oracle(lib, kind):
         assert abs(eps[b] - ref) <= tol * ref, (eps[b], ref)
         ref_s = orc.notay_ratio_scaled(lambda x: orc.apply_A(k[b], x), wb, e[b])
         assert abs(eps_s[b] - ref_s) <= max(tol, 1e-9) * ref_s, (eps_s[b], ref_s)
+
+
+# ----------------------------------------------------------------------------- device-side loop, graph cache
+def test_device_loop_edge_cases(lib):
+    # the solve's loop is a CUDA-graph WHILE node replaying 16-iteration bodies: maxit not a
+    # multiple of the body, every system converged at r0 = 0, maxit = 1, check_every = 1, and a
+    # run that stops mid-body; iterates equal the oracle's bit for bit (identity preconditioner)
+    n, B = 24, 3
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 97)
+    f = sy.normal_field(n, B, 98)
+    prob = lib.Problem(dev(k))
+    for maxit, ce in ((17, 16), (1, 16), (33, 1), (40, 7)):
+        res = lib.fcg_solve(prob, dev(f), m=5, tol=1e-30, maxit=maxit, check_every=ce)
+        assert list(host(res.iters)) == [maxit] * B and np.all(host(res.status) == lib.MAXIT)
+        for b in (0, B - 1):
+            ref = _oracle_fcg(k[b], f[b], 5, 1e-30, maxit)
+            assert np.array_equal(host(res.u)[b], ref["u"]) and np.array_equal(host(res.history)[b], ref["hist"])
+    zero = lib.fcg_solve(prob, dev(np.zeros_like(f)), m=5, tol=1e-8, maxit=50)
+    assert np.all(host(zero.iters) == 0) and np.all(host(zero.status) == lib.CONVERGED)
+    assert np.all(host(zero.u) == 0.0)
+    # converging mid-body: counts and iterates bitwise
+    res = lib.fcg_solve(prob, dev(f), m=5, tol=1e-6, maxit=3000)
+    for b in range(B):
+        ref = _oracle_fcg(k[b], f[b], 5, 1e-6, 3000)
+        assert host(res.iters)[b] == ref["iters"] and np.array_equal(host(res.u)[b], ref["u"])
+
+
+def test_graph_cache_reuse_with_other_buffers(lib):
+    # instantiated loop graphs are reused only for identical captured arguments: alternating
+    # right-hand sides / iterate buffers and a second problem must each give their own answer
+    n, B = 20, 2
+    k1 = sy.lognormal_k(n, B, 0.1, 1.0, 101)
+    k2 = sy.rectangles_k(n, B, seed=102)
+    fa, fb = sy.normal_field(n, B, 103), sy.normal_field(n, B, 104)
+    p1, p2 = lib.Problem(dev(k1)), lib.Problem(dev(k2))
+    s1 = lib.Solver(p1, 5, 1e-8, 3000)
+    s2 = lib.Solver(p2, 5, 1e-8, 3000)
+    dfa, dfb = dev(fa), dev(fb)
+    for _ in range(2):
+        for s, k, f, df in ((s1, k1, fa, dfa), (s1, k1, fb, dfb), (s2, k2, fa, dfa)):
+            u = torch.zeros_like(df)
+            s.solve(df, u)
+            for b in range(B):
+                ref = _oracle_fcg(k[b], f[b], 5, 1e-8, 3000)
+                assert host(s.iters)[b] == ref["iters"] and np.array_equal(host(u)[b], ref["u"])
