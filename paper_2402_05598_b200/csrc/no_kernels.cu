@@ -718,13 +718,19 @@ template size_t no_max_smem<double>(int, int);
 
 // Row split of the FFMA layer kernel: parts per system such that (CTAs x parts) fills the SMs
 // once at the kernel's occupancy, at most kRowSplitMax and one row chunk per part.
-static int layer_row_split(const void* fn, size_t smem, int ctas, int row_chunks) {
+static int sm_count() {
   static int sms = 0;
   if (!sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
   }
+  return sms;
+}
+
+static int layer_row_split(const void* fn, size_t smem, int ctas, int row_chunks) {
+  const int sms = sm_count();
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem) != cudaSuccess || per_sm < 1) {
     (void)cudaGetLastError();
@@ -808,6 +814,11 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
       LayerArgs<T> la{};
       int rows, nbuf, fs;
       layer_config<T>(n, l == 0 ? 2 : w, l == 0, lim, &rows, &nbuf, &fs);
+      // tiny batches (config 1: one system): shorter row chunks, so that the row split below can
+      // spread a system over up to kRowSplitMax CTAs
+      while (rows > 1 && (int)(lgrid.x * lgrid.y) * ((n + rows - 1) / rows) < kRowSplitMax * (int)(lgrid.x * lgrid.y) &&
+             (int)(lgrid.x * lgrid.y) * kRowSplitMax <= 2 * sm_count())
+        rows /= 2;
       la.n = n; la.N = N; la.w = w; la.B = B; la.rows = rows; la.nbuf = nbuf; la.use_gelu = no.use_gelu; la.fsm = fs;
       la.r = r; la.rr = rr; la.k = no.k;
       la.ghat = ghat; la.F = F; la.chat = chat; la.status = status;
