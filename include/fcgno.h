@@ -90,9 +90,12 @@ typedef struct {
   double tol;           /* stop at the first i with ||r_i||/||r_0|| <= tol */
   int32_t schedule;     /* FCGNO_SCHEDULE_PAPER: m_i = min(i, max(1, i mod (m+1)));
                            FCGNO_SCHEDULE_SLIDING: m_i = min(i, m) */
-  int32_t check_every;  /* iterations per convergence poll and per CUDA-graph replay (0 = default
-                           16); work on converged systems stops immediately regardless, this only
-                           bounds idle tail launches */
+  int32_t check_every;  /* iterations per replay of the captured loop body (0 = default 16): the
+                           solve is one CUDA graph whose WHILE node replays the body while a system
+                           is running (a condition kernel ends every body); work on converged
+                           systems stops immediately regardless, this only bounds idle tail
+                           launches.  With profiling or batch lanes the body is replayed from a
+                           host loop that polls the running count per replay instead. */
   int32_t profile_mask; /* bit c set: time the launches of kernel class c (fcgno_prof_class) in the
                            first unrolled iteration of every graph chunk (one sampled iteration
                            per check_every) with CUDA events recorded inside the solve's graphs;
@@ -173,8 +176,10 @@ FCGNO_API int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void
  *   history  [B][maxit+1] fp64 device or NULL: history[b][i] = ||r_i||/||r_0|| for
  *            i <= iters[b] (entries beyond are left untouched).
  *   ws       fcgno_solve_workspace_bytes(g, d_or_null, o) bytes.
- * Converged systems are frozen (no further writes).  Polls an on-device "any system running"
- * counter every check_every iterations and therefore synchronises `stream` before returning. */
+ * Converged systems are frozen (no further writes).  The iteration loop runs on the device (a
+ * CUDA-graph WHILE node on an on-device "systems running" counter); instantiated graphs are reused
+ * by later solves with identical arguments.  Synchronises `stream` before returning (iteration
+ * count, final lazy x update). */
 FCGNO_API size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* d_or_null, fcgno_solve_opts o);
 FCGNO_API int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* d_or_null, const void* packed,
                     const double* f, double* u, fcgno_solve_opts o, int32_t* iters,
