@@ -46,6 +46,7 @@ def parse_args(argv=None):
                     help="BASELINE configs[4] second half: isolated HBM bandwidth sweep of apply_A, the batched "
                          "dot and the FCG kernels at 1024^2 and 2048^2, batch 4 (one JSON line)")
     ap.add_argument("--sweep-n", type=int, nargs="*", default=[1024, 2048])
+    ap.add_argument("--check-every", type=int, default=16, help="iterations per captured loop body")
     ap.add_argument("--vec32", action="store_true",
                     help="FCG vectors and ring stored in fp32 (BASELINE configs[2] variant, DESIGN.md R21)")
     ap.add_argument("--precond", choices=["no", "identity", "structured"], default="no",
@@ -243,7 +244,8 @@ def run_ours(args):
     prob = F.Problem(dk)
     no = None if args.precond == "identity" else \
         F.NeuralOperator(w, blob, precision=F.FP32 if cfg["no_precision"] == "fp32" else F.FP64)
-    solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False, vec_fp32=args.vec32)
+    solver = F.Solver(prob, m, cfg["tol"], cfg["maxit"], no=no, history=False, vec_fp32=args.vec32,
+                      check_every=args.check_every)
     u = torch.zeros_like(df)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     # clock sampler first: nvidia-smi's start-up stalls the GPU briefly, so it must land in the
