@@ -27,7 +27,6 @@ template <> struct Cplx<double> { using type = double2; };
 __device__ __forceinline__ float gelu_t(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 __device__ __forceinline__ double gelu_t(double x) { return 0.5 * x * (1.0 + erf(x * 0.70710678118654752440)); }
 
-constexpr int kDftRows = 8;      // rows per CTA of k_dft_rows
 constexpr int kGhStride = kModes2 + 1;  // padded row of the per-channel mode array in smem
 constexpr int kMixBatch = 32;    // systems per CTA of k_mix
 constexpr int kMaxDynSmem = 227 * 1024;
