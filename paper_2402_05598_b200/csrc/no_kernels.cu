@@ -131,6 +131,7 @@ template cudaError_t launch_khat<float>(const double*, const float*, float*, flo
 template cudaError_t launch_khat<double>(const double*, const double*, double*, double*, int, int, int, cudaStream_t);
 
 // ------------------------------------------------------------------ layer-1 mixing with the lift folded in
+constexpr int kLiftCh = 4;      // output channels per CTA of k_lift_mix
 template <typename T>
 __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* __restrict__ rpart, int ngroups,
                                                   const typename Cplx<T>::type* __restrict__ khat,
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
   pdl_wait();
   pdl_trigger();
   using T2 = typename Cplx<T>::type;
-  const int b = blockIdx.x, ochunk = blockIdx.y;   // 8 output channels per CTA
+  const int b = blockIdx.x, ochunk = blockIdx.y;   // kLiftCh output channels per CTA
   if (status && status[b] != SYS_RUNNING) return;
   __shared__ T2 Rh[kModes2];
   for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
@@ -165,7 +166,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
   const int k0 = (kModes / 2) * kModes + kModes / 2;   // kappa = (0, 0)
   // element e -> (o, kappa): kappa fastest for the [B][w][400] layout (FFMA path), o fastest for the
   // mode-major [400][B][w] layout of the tensor-core path, so the stores stay contiguous
-  const int olo = ochunk * 8, ohi = min(w, olo + 8), no_ = ohi - olo, cnt = no_ * kModes2;
+  const int olo = ochunk * kLiftCh, ohi = min(w, olo + kLiftCh), no_ = ohi - olo, cnt = no_ * kModes2;
   auto decode = [&](int e, int& o, int& kk) {
     if (mode_major) { kk = e / no_; o = olo + (e - kk * no_); }
     else { o = olo + e / kModes2; kk = e % kModes2; }
@@ -768,7 +769,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
            reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status);
   ++launches;
   // 2. layer-1 mixing with the lift folded in
-  launch_k(k_lift_mix<T>, dim3(B, (w + 7) / 8), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
+  launch_k(k_lift_mix<T>, dim3(B, (w + kLiftCh - 1) / kLiftCh), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
            reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
            reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2), ghat, w, n2, inv_n2,
            status, (int)tc_layout_modes(no));
