@@ -71,7 +71,7 @@ struct Carver {
 };
 
 bool aligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 255u) == 0; }
-int ngroups_of(int n) { return (n + kDftRows - 1) / kDftRows; }
+int ngroups_of(int n) { return (n + dft_rows(n) - 1) / dft_rows(n); }
 int nblk_of(int n) { return part_cap(n); }   // partial-array capacity per system
 bool no_grid_ok(int n) { return n >= kModes && n <= FCGNO_NO_NMAX; }
 

@@ -64,9 +64,10 @@ __global__ void __launch_bounds__(256) k_dft_rows(const double* __restrict__ x, 
   const int b = blockIdx.y, g = blockIdx.x;
   if (status && status[b] != SYS_RUNNING) return;
   extern __shared__ __align__(16) unsigned char smraw[];
-  T* X = reinterpret_cast<T*>(smraw);                               // [kDftRows][n]
-  T2* Tx = reinterpret_cast<T2*>(X + ((kDftRows * n + 3) & ~3));    // [kDftRows][20]
-  const int N = n * n, i0 = g * kDftRows, rows = min(kDftRows, n - i0);
+  const int DR = dft_rows(n);
+  T* X = reinterpret_cast<T*>(smraw);                               // [DR][n]
+  T2* Tx = reinterpret_cast<T2*>(X + ((DR * n + 3) & ~3));          // [DR][20]
+  const int N = n * n, i0 = g * DR, rows = min(DR, n - i0);
   double inv = 1.0;
   if (FROM_R) {
     const double s = sqrt(rr[b]);
@@ -116,7 +117,9 @@ __global__ void k_reduce_groups(const typename Cplx<T>::type* __restrict__ part,
   }
 }
 
-static size_t dft_smem(int n, size_t tsz) { return ((size_t)((kDftRows * n + 3) & ~3)) * tsz + kDftRows * kModes * 2 * tsz; }
+static size_t dft_smem(int n, size_t tsz) {
+  return ((size_t)((dft_rows(n) * n + 3) & ~3)) * tsz + (size_t)dft_rows(n) * kModes * 2 * tsz;
+}
 
 template <typename T>
 cudaError_t launch_khat(const double* k, const T* F, T* part, T* khat, int n, int B, int ngroups, cudaStream_t s) {
