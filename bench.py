@@ -3,9 +3,10 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-A step is one fcgno_fcg_solve over the whole batch of configs[1] (config 2: 64x64 grid, batch 64,
-FCG(m=5), tol 1e-6, random-init SNO width 48 in fp32 with fp64 FCG vectors; the random-init NO
-does not converge, so every step runs maxit = 2000 iterations).  value =
+A step is one fcgno_fcg_solve over the whole batch of the largest single-GPU configuration,
+configs[2] (config 3: 128x128 grid, batch 128, high-contrast lognormal k, FCG(m=10), tol 1e-6,
+random-init SNO width 85 in fp32 with fp64 FCG vectors; the random-init NO does not converge, so
+every step runs maxit = 2000 iterations).  value =
 unknown-iterations/s = sum_b N*iters_b over all ranks / max-over-ranks device time.  Under
 torchrun each rank solves its own batch of independent systems (weak scaling, no data-path
 collective).  Rank 0 prints one JSON line.
@@ -38,7 +39,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--maxit", type=int, default=None, help="override the config's maxit")
     ap.add_argument("--no-split", action="store_true", help="skip the instrumented time-split solve")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -81,25 +82,51 @@ def shard_systems(batch: int, rank: int):
 
 # ----------------------------------------------------------------------------- workload model
 def layer_flops(B, n, w, cin):
-    """Algorithmic FLOPs of one SNO operator layer over the batch:
-    bypass 2*cin*w*N, x-synthesis 4K*w*N, x-analysis 4K*w*N, y-synthesis and y-analysis
-    8K^2*w*n each."""
+    """Algorithmic FLOPs of the GEMMs the tensor-core layer kernel itself performs for one SNO
+    operator layer over the batch: bypass 2*cin*w*N, x-synthesis 4K*w*N and
+    x-analysis 4K*w*N (the y-direction DFTs run in their own kernels and are not credited here)."""
     N = n * n
-    return B * (2 * cin * w * N + 8 * K_MODES * w * N + 16 * K_MODES * K_MODES * w * n)
+    return B * (2 * cin * w * N + 8 * K_MODES * w * N)
+
+
+def layer_flops_ffma(B, n, w, cin):
+    """FLOPs of one FFMA layer launch (k_no_layer also does the y-direction DFTs: 16K^2 w n)."""
+    return layer_flops(B, n, w, cin) + B * 16 * K_MODES * K_MODES * w * n
+
+
+def src_hash():
+    """sha256 (16 hex) of the library sources: ties a stored ncu capture to the code it measured."""
+    import hashlib
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2402_05598_b200", "csrc")
+    for name in sorted(os.listdir(csrc)):
+        if name.endswith((".cu", ".cuh", ".h")):
+            h.update(name.encode())
+            h.update(open(os.path.join(csrc, name), "rb").read())
+    h.update(open(os.path.join(ROOT, "include", "fcgno.h"), "rb").read())
+    return h.hexdigest()[:16]
+
+
+def ncu_traffic(config, kernel):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, ncu --set full) of
+    `kernel` at `config` from profiles/ncu_traffic.json, only when that capture was taken on these
+    exact sources (src_sha16); otherwise (None, reason)."""
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(tpath))
+    except (OSError, ValueError):
+        return None, "no ncu capture on file"
+    if d.get("src_sha16") != src_hash():
+        return None, "ncu capture on file is from other sources (src_sha16 mismatch); not reported"
+    v = d.get(f"config{config}", {}).get(kernel)
+    return (v, d.get("source", "ncu")) if v is not None else (None, f"no capture of {kernel} at config {config}")
 
 
 def layer_bytes(B, n, w):
-    """Algorithmic HBM bytes of the three tensor-core SNO layer launches of one NO apply, averaged
-    (DESIGN.md §6): layer 1 reads r, k (fp64) and G, writes v1 and T; layer 2 reads v1, G, writes
-    v2, T; layer 3 reads v2, G, writes the 1-channel projection term p3 and T.  Activations count
-    4 B per value (bf16 hi + lo), G and T 40 values per (row, channel)."""
-    N = n * n
-    act = B * N * w * 4
-    gt = B * n * w * 40 * 4
-    l1 = 2 * B * N * 8 + gt + act + gt
-    l2 = act + gt + act + gt
-    l3 = act + gt + B * N * 4 + gt
-    return (l1 + l2 + l3) / 3
+    """Algorithmic HBM bytes of one SNO layer launch ("NO activations,
+    materialised": 3 writes + 3 reads of w fp32 channels per FCG-NO iteration = 24 w B per unknown,
+    i.e. 8 w B per unknown for each of the three layer launches)."""
+    return 8 * w * B * n * n
 
 
 def mean_window(m, iters):
@@ -179,40 +206,84 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU baseline (oracle)
-def cpu_oracle_rate(cfg, budget_s=12.0, max_iters=400, precond="no"):
-    """The oracle as it stands: FCG-NO (fp64 NO, exact dots) on system 0 of the workload, on one
-    host thread, for as many iterations as fit ~budget_s.  Returns (unknown-iterations/s, sample).
-    precond: "no" (the config's random-init SNO), "identity", or "structured" (SURVEY C.2 #30)."""
+def _oracle_worker(job):
+    """One host process: the oracle as it stands (single-threaded numpy) on one system of the
+    workload for `iters` FCG iterations.  Returns (unknown-iterations done, seconds)."""
+    cfg, system, iters, precond = job
     import numpy as np
     from threadpoolctl import threadpool_limits
 
     import oracle as orc
     import synthetic as sy
     with threadpool_limits(limits=1):
-        k = sy.make_k(cfg, systems=[0])[0]
-        f = sy.make_f(cfg, systems=[0])[0]
+        k = sy.make_k(cfg, systems=[system])[0]
+        f = sy.make_f(cfg, systems=[system])[0]
         blob = sy.make_weights(cfg) if precond == "no" else sy.structured_no_weights(cfg["width"], cfg["n"])
         params = orc.unpack_weights(blob, cfg["width"])
-        A = lambda x: orc.apply_A(k, x)
         P = None if precond == "identity" else (lambda r: orc.no_forward(params, r, k))
         t0 = time.perf_counter()
-        orc.fcg(A, f, np.zeros_like(f), cfg["m"], cfg["tol"], 3, precond=P)
-        per_it = (time.perf_counter() - t0) / 3
-        iters = int(max(5, min(max_iters, budget_s / max(per_it, 1e-6))))
-        t0 = time.perf_counter()
-        res = orc.fcg(A, f, np.zeros_like(f), cfg["m"], cfg["tol"], iters, precond=P)
+        res = orc.fcg(lambda x: orc.apply_A(k, x), f, np.zeros_like(f), cfg["m"], cfg["tol"], iters, precond=P)
         dt = time.perf_counter() - t0
-    N = cfg["n"] ** 2
-    done = res["iters"]
+    return cfg["n"] ** 2 * res["iters"], dt
+
+
+def host_cpu_model():
     host = platform.processor() or platform.machine()
     try:
         host = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
     except (OSError, StopIteration):
         pass
+    return host
+
+
+def cpu_oracle_rate(cfg, budget_s=12.0, max_iters=400, precond="no", procs=None, pool=None):
+    """The oracle as it stands (fp64 NO, exact dots), parallel over systems only (SURVEY.md §8(d)
+    D.5): P = min(B, host cores) single-threaded processes, process p running system p of the
+    workload for ~budget_s.  value = all processes' unknown-iterations / the slowest process's time
+    (they run concurrently).  Returns (unknown-iterations/s, processes, sample)."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    P = max(1, min(cfg["batch"], cores if procs is None else procs))
+    # calibrate the per-iteration cost on one system (3 iterations, this process)
+    _, dt3 = _oracle_worker((cfg, 0, 3, precond))
+    per_it = dt3 / 3
+    iters = int(max(3, min(max_iters, budget_s / max(per_it, 1e-6))))
+    jobs = [(cfg, b, iters, precond) for b in range(P)]
+    if P == 1:
+        results = [_oracle_worker(jobs[0])]
+    elif pool is not None:
+        results = pool.map(_oracle_worker, jobs, chunksize=1)
+    else:
+        with mp.get_context("spawn").Pool(P) as own:
+            results = own.map(_oracle_worker, jobs, chunksize=1)
+    units = sum(u for u, _ in results)
+    wall = max(dt for _, dt in results)
     kind = {"no": "FCG-NO (fp64 NO, exact dots)", "identity": "FCG(I) (exact dots)",
             "structured": "FCG with the structured SNO (fp64, exact dots)"}[precond]
-    return N * done / dt, (f"system 0 of the workload, {done} {kind} iterations, {dt:.1f} s on 1 thread of "
-                           f"{host} ({os.cpu_count()} logical CPUs)")
+    done = units // (cfg["n"] ** 2)
+    sample = (f"systems 0..{P - 1} of the workload, {iters} {kind} iterations each ({done} in total), "
+              f"{P} single-threaded processes in parallel, slowest {wall:.1f} s, on {host_cpu_model()} "
+              f"({cores} logical CPUs)")
+    return units / wall, P, sample
+
+
+def workload_config(args, cfg, world):
+    """The `config` object of the JSON line (identical for both arms)."""
+    return {"workload": f"config{args.config}", "precond": args.precond,
+            "fcg_vectors": "fp32" if args.vec32 else "fp64", "n": cfg["n"], "batch": cfg["batch"], "m": cfg["m"],
+            "tol": cfg["tol"], "maxit": cfg["maxit"], "no_width": cfg["width"], "no_precision": cfg["no_precision"],
+            "k_field": cfg["k"], "rhs": cfg["rhs"], "l2": "flushed (256 MiB write) before every step",
+            "parallelism": f"batch replicas x{world} (weak)"}
+
+
+def bench_cfg(args):
+    import synthetic as sy
+    cfg = dict(sy.CONFIGS[args.config])
+    if args.precond != "no":   # converging runs: the iteration cap of SURVEY D.2's identity column
+        cfg["maxit"] = CONVERGE_MAXIT[args.config]
+    if args.maxit:
+        cfg["maxit"] = args.maxit
+    return cfg
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -228,11 +299,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    cfg = dict(sy.CONFIGS[args.config])
-    if args.precond != "no":   # converging runs: the iteration cap of SURVEY D.2's identity column
-        cfg["maxit"] = CONVERGE_MAXIT[args.config]
-    if args.maxit:
-        cfg["maxit"] = args.maxit
+    cfg = bench_cfg(args)
     n, B, w, m = cfg["n"], cfg["batch"], cfg["width"], cfg["m"]
     N = n * n
     systems = shard_systems(B, rank)
@@ -303,7 +370,7 @@ def run_ours(args):
     psolver.solve(df, u)
     F.profile_reset()
     prof_ms = 0.0
-    for _ in range(max(1, min(args.steps, 2))):
+    for _ in range(1):
         flush.zero_()
         u.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -327,14 +394,8 @@ def run_ours(args):
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peaks = json.load(open(peaks_path)) if os.path.exists(peaks_path) else {"hbm_gbs": 6650.0}
     hbm = float(peaks.get("hbm_gbs", 6650.0))
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            traffic = json.load(open(tpath)).get(f"config{args.config}", {}).get("k_no_layer")
-        except (ValueError, OSError):
-            traffic = None
-    tc_path = cfg["no_precision"] == "fp32" and 64 <= n <= 128 and n % 16 == 0 and w <= 128
+    tc_path = no is not None and F.no_uses_tensor_cores(prob, no)
+    traffic, traffic_src = ncu_traffic(args.config, "k_tc_layer" if tc_path else "k_no_layer")
     if no is None:
         # identity FCG: k_pform_stencil, (6 + m_i) 8 B per unknown at the sampled iterations (w = r;
         # 4 * 8 at i = 0), every system running
@@ -354,15 +415,19 @@ def run_ours(args):
         alg = layer_bytes(B, n, w)
         achieved = alg / (avg_layer_ms * 1e-3) / 1e9
         roofline = {"kernel": "k_tc_layer", "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                    "frac": achieved / hbm, "traffic": traffic, "algorithmic_bytes_per_launch": alg,
+                    "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                    "algorithmic_bytes_per_launch": alg,
+                    "bytes_definition": "SURVEY.md 8(d) D.3: 8 w B per unknown per layer launch (3 writes + 3 reads "
+                                        "of w fp32 channels per iteration)",
                     "avg_launch_ms": avg_layer_ms, "launches_timed": layer_n,
                     "share_of_step": 3 * avg_layer_ms / ms_per_iter,
                     "timing": "CUDA events recorded inside the solve graphs around the layer launches of one sampled "
                               "iteration per 16, in a second timed pass of the same workload",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth, measured on this pool)",
-                    "useful_tflops": (layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)) / 3 / (avg_layer_ms * 1e-3) / 1e12}
+                    "useful_tflops": (layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)) / 3 / (avg_layer_ms * 1e-3) / 1e12,
+                    "useful_tflops_definition": "the layer kernel's own GEMMs (bypass, x-synthesis, x-analysis)"}
     else:
-        flops_iter = layer_flops(B, n, w, 2) + 2 * layer_flops(B, n, w, w)
+        flops_iter = layer_flops_ffma(B, n, w, 2) + 2 * layer_flops_ffma(B, n, w, w)
         avg_flops = flops_iter / 3
         achieved = avg_flops / (avg_layer_ms * 1e-3) / 1e12
         roofline = {"kernel": "k_no_layer", "bound": "alu", "achieved": achieved, "peak": FP32_ALU_PEAK_TFLOPS,
@@ -386,11 +451,7 @@ def run_ours(args):
            "dtype": "f64" if no is None else "bf16x3 split (NO tensor cores, fp32 accumulate) + f64 (FCG vectors, dots)",
            "data": "synthetic (seeded; BASELINE configs recipe, " + {"no": "random-init NO weights)", "identity":
                    "identity preconditioner)", "structured": "structured SNO weights, SURVEY C.2 #30)"}[args.precond],
-           "config": {"workload": f"config{args.config}", "precond": args.precond,
-                      "fcg_vectors": "fp32" if args.vec32 else "fp64", "n": n, "batch": B, "m": m, "tol": cfg["tol"],
-                      "maxit": cfg["maxit"], "no_width": w, "no_precision": cfg["no_precision"],
-                      "k_field": cfg["k"], "rhs": cfg["rhs"], "l2": "flushed (256 MiB write) before every step",
-                      "parallelism": f"batch replicas x{world} (weak)"},
+           "config": workload_config(args, cfg, world),
            "iterations_per_step": iters_step, "ms_per_iteration": ms_per_iter,
            "step_ms": [round(t, 3) for t in times], "warmup_ms": warm_ms,
            "hbm_roofline_per_iteration": {"algorithmic_bytes_per_iter": bytes_iter, "peak_gbs": hbm,
@@ -409,10 +470,11 @@ def run_ours(args):
     if not args.no_split and rank == 0:
         out["time_split_ms_per_iter"] = time_split(F, prob, no, cfg, df, vec32=args.vec32)
     if rank == 0:
-        out["e2e"] = e2e_measure(F, no, cfg, k, f, args.steps, args.vec32)
+        out["e2e"] = e2e_measure(F, no, cfg, k, f, min(args.steps, 3), args.vec32)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, sample = cpu_oracle_rate(cfg, precond=args.precond)
-        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample}
+        rate, procs, sample = cpu_oracle_rate(cfg, precond=args.precond)
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": procs, "threads_per_process": 1,
+                               "kind": "oracle", "sample": sample}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -469,30 +531,36 @@ def e2e_measure(F, no, cfg, k, f, steps, vec32=False):
     N = n * n
     return {"value": units / (tot_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": 3 * B * N * 8,
             "d2h_bytes_per_step": B * N * 8 + 2 * 4 * B, "ms_per_step": tot_ms / steps,
-            "api": "fcgno_solve_host (pinned host buffers; includes assemble)"}
+            "steps": steps, "api": "fcgno_solve_host (pinned host buffers; includes assemble)"}
 
 
 # ----------------------------------------------------------------------------- reference arm (oracle)
 def run_reference(args):
+    """Reference arm: the oracle as it stands on the host cores (there is no reference implementation:
+    the reference is a paper).  Each of the W + K steps is a bounded sample of the workload (one
+    oracle run per process over min(B, cores) systems, ~3 s); value = mean over the K timed steps."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    import synthetic as sy
-    cfg = dict(sy.CONFIGS[args.config])
-    if args.maxit:
-        cfg["maxit"] = args.maxit
-    rates, samples = [], []
-    for step in range(args.warmup + args.steps):
-        rate, sample = cpu_oracle_rate(cfg, budget_s=4.0, max_iters=100, precond=args.precond)
-        if step >= args.warmup:
-            rates.append(rate); samples.append(sample)
+    import multiprocessing as mp
+    cfg = bench_cfg(args)
+    P = max(1, min(cfg["batch"], os.cpu_count() or 1))
+    rates, samples, walls = [], [], []
+    with mp.get_context("spawn").Pool(P) as pool:
+        for step in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            rate, procs, sample = cpu_oracle_rate(cfg, budget_s=3.0, max_iters=100, precond=args.precond, pool=pool)
+            if step >= args.warmup:
+                rates.append(rate); samples.append(sample); walls.append(time.perf_counter() - t0)
     value = statistics.mean(rates)
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-           "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"config{args.config}", "n": cfg["n"], "batch": cfg["batch"], "m": cfg["m"],
-                      "tol": cfg["tol"], "maxit": cfg["maxit"], "no_width": cfg["width"]},
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": samples[-1]},
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(walls),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded; BASELINE configs recipe, " + {"no": "random-init NO weights)", "identity":
+                   "identity preconditioner)", "structured": "structured SNO weights, SURVEY C.2 #30)"}[args.precond],
+           "config": workload_config(args, cfg, world),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "threads_per_process": 1, "kind": "oracle",
+                            "sample": samples[-1]},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 

@@ -158,6 +158,10 @@ FCGNO_API int fcgno_batched_dot(const fcgno_problem* p, const double* x, const d
 FCGNO_API size_t fcgno_no_packed_bytes(fcgno_no_desc d);
 FCGNO_API int fcgno_no_pack(fcgno_no_desc d, const double* weights_host, void* packed, void* stream);
 
+/* 1 when fcgno_apply_NO / fcgno_fcg_solve run the NO operator layers of grid g on the tcgen05 tensor
+ * cores (fp32 NO, supported n and w, an sm_100 device present), 0 for the FFMA kernels.  Diagnostics. */
+FCGNO_API int fcgno_no_uses_tensor_cores(fcgno_grid g, fcgno_no_desc d);
+
 /* apply_NO(weights, r, k) — w_b = ||r_b|| * NO([r_b/||r_b||, k_b]) for every system, w_b = 0
  * when r_b = 0 ("w_i <- B(r_i)").
  *   r, w [B][n][n] fp64 device (w != r); requires 20 <= n <= FCGNO_NO_NMAX.

@@ -373,6 +373,12 @@ int fcgno_no_pack(fcgno_no_desc d, const double* blob, void* packed, void* strea
   return FCGNO_OK;
 }
 
+int fcgno_no_uses_tensor_cores(fcgno_grid g, fcgno_no_desc d) {
+  if (check_desc(d) != FCGNO_OK || g.n < 2 || g.batch < 1) return 0;
+  return (d.precision == FCGNO_FP32 && tc_enabled() && tc_layer_supported_host(g.n, d.width) &&
+          tc_layer_supported(g.n, d.width)) ? 1 : 0;
+}
+
 // ------------------------------------------------------------------ apply_NO
 size_t fcgno_apply_no_workspace_bytes(fcgno_grid g, fcgno_no_desc d) {
   if (g.n < 2 || g.batch < 1 || check_desc(d) != FCGNO_OK) return 0;
@@ -771,21 +777,39 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
   }
 
   // Private streams (graph capture is not allowed on the legacy default stream), ordered after
-  // everything already enqueued on the caller's stream.
-  cudaStream_t st[kMaxLanes];
+  // everything already enqueued on the caller's stream.  Owned by `res`, whose destructor releases
+  // whatever was created, on every return path.
+  struct SolveResources {
+    cudaStream_t st[kMaxLanes] = {};
+    cudaEvent_t ev_in = nullptr, ev_poll[2] = {}, ev_fj[kMaxLanes] = {};
+    int* h_active = nullptr;
+    Chunk full[2], tail;
+    ~SolveResources() {
+      full[0].destroy(); full[1].destroy(); tail.destroy();
+      if (h_active) cudaFreeHost(h_active);
+      if (ev_in) cudaEventDestroy(ev_in);
+      for (cudaEvent_t e : ev_poll) if (e) cudaEventDestroy(e);
+      for (cudaEvent_t e : ev_fj) if (e) cudaEventDestroy(e);
+      for (cudaStream_t q : st) if (q) cudaStreamDestroy(q);
+    }
+  } res;
+  cudaStream_t* st = res.st;
+  cudaEvent_t* ev_poll = res.ev_poll;
+  cudaEvent_t* ev_fj = res.ev_fj;
   for (int l = 0; l < nl; ++l) CK(cudaStreamCreateWithFlags(&st[l], cudaStreamNonBlocking));
   cudaStream_t s = st[0];
-  cudaEvent_t ev_in, ev_poll[2], ev_fj[kMaxLanes];
-  CK(cudaEventCreateWithFlags(&ev_in, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&res.ev_in, cudaEventDisableTiming));
+  cudaEvent_t ev_in = res.ev_in;
   CK(cudaEventCreateWithFlags(&ev_poll[0], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&ev_poll[1], cudaEventDisableTiming));
   for (int l = 0; l < nl; ++l) CK(cudaEventCreateWithFlags(&ev_fj[l], cudaEventDisableTiming));
   CK(cudaEventRecord(ev_in, caller));
   CK(cudaStreamWaitEvent(s, ev_in, 0));
-  int* h_active = nullptr;
-  CK(cudaHostAlloc(&h_active, 2 * kMaxLanes * sizeof(int), cudaHostAllocDefault));
+  CK(cudaHostAlloc(&res.h_active, 2 * kMaxLanes * sizeof(int), cudaHostAllocDefault));
+  int* h_active = res.h_active;
   int rc = FCGNO_OK;
-  Chunk full[2], tail;
+  Chunk* full = res.full;
+  Chunk& tail = res.tail;
   do {
     cudaError_t e = cudaSuccess;
     for (int l = 0; l < nl && rc == FCGNO_OK; ++l) {
@@ -889,15 +913,8 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
   }
   if (rc == FCGNO_OK && e_end != cudaSuccess) rc = cuda_fail(e_end, "solve");
   if (rc == FCGNO_OK) (void)cudaGetLastError();
-  // order the caller's stream after the solve
+  // order the caller's stream after the solve (resources are released by `res`)
   if (cudaEventRecord(ev_in, s) == cudaSuccess) cudaStreamWaitEvent(caller, ev_in, 0);
-  full[0].destroy(); full[1].destroy(); tail.destroy();
-  cudaFreeHost(h_active);
-  cudaEventDestroy(ev_in);
-  cudaEventDestroy(ev_poll[0]);
-  cudaEventDestroy(ev_poll[1]);
-  for (int l = 0; l < nl; ++l) cudaEventDestroy(ev_fj[l]);
-  for (int l = 0; l < nl; ++l) cudaStreamDestroy(st[l]);
   return rc;
 }
 

@@ -59,6 +59,7 @@ EXPORTS = {
     "fcgno_batched_dot": (_i, [_vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "fcgno_no_packed_bytes": (_sz, [NoDesc]),
     "fcgno_no_pack": (_i, [NoDesc, _vp, _vp, _vp]),
+    "fcgno_no_uses_tensor_cores": (_i, [Grid, NoDesc]),
     "fcgno_apply_no_workspace_bytes": (_sz, [Grid, NoDesc]),
     "fcgno_apply_NO": (_i, [_vp, NoDesc, _vp, _vp, _vp, _vp, _sz, _vp]),
     "fcgno_solve_workspace_bytes": (_sz, [Grid, _P(NoDesc), SolveOpts]),
@@ -98,9 +99,22 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def _workspace(nbytes: int, device) -> torch.Tensor:
-    # torch's caching allocator returns 512-byte aligned blocks
-    return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+def _workspace(nbytes: int, device, stream=None) -> torch.Tensor:
+    """Device workspace (torch's caching allocator returns 512-byte aligned blocks).  When the
+    library call runs on `stream` rather than torch's current stream, the block is allocated on
+    `stream`, so the allocator cannot hand it to other work while the call's kernels still use it."""
+    if stream is None:
+        return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+    with torch.cuda.stream(stream):
+        return torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=device)
+
+
+def _on(stream, make):
+    """Allocate an output with `make()` on `stream` (see _workspace)."""
+    if stream is None:
+        return make()
+    with torch.cuda.stream(stream):
+        return make()
 
 
 def _require(t: torch.Tensor, shape, name):
@@ -121,6 +135,11 @@ def abi_version() -> int:
 PROF_NCLASS = 10
 PROF_NO_LAYER, PROF_NO_MIX, PROF_NO_OUT, PROF_NO_INPUT, PROF_WINDOW, PROF_PFORM, PROF_STENCIL, PROF_UPDATE, \
     PROF_FINALIZE, PROF_NO_YDIR = range(PROF_NCLASS)
+
+
+def no_uses_tensor_cores(problem: "Problem", no: "NeuralOperator") -> bool:
+    """True when the NO's operator layers run on the tcgen05 tensor-core kernels for this grid."""
+    return bool(_lib.fcgno_no_uses_tensor_cores(problem.grid, no.desc))
 
 
 def profile_reset() -> None:
@@ -169,15 +188,15 @@ class Problem:
 
     def apply_A(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         _require(x, self.shape, "x")
-        y = torch.empty_like(x) if out is None else out
+        y = _on(stream, lambda: torch.empty_like(x)) if out is None else out
         _check(_lib.fcgno_apply_A(self._h, _ptr(x), _ptr(y), _stream(stream)))
         return y
 
     def dot(self, x: torch.Tensor, y: torch.Tensor, stream=None) -> torch.Tensor:
         _require(x, self.shape, "x")
         _require(y, self.shape, "y")
-        out = torch.empty(self.B, dtype=torch.float64, device=self.device)
-        ws = _workspace(_lib.fcgno_dot_workspace_bytes(self.grid), self.device)
+        out = _on(stream, lambda: torch.empty(self.B, dtype=torch.float64, device=self.device))
+        ws = _workspace(_lib.fcgno_dot_workspace_bytes(self.grid), self.device, stream)
         _check(_lib.fcgno_batched_dot(self._h, _ptr(x), _ptr(y), _ptr(out), _ptr(ws), ws.numel(), _stream(stream)))
         return out
 
@@ -198,8 +217,8 @@ class NeuralOperator:
 
     def apply(self, problem: Problem, r: torch.Tensor, stream=None) -> torch.Tensor:
         _require(r, problem.shape, "r")
-        w = torch.empty_like(r)
-        ws = _workspace(_lib.fcgno_apply_no_workspace_bytes(problem.grid, self.desc), problem.device)
+        w = _on(stream, lambda: torch.empty_like(r))
+        ws = _workspace(_lib.fcgno_apply_no_workspace_bytes(problem.grid, self.desc), problem.device, stream)
         _check(_lib.fcgno_apply_NO(problem._h, self.desc, _ptr(self.packed), _ptr(r), _ptr(w), _ptr(ws), ws.numel(),
                                    _stream(stream)))
         return w

@@ -290,26 +290,6 @@ def test_identity_vec32_ragged_and_wide(lib, n, B, m, maxit, systems):
     _check_identity(lib, k, f, m, 1e-6 if n < 100 else 1e-14, maxit, systems, vec32=True)
 
 
-def test_fcg_no_fp32_vec32_config3_first_step(lib):
-    # BASELINE configs[2]: fp32 NO with fp32 FCG vectors.  As for the fp64-vector variant, the
-    # fp32 NO is compared over one NO application + one FCG update from identical state.
-    cfg = sy.CONFIGS[3]
-    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
-    w = cfg["width"]
-    params = orc.unpack_weights(blob, w)
-    maxit = 6
-    prob = lib.Problem(dev(k))
-    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit,
-                        no=lib.NeuralOperator(w, blob, precision=lib.FP32), vec_fp32=True)
-    assert np.all(host(res.status) == lib.MAXIT)
-    for b in (0, cfg["batch"] - 1):
-        ref = orc.fcg(lambda x: orc.apply_A(k[b], x), f[b], np.zeros_like(f[b]), cfg["m"], cfg["tol"], maxit,
-                      precond=lambda r: orc.no_forward(params, r, k[b]), vec32=True)
-        h = host(res.history)[b]
-        assert abs(h[1] - ref["hist"][1]) / ref["hist"][1] <= 1e-4
-        assert np.all(np.isfinite(h[:maxit + 1]))
-
-
 @pytest.mark.parametrize("n", [4, 8])
 def test_identity_sliding_full_window_finite_termination(lib, n):
     k = sy.lognormal_k(n, 2, 0.1, 4.0, 71)
@@ -398,22 +378,76 @@ def test_fcg_structured_no_fp64_counts(lib):
         assert _prefix_window_ok(host(res.history)[b], ref["hist"], window)
 
 
-def test_fcg_no_fp32_config2_sampled(lib):
-    cfg = sy.CONFIGS[2]
-    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
-    w = cfg["width"]
-    params = orc.unpack_weights(blob, w)
-    maxit = 30
+# ----------------------------------------------------------------------------- FCG with the fp32 NO: hybrid runs
+# Algorithm 1 as the oracle writes it, with B(r) = the library's own fp32 NO
+# (fcgno_apply_NO on the full batch, the system's r in its slot and r = 0 elsewhere, so the launch
+# geometry is the solve's own), against fcg_solve with that NO.  The NO kernels are deterministic
+# and the FCG step is bitwise equal to the oracle's (identity tests above), so histories, iterates,
+# counts and statuses must agree bit for bit: a wrong window slot, beta, ring index or fused-dot
+# prefetch in the solve's NO-output kernel (k_no_out_blob) fails here at the first iteration it
+# touches.  The fp32 NO itself is held to the oracle's fp64 NO by the <= 1e-4 forward tests.
+def _gpu_precond(lib, prob, no, B, n, b, vec32=False):
+    def P(r):
+        full = np.zeros((B, n, n))
+        full[b] = r
+        return host(no.apply(prob, dev(full)))[b]
+    return P
+
+
+def _hybrid_check(lib, cfg, systems, maxit, vec32=False, blob=None, tol=None, expect_status=None):
+    k, f = sy.make_k(cfg), sy.make_f(cfg)
+    blob = sy.make_weights(cfg) if blob is None else blob
+    tol = cfg["tol"] if tol is None else tol
+    n, B, w, m = cfg["n"], cfg["batch"], cfg["width"], cfg["m"]
     prob = lib.Problem(dev(k))
     no = lib.NeuralOperator(w, blob, precision=lib.FP32)
-    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit, no=no)
-    assert np.all(host(res.status) == lib.MAXIT) and np.all(host(res.iters) == maxit)
-    for b in (0, cfg["batch"] - 1):
-        ref = _oracle_fcg(k[b], f[b], cfg["m"], cfg["tol"], maxit,
-                          precond=lambda r: orc.no_forward(params, r, k[b]))
-        h = host(res.history)[b]
-        # fp32 NO vs fp64 NO moves histories by ~1e-5..1e-3
-        assert np.max(np.abs(h - ref["hist"]) / ref["hist"]) <= 1e-2
+    res = lib.fcg_solve(prob, dev(f), m=m, tol=tol, maxit=maxit, no=no, vec_fp32=vec32)
+    iters, status, hist, u = host(res.iters), host(res.status), host(res.history), host(res.u)
+    for b in systems:
+        ref = orc.fcg(lambda x: orc.apply_A(k[b], x), f[b], np.zeros_like(f[b]), m, tol, maxit,
+                      precond=_gpu_precond(lib, prob, no, B, n, b), vec32=vec32)
+        it = ref["iters"]
+        assert iters[b] == it and status[b] == ref["status"], (b, iters[b], it, status[b], ref["status"])
+        assert np.array_equal(hist[b, :it + 1], ref["hist"]), \
+            (b, int(np.argmax(hist[b, :it + 1] != ref["hist"])))
+        assert np.array_equal(u[b], ref["u"])
+        if expect_status is not None:
+            assert status[b] == expect_status
+    return prob, no, iters, status
+
+
+@pytest.mark.parametrize("vec32", [False, True])
+def test_fcg_no_fp32_hybrid_bitwise_config2_full(lib, vec32):
+    # The headline path at config 2: the tensor-core NO feeding FCG(5), all 2000 iterations (R19).
+    cfg = sy.CONFIGS[2]
+    prob, no, iters, status = _hybrid_check(lib, cfg, [0, cfg["batch"] - 1], cfg["maxit"], vec32=vec32,
+                                            expect_status=lib.MAXIT)
+    assert lib.no_uses_tensor_cores(prob, no)
+    assert np.all(iters == cfg["maxit"])
+
+
+@pytest.mark.parametrize("cfg_id,maxit", [(3, 200), (4, 120), (5, 40)])
+def test_fcg_no_fp32_hybrid_bitwise_large_configs(lib, cfg_id, maxit):
+    # Prefixes of the large workloads: config 3 (tensor cores, n = 128, w = 85, m = 10), configs 4
+    # and 5 (n = 256 / 512), systems {0, B-1}.
+    cfg = sy.CONFIGS[cfg_id]
+    _hybrid_check(lib, cfg, [0, cfg["batch"] - 1], maxit, expect_status=lib.MAXIT)
+
+
+def test_fcg_no_fp32_hybrid_bitwise_config3_vec32(lib):
+    cfg = sy.CONFIGS[3]
+    _hybrid_check(lib, cfg, [0, cfg["batch"] - 1], 100, vec32=True, expect_status=lib.MAXIT)
+
+
+def test_fcg_structured_no_fp32_tensor_core_counts(lib):
+    # The convergent structured SNO at the config-2 geometry on the tensor-core
+    # path: converging runs, iteration counts, histories and iterates bit for bit.
+    cfg = dict(sy.CONFIGS[2], batch=4, width=4)
+    blob = sy.structured_no_weights(4, cfg["n"])
+    prob, no, iters, status = _hybrid_check(lib, cfg, [0, 3], 1000, blob=blob, tol=1e-8,
+                                            expect_status=lib.CONVERGED)
+    assert lib.no_uses_tensor_cores(prob, no)
+
 
 
 def test_solve_host_matches_device(lib):
@@ -436,30 +470,6 @@ def test_repeat_solves_deterministic(lib):
     u1 = torch.zeros_like(dev(f)); s.solve(dev(f), u1); h1 = s.history.clone()
     u2 = torch.zeros_like(dev(f)); s.solve(dev(f), u2)
     assert torch.equal(u1, u2) and torch.equal(h1, s.history)
-
-
-@pytest.mark.parametrize("cfg_id", [3, 5])
-def test_fcg_no_fp32_large_configs_sampled(lib, cfg_id):
-    # Config 3 runs the tensor-core NO path (n = 128, w = 85), config 5 the FFMA fallback (n = 512).
-    # FCG amplifies NO rounding chaotically at these contrasts (config 3: a 1e-6 relative perturbation
-    # of the oracle's own NO output moves ||r_2||/||r_0|| by 1.6e-3), so histories of an
-    # fp32 NO are compared over the first step only: one NO application + one FCG update from
-    # identical state, within the fp32-NO tolerance.
-    cfg = sy.CONFIGS[cfg_id]
-    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
-    w = cfg["width"]
-    params = orc.unpack_weights(blob, w)
-    maxit = 6
-    prob = lib.Problem(dev(k))
-    res = lib.fcg_solve(prob, dev(f), m=cfg["m"], tol=cfg["tol"], maxit=maxit,
-                        no=lib.NeuralOperator(w, blob, precision=lib.FP32))
-    assert np.all(host(res.status) == lib.MAXIT)
-    for b in (0, cfg["batch"] - 1):
-        ref = _oracle_fcg(k[b], f[b], cfg["m"], cfg["tol"], maxit,
-                          precond=lambda r: orc.no_forward(params, r, k[b]))
-        h = host(res.history)[b]
-        assert abs(h[1] - ref["hist"][1]) / ref["hist"][1] <= 1e-4
-        assert np.all(np.isfinite(h[:maxit + 1]))
 
 
 def test_fcg_no_fp64_config3_prefix(lib):
