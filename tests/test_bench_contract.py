@@ -22,8 +22,8 @@ def test_bench_json_line_contract():
                 "gpu_launches", "clocks"):
         assert key in d, key
     assert d["steps"] == 2 and d["warmup"] >= 3 and d["n_gpus"] == 1 and d["higher_is_better"] is True
-    assert d["config"]["workload"] == "config2" and d["scaling"] == "weak"
-    cfg_units = 64 * 64 * 64 * 32 * 2                      # B * N * iterations * steps
+    assert d["config"]["workload"] == "config3" and d["scaling"] == "weak"   # the largest single-GPU config
+    cfg_units = 128 * 128 * 128 * 32 * 2                   # B * N * iterations * steps
     assert abs(d["value"] - cfg_units / (d["ms_per_step"] * 2 / 1e3)) <= 1e-6 * d["value"]
     r = d["roofline"]
     assert r["bound"] in ("hbm", "tensor", "alu") and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-12
@@ -42,3 +42,8 @@ def test_reference_arm_contract():
     d = json.loads(out.stdout.strip().splitlines()[-1])
     assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "unknown-iterations/s"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["value"] == d["value"]
+    # same workload description as our arm (the driver compares the two lines' configs)
+    sys.path.insert(0, ROOT)
+    import bench
+    args = bench.parse_args([])
+    assert d["config"] == bench.workload_config(args, bench.bench_cfg(args), 1)
