@@ -17,7 +17,6 @@
 
 #include "../../include/fcgno.h"
 #include "internal.h"
-#include "tc_layout.cuh"
 
 using namespace fcgno;
 
@@ -91,18 +90,25 @@ ProblemWs carve_problem(Carver& c, int n, int B) {
   return w;
 }
 
-// Shapes the tensor-core NO path handles (device smem is re-checked at launch time).
-bool tc_layer_supported_host(int n, int w) {
-  if (w > 128 || w < 1 || n % 16 != 0 || n < 64 || n > 128) return false;
-  const TcGeom g(n, w);
-  return n % g.R == 0;
+// FCGNO_TC=0 in the environment forces the FFMA layer kernel (A/B comparisons, fallbacks).
+bool tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FCGNO_TC");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
+
+// The fp32 NO runs its operator layers on the tensor cores (no_px_kernels.cu) for these shapes; the
+// workspace then holds the tensor-core blobs and no FFMA activations (the carve decides the path).
+bool use_px(int n, int w, bool fp32) { return fp32 && tc_enabled() && px_supported_shape(n, w); }
 
 template <typename T>
 struct NoWs {
   T *rpart, *v0, *v1, *chat, *ghat;
-  unsigned char *vb0, *vb1, *Gb, *Tb, *cst;   // tensor-core path blobs (fp32 NO only)
-  float* p3;
+  unsigned char *vb0, *vb1, *Gb, *cst;   // tensor-core path blobs (fp32 NO only)
+  float *Tb, *p3;
   size_t vb_bytes, gb_bytes;
 };
 template <typename T>
@@ -110,20 +116,21 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
   NoWs<T> r{};
   const size_t N = (size_t)n * n;
   r.rpart = c.take<T>((size_t)B * ngroups_of(n) * kModes2 * 2);
-  r.v0 = c.take<T>((size_t)B * w * N);
-  r.v1 = c.take<T>((size_t)B * w * N);
-  r.chat = c.take<T>((size_t)kRowSplitMax * kModes2 * B * w * 2);   // row-split partials (FFMA layer)
   r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
-  if (sizeof(T) == sizeof(float) && tc_layer_supported_host(n, w)) {
-    const TcGeom g(n, w);
-    r.vb_bytes = g.v_bytes_total(B);
-    r.gb_bytes = g.g_bytes_total(B);
+  if (use_px(n, w, sizeof(T) == sizeof(float))) {
+    r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
+    r.vb_bytes = px_v_bytes(n, w, B);
+    r.gb_bytes = px_g_bytes(n, w, B);
     r.vb0 = c.take<unsigned char>(r.vb_bytes);
     r.vb1 = c.take<unsigned char>(r.vb_bytes);
     r.Gb = c.take<unsigned char>(r.gb_bytes);
-    r.Tb = c.take<unsigned char>(g.t_bytes_total(B));
-    r.cst = c.take<unsigned char>(tc_const_bytes(n, w));
-    r.p3 = c.take<float>((size_t)B * n * n);
+    r.Tb = c.take<float>(px_t_floats(n, w, B));
+    r.cst = c.take<unsigned char>(px_const_bytes(n, w));
+    r.p3 = c.take<float>((size_t)B * N);
+  } else {
+    r.v0 = c.take<T>((size_t)B * w * N);
+    r.v1 = c.take<T>((size_t)B * w * N);
+    r.chat = c.take<T>((size_t)kRowSplitMax * kModes2 * B * w * 2);   // row-split partials (FFMA layer)
   }
   return r;
 }
@@ -139,16 +146,6 @@ int check_desc(const fcgno_no_desc& d) {
   return FCGNO_OK;
 }
 
-// FCGNO_TC=0 in the environment forces the FFMA layer kernel (A/B comparisons, fallbacks).
-bool tc_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FCGNO_TC");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 template <typename T>
 NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* packed, const NoWs<T>& w,
                     const T* F, const T* khat) {
@@ -158,11 +155,15 @@ NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* 
   no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
   no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
   no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb; no.cst = w.cst; no.p3 = w.p3;
-  no.tc = (sizeof(T) == sizeof(float)) && w.Gb != nullptr && tc_enabled() && tc_layer_supported(p->n, d.width);
+  no.tc = (sizeof(T) == sizeof(float)) && w.Gb != nullptr;
   return no;
 }
 
 int check_no_smem(const fcgno_no_desc& d, int n) {
+  if (use_px(n, d.width, d.precision == FCGNO_FP32)) {
+    if (!px_supported(n, d.width)) return fail(FCGNO_EUNSUPPORTED, "tensor-core NO needs 227 KB of shared memory per CTA");
+    return FCGNO_OK;
+  }
   const size_t need = d.precision == FCGNO_FP64 ? no_max_smem<double>(n, d.width) : no_max_smem<float>(n, d.width);
   if (need > 227 * 1024)
     return fail(FCGNO_EUNSUPPORTED, "NO width %d at n=%d needs %zu B of shared memory per CTA", d.width, n, need);
@@ -375,8 +376,7 @@ int fcgno_no_pack(fcgno_no_desc d, const double* blob, void* packed, void* strea
 
 int fcgno_no_uses_tensor_cores(fcgno_grid g, fcgno_no_desc d) {
   if (check_desc(d) != FCGNO_OK || g.n < 2 || g.batch < 1) return 0;
-  return (d.precision == FCGNO_FP32 && tc_enabled() && tc_layer_supported_host(g.n, d.width) &&
-          tc_layer_supported(g.n, d.width)) ? 1 : 0;
+  return (use_px(g.n, d.width, d.precision == FCGNO_FP32) && px_supported(g.n, d.width)) ? 1 : 0;
 }
 
 // ------------------------------------------------------------------ apply_NO
@@ -408,11 +408,6 @@ int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, 
   NoWs<float> w32{}; NoWs<double> w64{};
   carve_no_any(c, p->n, p->B, d, &w32, &w64);
   CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * p->B, s));
-  if (w32.Gb) {   // blob padding (channels >= w, modes 40..47, K rows >= R*CP) must read as zeros
-    CK(cudaMemsetAsync(w32.vb0, 0, w32.vb_bytes, s));
-    CK(cudaMemsetAsync(w32.vb1, 0, w32.vb_bytes, s));
-    CK(cudaMemsetAsync(w32.Gb, 0, w32.gb_bytes, s));
-  }
   CK(launch_dot(r, r, rr, part, cnt, p->n, p->B, s));
   if (d.precision == FCGNO_FP64) {
     CK(prepare_no_kernels<double>());
@@ -420,7 +415,7 @@ int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, 
     CK(launch_no_forward<double>(no, r, rr, w, nullptr, nullptr, s, nullptr));
   } else {
     CK(prepare_no_kernels<float>());
-    CK(prepare_tc_kernels());
+    CK(prepare_px_kernels());
     NoDev<float> no = make_nodev<float>(p, d, packed, w32, p->F32, p->khat32);
     CK(prepare_no_constants(no, s));
     CK(launch_no_forward<float>(no, r, rr, w, nullptr, nullptr, s, nullptr));
@@ -750,7 +745,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
   if (!aligned(ws) || ws_bytes < fcgno_solve_workspace_bytes(g, nd, o)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
   if (nd) {
     if (nd->precision == FCGNO_FP64) CK(prepare_no_kernels<double>());
-    else { CK(prepare_no_kernels<float>()); CK(prepare_tc_kernels()); }
+    else { CK(prepare_no_kernels<float>()); CK(prepare_px_kernels()); }
   }
   cudaStream_t caller = static_cast<cudaStream_t>(stream);
   Carver c(ws);
@@ -817,10 +812,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
       const SolveWs& sw = lanes[l].sw;
       if ((e = cudaMemsetAsync(d.cnt, 0, sizeof(unsigned) * (3 * d.B + 2), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if ((e = cudaMemsetAsync(d.iter, 0, 2 * sizeof(int), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
-      if (nd && sw.n32.Gb) {   // blob padding must read as zeros
-        if ((e = cudaMemsetAsync(sw.n32.vb0, 0, sw.n32.vb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
-        if ((e = cudaMemsetAsync(sw.n32.vb1, 0, sw.n32.vb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
-        if ((e = cudaMemsetAsync(sw.n32.Gb, 0, sw.n32.gb_bytes, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+      if (nd && sw.n32.Gb) {   // tensor-core constant operands (every blob byte the kernels read is written by them)
         NoDev<float> no = make_nodev<float>(&lanes[l].p, *nd, packed, sw.n32, p->F32, lanes[l].p.khat32);
         if ((e = prepare_no_constants(no, s)) != cudaSuccess) { rc = cuda_fail(e, "tc constants"); break; }
       }

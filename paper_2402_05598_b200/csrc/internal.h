@@ -70,39 +70,44 @@ struct NoDev {
   T* v1;                      // [B][w][N]
   T* chat;                    // [400][B][w] complex
   T* ghat;                    // [B][w][400] complex
-  unsigned char* vb0;         // tensor-core path: activation blobs (ping-pong), tc_layout.cuh
+  unsigned char* vb0;         // tensor-core path: activation blobs (ping-pong), px_layout.cuh
   unsigned char* vb1;
-  unsigned char* Gb;          // G blobs (y-synthesised spectral term)
-  unsigned char* Tb;          // T blobs (x-analysed activations)
-  unsigned char* cst;         // constant operand blobs (twiddles, block-diagonal weights)
+  unsigned char* Gb;          // G rows (y-synthesised spectral term)
+  float* Tb;                  // T rows (x-analysed activations)
+  unsigned char* cst;         // constant operand blobs (twiddles, layer weights, mixing weights)
   float* p3;                  // [B][n][n] layer-3 projection bypass term (tensor-core path)
-  int tc;                     // 1: fp32 layers on tcgen05 (no_tc_kernels.cu)
+  int tc;                     // 1: fp32 layers on tcgen05 (no_px_kernels.cu)
 };
 
-// Tensor-core SNO layer (no_tc_kernels.cu).
-struct TcLayerArgsHost {
-  int n, w, cin, B, use_gelu, first, layer;
-  const double *r, *rr, *k;
-  const unsigned char* vin;
-  const float *W, *bias;
-  const unsigned char* G;
-  const unsigned char* cst;   // constant operand blobs (launch_tc_prep)
-  unsigned char *vout, *T;
-  const float* dw;   // layer 3: projection weights -> pout (fused projection)
-  float* pout;
+// Tensor-core (pixel-major) SNO path, no_px_kernels.cu.
+struct PxLayerHost {
+  int n, w, B, layer, use_gelu;              // layer 0, 1, 2 = SNO layers 1-3
+  const double *r, *rr, *k;                  // layer 1 inputs
+  const unsigned char* vin;                  // V blobs (layers 2, 3)
+  unsigned char* vout;                       // V blobs written (layers 1, 2)
+  const unsigned char* G;                    // G rows (y-synthesised spectral term)
+  float* T;                                  // T rows (x-analysed activations)
+  const unsigned char* cst;                  // constant operand blobs (launch_px_prep)
+  const float *bias, *w1e, *dw;              // [w]; layer 1: W1 E [w][2]; layer 3: D W4 [w]
+  float* p3;                                 // layer 3: projection bypass term [B][n][n]
   const int* status;
 };
-bool tc_layer_supported(int n, int w);
-cudaError_t prepare_tc_kernels();
-cudaError_t launch_tc_layer(const TcLayerArgsHost& h, cudaStream_t s);
-cudaError_t launch_ysyn(const float* ghat, const unsigned char* cst, unsigned char* Gb, int n, int w, int B,
-                        const int* status, cudaStream_t s);
-cudaError_t launch_yan(const unsigned char* Tb, const unsigned char* cst, float* chat, int n, int w, int B,
-                       const int* status, cudaStream_t s);
-size_t tc_const_bytes(int n, int w);
-cudaError_t launch_tc_prep(int n, int w, const float* W1, const float* W2, const float* W3, const float* R2,
-                           const float* R3, const float* Q, const float* F, unsigned char* out, cudaStream_t s);
-cudaError_t launch_mix_tc(int mix, const float* chat, const unsigned char* cst, float* ghat, int n, int w, int B,
+bool px_supported_shape(int n, int w);       // geometry and shared-memory budget (no device query)
+bool px_supported(int n, int w);             // ... and the device's opt-in shared memory allows it
+size_t px_const_bytes(int n, int w);
+size_t px_v_bytes(int n, int w, int B);
+size_t px_g_bytes(int n, int w, int B);
+size_t px_t_floats(int n, int w, int B);
+size_t px_mx_offset(int n, int w, int mix);
+cudaError_t prepare_px_kernels();
+cudaError_t launch_px_prep(int n, int w, const float* W2, const float* W3, const float* R2, const float* R3,
+                           const float* Q, const float* F, unsigned char* out, cudaStream_t s);
+cudaError_t launch_px_layer(const PxLayerHost& h, cudaStream_t s);
+cudaError_t launch_px_ysyn(const float* ghat, const unsigned char* cst, unsigned char* Gb, int n, int w, int B,
+                           const int* status, cudaStream_t s);
+cudaError_t launch_px_yan(const float* T, const unsigned char* cst, float* chat, int n, int w, int B, const int* status,
+                          cudaStream_t s);
+cudaError_t launch_mix_px(int mix, const float* chat, const unsigned char* cst, float* ghat, int n, int w, int B,
                           float inv_n2, const int* status, cudaStream_t s);
 
 // In-graph profiling hook: begin/end record CUDA events around launches of a kernel class.

@@ -15,7 +15,6 @@
 
 #include "internal.h"
 #include "fcg_device.cuh"
-#include "tc_layout.cuh"
 #include "tc_common.cuh"
 
 namespace fcgno {
@@ -786,7 +785,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   if constexpr (sizeof(T) == sizeof(float)) tc_path = no.tc != 0;
   if (tc_path) {
     pb(PROF_NO_YDIR);
-    launch_ysyn(reinterpret_cast<const float*>(ghat), no.cst, no.Gb, n, w, B, status, s);
+    launch_px_ysyn(reinterpret_cast<const float*>(ghat), no.cst, no.Gb, n, w, B, status, s);
     pe(PROF_NO_YDIR);
     launches += 1;
   }
@@ -794,23 +793,21 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   int nparts = 1;
   for (int l = 0; l < 3; ++l) {
     if (tc_path) {
-      TcLayerArgsHost h{};
-      h.n = n; h.w = w; h.B = B; h.use_gelu = no.use_gelu; h.first = l == 0;
+      PxLayerHost h{};
+      h.n = n; h.w = w; h.B = B; h.use_gelu = no.use_gelu; h.layer = l;
       h.r = r; h.rr = rr; h.k = no.k;
-      h.cin = l == 0 ? 2 : w;
-      h.layer = l;
       h.cst = no.cst;
-      h.W = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.W1E : no.L.W[l - 1]));
       h.bias = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.b1 : no.L.b[l - 1]));
+      h.w1e = reinterpret_cast<const float*>(pk + no.L.W1E);
       h.vin = l == 0 ? nullptr : vblob[(l - 1) & 1];
-      h.vout = vblob[l & 1];
+      h.vout = l == 2 ? nullptr : vblob[l & 1];
       h.G = no.Gb; h.T = no.Tb; h.status = status;
-      if (l == 2) { h.dw = reinterpret_cast<const float*>(pk + no.L.dw); h.pout = no.p3; }
+      if (l == 2) { h.dw = reinterpret_cast<const float*>(pk + no.L.dw); h.p3 = no.p3; }
       pb(PROF_NO_LAYER);
-      launch_tc_layer(h, s);
+      launch_px_layer(h, s);
       pe(PROF_NO_LAYER);
       pb(PROF_NO_YDIR);
-      launch_yan(no.Tb, no.cst, reinterpret_cast<float*>(chat), n, w, B, status, s);
+      launch_px_yan(no.Tb, no.cst, reinterpret_cast<float*>(chat), n, w, B, status, s);
       pe(PROF_NO_YDIR);
       launches += 2;
     } else {
@@ -853,7 +850,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     const size_t msmem = ((size_t)w * cout + (size_t)kMixBatch * w) * sizeof(T2);
     pb(PROF_NO_MIX);
     if (tc_path)
-      launch_mix_tc(l, reinterpret_cast<const float*>(chat), no.cst, reinterpret_cast<float*>(ghat), n, w, B,
+      launch_mix_px(l, reinterpret_cast<const float*>(chat), no.cst, reinterpret_cast<float*>(ghat), n, w, B,
                     (float)inv_n2, status, s);
     else
       launch_k(k_mix<T>, dim3(kModes2, (B + kMixBatch - 1) / kMixBatch), dim3(256), msmem, s,
@@ -862,7 +859,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     ++launches;
     if (tc_path && l < 2) {
       pb(PROF_NO_YDIR);
-      launch_ysyn(reinterpret_cast<const float*>(ghat), no.cst, no.Gb, n, w, B, status, s);
+      launch_px_ysyn(reinterpret_cast<const float*>(ghat), no.cst, no.Gb, n, w, B, status, s);
       pe(PROF_NO_YDIR);
       ++launches;
     }
@@ -904,8 +901,8 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
 cudaError_t prepare_no_constants(const NoDev<float>& no, cudaStream_t s) {
   if (!no.tc) return cudaSuccess;
   const float* pk = no.pk;
-  return launch_tc_prep(no.n, no.w, pk + no.L.W1E, pk + no.L.W[0], pk + no.L.W[1], pk + no.L.R[0], pk + no.L.R[1],
-                        pk + no.L.Q, no.F, no.cst, s);
+  return launch_px_prep(no.n, no.w, pk + no.L.W[0], pk + no.L.W[1], pk + no.L.R[0], pk + no.L.R[1], pk + no.L.Q, no.F,
+                        no.cst, s);
 }
 
 template cudaError_t launch_no_forward<float>(const NoDev<float>&, const double*, const double*, double*,

@@ -1,0 +1,1039 @@
+// no_px_kernels.cu — pixel-major tensor-core (tcgen05 / TMEM) SNO layers for the fp32 NO path,
+// n = 64 or n a multiple of 128 up to 512 (BASELINE configs 2-5).
+//
+// One layer (§2.4.2, R7-R11), per system:
+//   u[i][j][o] = sum_c W[o][c] v[i][j][c] + b[o] + n^-2 Re sum_kappa g[o](kappa) e^{+2 pi i kappa.(i,j)/n}
+//   v'         = GELU(u)                               (layers 1-3; layer 4 is folded away)
+//   c'[o](k)   = sum_{i,j} v'[i][j][o] e^{-2 pi i k.(i,j)/n}
+// with the DFTs separable, so that every contraction is a dense GEMM on the tensor cores:
+//   k_px_ysyn   per (system, 128 rows, kappa2 group):  G[i][(q,o)] = Fp[i][(k1,p)] . Gh_kappa2[(k1,p)][(q,o)]
+//   k_px_layer  per tile of 128 pixels (M = pixels, N = channels):
+//                 D1[p][o]  = sum_c V[p][c] W[o][c]                 bypass        (layers 2, 3)
+//                           + sum_k' F[p][k'] G_row(p)[k'][o]       x-synthesis
+//                 epilogue  v' = GELU(D1 + b (+ layer 1's 2-channel lift bypass on the CUDA cores))
+//                           -> the tile in shared memory, bulk-stored as the next layer's V blob
+//                           (layer 3: sum_o (D W4)[o] v'[o] per pixel instead)
+//                 D2[o][k'] = sum_p v'[p][o] F[p][k']               x-analysis (the same smem tile read
+//                           MN-major; n >= 256: accumulated over the row's column blocks)
+//                 epilogue  -> T rows (fp32)
+//   k_px_yan    per (system, 128 (kappa2, o, re|im) rows): C[(k2,o,p)][(k1,x|y)] = sum_i T[i][..] F[i][(k1,x|y)],
+//               complex recombination of lane pairs in the epilogue -> c'[kappa][b][o]
+// Precision: 3xBF16 split (hi*hi + hi*lo + lo*hi, fp32 accumulation), ~1e-5 relative L2 for the NO.
+//
+// k_px_layer is warp-specialised, one CTA per SM over its tiles: warp 0 issues the bulk loads (V
+// tile or layer 1's fp64 r/k, G rows) into a 2-stage ring; warp 1 issues the MMAs (D1 of tile t
+// into one of two TMEM accumulators, then the x-analysis of tile t-1); warps 3-6 run epilogue 1
+// (thread = pixel) and write v' in place into the stage the tile arrived in; warp 2 bulk-stores it
+// and releases the stage; warps 7-10 run epilogue 2 (thread = channel) into T.
+#include <algorithm>
+
+#include "internal.h"
+#include "px_layout.cuh"
+#include "tc_common.cuh"
+
+namespace fcgno {
+
+namespace {
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// GELU(x) = x/2 (1 + erf(x / sqrt 2)) (reading R11), erf by Abramowitz & Stegun 7.1.26 (|error| <=
+// 1.5e-7, two orders below the 3xBF16 operand rounding) evaluated branch-free through erfc.
+__device__ __forceinline__ float gelu_px(float x) {
+  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x), 1.0f));
+  float p = fmaf(1.061405429f, t, -1.453152027f);
+  p = fmaf(p, t, 1.421413741f);
+  p = fmaf(p, t, -0.284496736f);
+  p = fmaf(p, t, 0.254829592f);
+  p *= t;
+  const float pe = p * ex2_approx((x * x) * -0.72134752044448170f);
+  return 0.5f * x * (x >= 0.f ? 2.0f - pe : pe);
+}
+
+// bulk copy shared -> global (async proxy), completion tracked by bulk groups
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(tc::smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ void st_split8(unsigned char* hi, unsigned char* lo, const float* v) {
+  uint4 h, l;
+  tc::split8(v, h, l);
+  *reinterpret_cast<uint4*>(hi) = h;
+  *reinterpret_cast<uint4*>(lo) = l;
+}
+
+__device__ __forceinline__ void store_split8(unsigned char* hi, unsigned char* lo, const float (&v)[8]) {
+  st_split8(hi, lo, v);
+}
+using tc::tmem_ld8;
+
+__host__ __device__ inline uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32u : c <= 64 ? 64u : c <= 128 ? 128u : c <= 256 ? 256u : 512u; }
+
+}  // namespace
+
+// ------------------------------------------------------------------ constant blobs
+struct PxPrepArgs {
+  int n, w;
+  const float* W[2];      // layers 2, 3: [w][w]
+  const float2* Rm[3];    // mixing weights [400][w][cout]
+  const float2* F;        // [n][20] exp(-2 pi i kappa j / n)
+  unsigned char* out;
+};
+
+__global__ void __launch_bounds__(256) k_px_prep(const PxPrepArgs a) {
+  const PxGeom g(a.n, a.w);
+  const PxConst C(g);
+  const int n = a.n, w = a.w;
+  const int nF = g.nF * 128 * 6, nW = 2 * g.NP * g.KCG, nFP = g.nMT * 128 * 6, nFY = 48 * (n / 8);
+  int nMX[3], tot = nF + nW + nFP + nFY;
+  for (int l = 0; l < 3; ++l) { nMX[l] = kModes2 * C.NM[l] * (C.KM / 8); tot += nMX[l]; }
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+    float v[8];
+    unsigned char* dst;
+    uint32_t half, off;
+    int u = t;
+    if (u < nF) {                                  // F[f][p][k'] K-major (M = p, K = k')
+      const int f = u / (128 * 6), rem = u % (128 * 6), p = rem % 128, kg = rem / 128;
+      const int j = n < 128 ? p % n : f * 128 + p;
+      const int row = n < 128 ? p / n : 0;
+      const bool keep = n >= 128 || f == 0 || (f == 1 && row == 0) || (f == 2 && row == 1);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int kp = kg * 8 + q;
+        v[q] = 0.f;
+        if (keep && kp < 2 * kModes) { const float2 z = a.F[(size_t)j * kModes + (kp >> 1)]; v[q] = (kp & 1) ? z.y : z.x; }
+      }
+      dst = a.out + C.F + (size_t)f * 2 * C.f_half; half = C.f_half;
+      off = (uint32_t)(p >> 3) * 768u + (uint32_t)kg * 128u + (uint32_t)(p & 7) * 16u;
+    } else if ((u -= nF) < nW) {                   // W[l][o][c] K-major B (N = o, K = c)
+      const int l = u / (g.NP * g.KCG), rem = u % (g.NP * g.KCG), o = rem % g.NP, cg = rem / g.NP;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = cg * 8 + q;
+        v[q] = (o < w && c < w) ? a.W[l][(size_t)o * w + c] : 0.f;
+      }
+      dst = a.out + C.W[l]; half = C.w_half;
+      off = (uint32_t)(o >> 3) * (uint32_t)(g.KCG * 128) + (uint32_t)cg * 128u + (uint32_t)(o & 7) * 16u;
+    } else if ((u -= nW) < nFP) {                  // Fp[mt][i][(k1, p)] K-major (M = i, K = 48)
+      const int mt = u / (128 * 6), rem = u % (128 * 6), i = rem % 128, kg = rem / 128, row = mt * 128 + i;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int k = kg * 8 + q, k1 = k >> 1;
+        v[q] = 0.f;
+        if (row < n && k1 < kModes) { const float2 z = a.F[(size_t)row * kModes + k1]; v[q] = (k & 1) ? z.y : z.x; }
+      }
+      dst = a.out + C.FP + (size_t)mt * 2 * C.fp_half; half = C.fp_half;
+      off = (uint32_t)(i >> 3) * 768u + (uint32_t)kg * 128u + (uint32_t)(i & 7) * 16u;
+    } else if ((u -= nFP) < nFY) {                 // Fy[i][(k1, x|y)] K-major B (N = 48, K = i)
+      const int nn = u % 48, ig = u / 48, k1 = nn >> 1;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = ig * 8 + q;
+        v[q] = 0.f;
+        if (k1 < kModes) { const float2 z = a.F[(size_t)i * kModes + k1]; v[q] = (nn & 1) ? z.y : z.x; }
+      }
+      dst = a.out + C.FY; half = C.fy_half;
+      off = (uint32_t)(nn >> 3) * (uint32_t)((n / 8) * 128) + (uint32_t)ig * 128u + (uint32_t)(nn & 7) * 16u;
+    } else {                                       // mode-mixing B: row o, K = (c, re|im) = (Rr, Ri)
+      u -= nFY;
+      int l = 0;
+      while (u >= nMX[l]) { u -= nMX[l]; ++l; }
+      const int cout = l < 2 ? w : 1, NM = C.NM[l], KM = C.KM;
+      const int per_mode = NM * (KM / 8), kk = u / per_mode, rem = u % per_mode, nn = rem % NM, kc = rem / NM;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = kc * 4 + q;
+        float rr = 0.f, ri = 0.f;
+        if (c < w && nn < cout) { const float2 R2 = a.Rm[l][((size_t)kk * w + c) * cout + nn]; rr = R2.x; ri = R2.y; }
+        v[2 * q] = rr;
+        v[2 * q + 1] = ri;
+      }
+      dst = a.out + C.MX[l] + (size_t)kk * 2 * C.mx_half[l]; half = C.mx_half[l];
+      off = (uint32_t)(nn >> 3) * (uint32_t)((KM / 8) * 128) + (uint32_t)kc * 128u + (uint32_t)(nn & 7) * 16u;
+    }
+    uint4 h, lo;
+    tc::split8(v, h, lo);
+    *reinterpret_cast<uint4*>(dst + off) = h;
+    *reinterpret_cast<uint4*>(dst + half + off) = lo;
+  }
+}
+
+// ------------------------------------------------------------------ k_px_layer
+constexpr int kPxThreads = 11 * 32;
+constexpr int kPxMaxSys = 4096;
+
+struct PxSmem {
+  uint32_t ST, GS, RK, WB, FB, bias, w1e, dw, bar, tptr, runb, total, stage_bytes, gs_bytes;
+  __host__ __device__ PxSmem(const PxGeom& g, bool first) {
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
+    stage_bytes = 2u * g.stage_half();
+    ST = take(2 * stage_bytes);
+    gs_bytes = (uint32_t)g.RT * 12u * (uint32_t)g.LBO_G;   // per stage: RT rows x [hi 6 k-groups | lo 6]
+    GS = take(2 * gs_bytes);
+    RK = take(first ? 2u * 2048u : 16u);
+    WB = take(first ? 16u : 2u * (uint32_t)g.NP * g.NP * 2u);
+    FB = take((uint32_t)g.nF * 2u * 128u * 48u * 2u);
+    bias = take(128 * 4);
+    w1e = take(256 * 4);
+    dw = take(128 * 4);
+    bar = take(256);
+    tptr = bar + 192;
+    runb = take(kPxMaxSys / 8);
+    total = o;
+    // the x-analysis reads its A (the stage tile, MN-major, M = 128 channels) over 16 channel groups:
+    // rows o >= NP read whatever follows (their results are ignored), which must lie inside the smem
+    const uint32_t reach = ST + stage_bytes + g.stage_half() + 16u * 2048u;
+    if (reach > total) total = reach;
+  }
+};
+
+struct PxLayerArgs {
+  int n, w, B, layer, use_gelu;
+  const double* r; const double* rr; const double* k;   // layer 1 inputs (fp64)
+  const unsigned char* vin;                              // V blobs (layers 2, 3)
+  unsigned char* vout;                                   // V blobs of the next layer (layers 1, 2)
+  const unsigned char* G;                                // G rows
+  float* T;                                              // T rows
+  const unsigned char* cst;                              // PxConst
+  const float* bias;                                     // [w]
+  const float* w1e;                                      // layer 1: lift folded into W1, [w][2]
+  const float* dw;                                       // layer 3: projection (D W4) [w]
+  float* p3;                                             // layer 3: sum_o dw[o] v3[o] per pixel [B][n][n]
+  const int* status;
+};
+
+template <bool FIRST, bool PROJ>
+__global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a) {
+  const PxGeom g(a.n, a.w);
+  const PxConst C(g);
+  const PxSmem L(g, FIRST);
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int n = a.n, N = n * n, w = a.w, NP = g.NP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bar);
+  uint64_t *full = bars, *empty = bars + 2, *d1full = bars + 4, *d1empty = bars + 6, *vfull = bars + 8,
+           *d2full = bars + 10, *d2empty = bars + 12, *cstb = bars + 14;
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
+  float* sbias = reinterpret_cast<float*>(sm + L.bias);
+  float* sw1e = reinterpret_cast<float*>(sm + L.w1e);
+  float* sdw = reinterpret_cast<float*>(sm + L.dw);
+  uint32_t* runb = reinterpret_cast<uint32_t*>(sm + L.runb);
+  const int nunits = a.B * g.units;
+  const bool cached = a.status && a.B <= kPxMaxSys;
+  const uint32_t ncols = pow2_cols(2u * NP + 2u * g.D2W);
+
+  // ---- prologue (overlaps the predecessor's tail under programmatic dependent launch)
+  if (tid == 0) {
+    // full, d1full, d2full, cstb: one arrival (expect_tx / MMA commit); empty: MMA commit + storer;
+    // d1empty, vfull, d2empty: the 128 epilogue threads
+    for (int q = 0; q < 15; ++q) {
+      const bool epi = (q >= 6 && q < 10) || (q >= 12 && q < 14);
+      tc::mbar_init(&bars[q], epi ? 128u : (q == 2 || q == 3) ? 2u : 1u);
+    }
+    tc::fence_mbar_init();
+    const uint32_t fbytes = (uint32_t)g.nF * 2u * C.f_half;
+    tc::mbar_expect_tx(cstb, fbytes + (FIRST ? 0u : 2u * C.w_half));
+    tc::bulk_g2s(sm + L.FB, a.cst + C.F, fbytes, cstb);
+    if (!FIRST) tc::bulk_g2s(sm + L.WB, a.cst + C.W[a.layer - 1], 2u * C.w_half, cstb);
+  }
+  {   // stages and G stages zeroed: padding channel groups and k-group 5 (k' 40..47) must read as zeros
+    uint4* z = reinterpret_cast<uint4*>(sm + L.ST);
+    for (uint32_t t = tid; t < (2u * L.stage_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
+    z = reinterpret_cast<uint4*>(sm + L.GS);
+    for (uint32_t t = tid; t < (2u * L.gs_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
+  }
+  for (int o = tid; o < 128; o += blockDim.x) {
+    sbias[o] = o < w ? a.bias[o] : 0.f;
+    if (FIRST) { sw1e[2 * o] = o < w ? a.w1e[2 * o] : 0.f; sw1e[2 * o + 1] = o < w ? a.w1e[2 * o + 1] : 0.f; }
+    if (PROJ) sdw[o] = o < w ? a.dw[o] : 0.f;
+  }
+  if (cached)
+    for (int q = warp; q < (a.B + 31) / 32; q += blockDim.x / 32) {
+      const int sb = q * 32 + lane;
+      const unsigned bits = __ballot_sync(0xffffffffu, sb < a.B && __ldcg(a.status + sb) == SYS_RUNNING);
+      if (lane == 0) runb[q] = bits;
+    }
+  if (warp == 0) tc::tmem_alloc(tptr, ncols);
+  tc::fence_proxy_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tptr;
+  pdl_wait();
+  pdl_trigger();
+
+  auto running = [&](int u) {
+    const int b = u / g.units;
+    if (!a.status) return true;
+    if (cached) return ((runb[b >> 5] >> (b & 31)) & 1u) != 0;
+    return __ldcg(a.status + b) == SYS_RUNNING;
+  };
+  auto next_unit = [&](int u) {
+    while (u < nunits && !running(u)) u += gridDim.x;
+    return u;
+  };
+
+  if (warp == 0) {
+    // ================= producer: bulk loads of the tile inputs into the 2-stage ring
+    if (lane == 0) {
+      int t = 0;
+      for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x)) {
+        const int b = u / g.units, ul = u % g.units;
+        for (int cb = 0; cb < g.CB; ++cb, ++t) {
+          const int s = t & 1;
+          const uint32_t ph = (uint32_t)(t >> 1) & 1u;
+          tc::mbar_wait(&empty[s], ph ^ 1u);
+          const int tt = ul * g.CB + cb;
+          tc::mbar_expect_tx(&full[s], (uint32_t)g.RT * 2u * g.g_half() + (FIRST ? 2048u : 2u * g.v_half()));
+          unsigned char* st = sm + L.ST + (uint32_t)s * L.stage_bytes;
+          if (FIRST) {
+            const size_t e = (size_t)b * N + (size_t)tt * 128;
+            tc::bulk_g2s(sm + L.RK + s * 2048, a.r + e, 1024u, &full[s]);
+            tc::bulk_g2s(sm + L.RK + s * 2048 + 1024, a.k + e, 1024u, &full[s]);
+          } else {
+            const unsigned char* src = a.vin + ((size_t)b * g.TPS + tt) * 2 * g.v_half();
+            tc::bulk_g2s(st, src, g.v_half(), &full[s]);
+            tc::bulk_g2s(st + g.stage_half(), src + g.v_half(), g.v_half(), &full[s]);
+          }
+          for (int r = 0; r < g.RT; ++r) {
+            const unsigned char* gsrc = a.G + ((size_t)b * n + ul * g.RT + r) * 2 * g.g_half();
+            unsigned char* gdst = sm + L.GS + (uint32_t)s * L.gs_bytes + (uint32_t)r * 12u * g.LBO_G;
+            tc::bulk_g2s(gdst, gsrc, g.g_half(), &full[s]);
+            tc::bulk_g2s(gdst + 6u * g.LBO_G, gsrc + g.g_half(), g.g_half(), &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (one thread)
+    if (lane == 0) {
+      tc::mbar_wait(cstb, 0);
+      const uint32_t id1 = tc::make_idesc_bf16(128, NP, false, false);   // V (K-major) . W (K-major)
+      const uint32_t id2 = tc::make_idesc_bf16(128, NP, false, true);    // F (K-major) . G (MN-major)
+      const uint32_t id3 = tc::make_idesc_bf16(128, 48, true, true);     // v'^T (MN-major) . F (MN-major)
+      const uint32_t base = tc::smem_u32(sm);
+      const uint32_t sth0 = base + L.ST, fb0 = base + L.FB, gs0 = base + L.GS, wb0 = base + L.WB;
+      const uint32_t sh = g.stage_half(), fh = C.f_half, LG = (uint32_t)g.LBO_G, KCG = (uint32_t)g.KCG;
+      // x-analysis of tile tq (its v' is in stage tq & 1) into D2 buffer uiq & 1
+      auto issue_d3 = [&](int tq, int cbq, int uiq) {
+        const int s = tq & 1, b2 = uiq & 1;
+        tc::mbar_wait(&vfull[s], (uint32_t)(tq >> 1) & 1u);
+        if (cbq == 0) tc::mbar_wait(&d2empty[b2], ((uint32_t)(uiq >> 1) & 1u) ^ 1u);
+        tc::fence_after_sync();
+        const uint32_t sth = sth0 + (uint32_t)s * L.stage_bytes, stl = sth + sh;
+        const uint32_t d2 = tmem + 2u * NP + (uint32_t)b2 * g.D2W;
+        if (g.RT == 2) {        // two rows: pixels 0-63 -> columns [0, 48), pixels 64-127 -> [48, 96)
+          for (int r = 0; r < 2; ++r)
+            for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+              for (int p = 0; p < 3; ++p) {
+                const int kk = r * 4 + ks;
+                const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)kk * 256u;
+                const uint32_t bb = fb0 + (p == 1 ? fh : 0u) + (uint32_t)kk * 2u * 768u;
+                tc::mma_bf16(d2 + (uint32_t)r * 48u, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3,
+                             (ks | p) != 0);
+              }
+        } else {
+          const uint32_t fbc = fb0 + (uint32_t)cbq * 2u * fh;
+          for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+            for (int p = 0; p < 3; ++p) {
+              const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)ks * 256u;
+              const uint32_t bb = fbc + (p == 1 ? fh : 0u) + (uint32_t)ks * 2u * 768u;
+              tc::mma_bf16(d2, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3, (cbq | ks | p) != 0);
+            }
+        }
+        tc::mma_commit(&empty[s]);                       // stage tq consumed by the MMAs
+        if (cbq == g.CB - 1) tc::mma_commit(&d2full[b2]);
+      };
+      int t = 0, ui = 0, pt = -1, pcb = 0, pui = 0;
+      for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x), ++ui) {
+        for (int cb = 0; cb < g.CB; ++cb, ++t) {
+          const int s = t & 1;
+          const uint32_t ph = (uint32_t)(t >> 1) & 1u;
+          tc::mbar_wait(&full[s], ph);
+          tc::mbar_wait(&d1empty[s], ph ^ 1u);
+          tc::fence_after_sync();
+          const uint32_t d1 = tmem + (uint32_t)s * NP;
+          const uint32_t sth = sth0 + (uint32_t)s * L.stage_bytes, stl = sth + sh;
+          uint32_t acc = 0;
+          if (!FIRST) {   // bypass: K = channels, 16 per step
+            for (uint32_t ks = 0; ks < KCG / 2; ++ks)
+#pragma unroll
+              for (int p = 0; p < 3; ++p) {
+                const uint32_t aa = (p == 2 ? stl : sth) + ks * 4096u;
+                const uint32_t bb = wb0 + (p == 1 ? C.w_half : 0u) + ks * 256u;
+                tc::mma_bf16(d1, tc::make_sdesc(aa, 2048, 128), tc::make_sdesc(bb, 128, KCG * 128u), id1, acc);
+                acc = 1;
+              }
+          }
+          const uint32_t gsb = gs0 + (uint32_t)s * L.gs_bytes;
+          for (int r = 0; r < g.RT; ++r) {   // x-synthesis: K = k' (40 of 48), per row of the tile
+            const uint32_t fbr = fb0 + (uint32_t)(g.RT == 2 ? 1 + r : cb) * 2u * fh;
+            const uint32_t gh = gsb + (uint32_t)r * 12u * LG, gl = gh + 6u * LG;
+            for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+              for (int p = 0; p < 3; ++p) {
+                const uint32_t aa = fbr + (p == 2 ? fh : 0u) + (uint32_t)ks * 256u;
+                const uint32_t bb = (p == 1 ? gl : gh) + (uint32_t)ks * 2u * LG;
+                tc::mma_bf16(d1, tc::make_sdesc(aa, 128, 768), tc::make_sdesc(bb, LG, 128), id2, acc);
+                acc = 1;
+              }
+          }
+          tc::mma_commit(&d1full[s]);
+          if (pt >= 0) issue_d3(pt, pcb, pui);
+          pt = t; pcb = cb; pui = ui;
+        }
+      }
+      if (pt >= 0) issue_d3(pt, pcb, pui);
+    }
+  } else if (warp == 2) {
+    // ================= storer: v' tile -> next layer's V blob, then release the stage
+    if (lane == 0) {
+      int t = 0;
+      for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x)) {
+        const int b = u / g.units, ul = u % g.units;
+        for (int cb = 0; cb < g.CB; ++cb, ++t) {
+          const int s = t & 1;
+          tc::mbar_wait(&vfull[s], (uint32_t)(t >> 1) & 1u);
+          if (!PROJ) {
+            const unsigned char* st = sm + L.ST + (uint32_t)s * L.stage_bytes;
+            unsigned char* dst = a.vout + ((size_t)b * g.TPS + ul * g.CB + cb) * 2 * g.v_half();
+            bulk_s2g(dst, st, g.v_half());
+            bulk_s2g(dst + g.v_half(), st + g.stage_half(), g.v_half());
+            bulk_commit();
+            bulk_wait_read0();
+          }
+          tc::mbar_arrive(&empty[s]);
+        }
+      }
+      bulk_wait0();
+    }
+  } else if (warp <= 6) {
+    // ================= epilogue 1: thread = pixel p of the tile (TMEM lane p)
+    const int q4 = warp & 3, p = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    const uint32_t poff = (uint32_t)(p >> 3) * 128u + (uint32_t)(p & 7) * 16u;
+    int t = 0;
+    for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x)) {
+      const int b = u / g.units, ul = u % g.units;
+      float rh = 0.f, kf = 0.f;
+      double inv_s = 0.0;
+      if (FIRST) {
+        const double sr = sqrt(a.rr[b]);
+        inv_s = sr > 0.0 ? 1.0 / sr : 0.0;
+      }
+      for (int cb = 0; cb < g.CB; ++cb, ++t) {
+        const int s = t & 1;
+        const uint32_t ph = (uint32_t)(t >> 1) & 1u;
+        tc::mbar_wait(&d1full[s], ph);
+        tc::fence_after_sync();
+        if (FIRST) {   // the lift's 2-channel bypass W1 (E [r/||r||, k] + bE) on the CUDA cores
+          tc::mbar_wait(&full[s], ph);
+          const double* rk = reinterpret_cast<const double*>(sm + L.RK + s * 2048);
+          rh = (float)(rk[p] * inv_s);
+          kf = (float)rk[128 + p];
+        }
+        unsigned char* sth = sm + L.ST + (uint32_t)s * L.stage_bytes;
+        unsigned char* stl = sth + g.stage_half();
+        float pacc = 0.f;
+        for (int c0 = 0; c0 < NP; c0 += 16) {
+          uint32_t uu[16];
+          tc::tmem_ld16(tmem + (uint32_t)s * NP + lane_off + (uint32_t)c0, uu);
+          tc::tmem_wait_ld();
+          float v[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int o = c0 + q;
+            float x = __uint_as_float(uu[q]) + sbias[o];
+            if (FIRST) x = fmaf(sw1e[2 * o], rh, fmaf(sw1e[2 * o + 1], kf, x));
+            v[q] = a.use_gelu ? gelu_px(x) : x;
+            if (PROJ) pacc = fmaf(sdw[o], v[q], pacc);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t off = (uint32_t)(c0 / 8 + h) * 2048u + poff;
+            st_split8(sth + off, stl + off, v + 8 * h);
+          }
+        }
+        tc::fence_before_sync();
+        tc::mbar_arrive(&d1empty[s]);
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&vfull[s]);
+        if (PROJ) a.p3[(size_t)b * N + (size_t)(ul * g.CB + cb) * 128 + p] = pacc;
+      }
+    }
+  } else {
+    // ================= epilogue 2: thread = channel o (TMEM lane o) -> T rows [kappa2][o][re|im]
+    const int q4 = warp & 3, o = q4 * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    int ui = 0;
+    for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x), ++ui) {
+      const int b = u / g.units, ul = u % g.units, b2 = ui & 1;
+      tc::mbar_wait(&d2full[b2], (uint32_t)(ui >> 1) & 1u);
+      tc::fence_after_sync();
+      for (int r = 0; r < g.RT; ++r) {
+        uint32_t v[48];
+        const uint32_t col = tmem + 2u * NP + (uint32_t)b2 * g.D2W + (uint32_t)r * 48u + lane_off;
+        tc::tmem_ld16(col, *reinterpret_cast<uint32_t(*)[16]>(v));
+        tc::tmem_ld16(col + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+        tc::tmem_ld16(col + 32, *reinterpret_cast<uint32_t(*)[16]>(v + 32));
+        tc::tmem_wait_ld();
+        if (o < w) {
+          float2* dst = reinterpret_cast<float2*>(a.T + ((size_t)b * n + ul * g.RT + r) * 40 * w) + o;
+#pragma unroll
+          for (int k2 = 0; k2 < kModes; ++k2)
+            dst[(size_t)k2 * w] = make_float2(__uint_as_float(v[2 * k2]), __uint_as_float(v[2 * k2 + 1]));
+        }
+      }
+      tc::fence_before_sync();
+      tc::mbar_arrive(&d2empty[b2]);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(tmem, ncols);
+}
+
+// ------------------------------------------------------------------ k_px_ysyn: y-synthesis
+// Item = (system b, M tile of 128 rows i, group of KG consecutive kappa2).  For each kappa2 the B
+// operand Gh[(k1, p)][(q, o)] (K = 48, N = 2 NP) is built from the mixed spectrum g[kappa][b][o]:
+//   rows (k1, 0): (gr | gi),  rows (k1, 1): (gi | -gr)    so that  D[i][(q,o)] = (Gr | Gi)[i][kappa2][o]
+// with Fp[i][(k1,0)] = cos, Fp[i][(k1,1)] = -sin: Gr = sum gr cos - gi sin, Gi = sum gi cos + gr sin
+// (g e^{+i theta}).  The epilogue writes the G rows' bf16 hi/lo chunks of k' = 2 kappa2 + q.
+struct PxYsynSmem {
+  uint32_t A, Bb, bar, tptr, total, b_half;
+  __host__ __device__ PxYsynSmem(const PxGeom& g) {
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
+    A = take(2u * 128u * 48u * 2u);
+    b_half = 2u * (uint32_t)g.NP * 48u * 2u;
+    Bb = take(2u * 2u * b_half);
+    bar = take(64);
+    tptr = bar + 32;
+    total = o;
+  }
+};
+
+__global__ void __launch_bounds__(256, 1) k_px_ysyn(const float2* __restrict__ ghat, const unsigned char* __restrict__ cst,
+                                                    unsigned char* __restrict__ Gb, int n, int w, int B, int kg,
+                                                    const int* __restrict__ status) {
+  const PxGeom g(n, w);
+  const PxConst C(g);
+  const PxYsynSmem L(g);
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int NP = g.NP, N2 = 2 * NP, nkg = kModes / kg;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0], [1] MMA into D buffer; [2] A landed
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
+  const int nitems = B * g.nMT * nkg;
+  const uint32_t LBO_B = (uint32_t)(N2 / 8) * 128u, ncols = pow2_cols(2u * N2);
+  auto next_item = [&](int it) {
+    while (it < nitems && status && status[it / (g.nMT * nkg)] != SYS_RUNNING) it += gridDim.x;
+    return it;
+  };
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
+    tc::fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tptr, ncols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tptr;
+  const uint32_t base = tc::smem_u32(sm);
+  const uint32_t id = tc::make_idesc_bf16(128, N2, false, false);
+  pdl_wait();
+  pdl_trigger();
+  uint32_t cnt = 0, aph = 0;   // MMA groups issued by this CTA; A loads
+  for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + gridDim.x)) {
+    const int b = it / (g.nMT * nkg), mt = (it / nkg) % g.nMT, k20 = (it % nkg) * kg;
+    if (tid == 0) {
+      tc::mbar_expect_tx(&bar[2], 2u * C.fp_half);
+      tc::bulk_g2s(sm + L.A, cst + C.FP + (size_t)mt * 2 * C.fp_half, 2u * C.fp_half, &bar[2]);
+    }
+    const int i = mt * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    unsigned char* grow = Gb + ((size_t)b * n + (i < n ? i : 0)) * 2 * g.g_half();
+    for (int kk = 0; kk <= kg; ++kk) {
+      const uint32_t c = cnt + (uint32_t)kk;
+      if (kk < kg) {   // B for kappa2 = k20 + kk into buffer c & 1
+        const int k2 = k20 + kk;
+        unsigned char* bh = sm + L.Bb + (c & 1u) * 2u * L.b_half;
+        for (int t = tid; t < N2 * 6; t += blockDim.x) {
+          const int nn = t % N2, kgp = t / N2, q = nn / NP, o = nn % NP;
+          float v[8];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k1 = kgp * 4 + e;
+            float2 gg = make_float2(0.f, 0.f);
+            if (k1 < kModes && o < w) gg = __ldg(ghat + ((size_t)(k1 * kModes + k2) * B + b) * w + o);
+            v[2 * e] = q == 0 ? gg.x : gg.y;
+            v[2 * e + 1] = q == 0 ? gg.y : -gg.x;
+          }
+          const uint32_t off = (uint32_t)(nn >> 3) * 128u + (uint32_t)kgp * LBO_B + (uint32_t)(nn & 7) * 16u;
+          st_split8(bh + off, bh + L.b_half + off, v);
+        }
+      }
+      tc::fence_proxy_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      tc::fence_after_sync();
+      if (kk < kg && tid == 0) {
+        if (kk == 0) { tc::mbar_wait(&bar[2], aph); }
+        tc::fence_after_sync();
+        const uint32_t bh = base + L.Bb + (c & 1u) * 2u * L.b_half, bl = bh + L.b_half;
+        const uint32_t ah = base + L.A, al = ah + C.fp_half;
+        const uint32_t d = tmem + (c & 1u) * (uint32_t)N2;
+        for (int ks = 0; ks < 3; ++ks)
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            const uint32_t aa = (p == 2 ? al : ah) + (uint32_t)ks * 256u;
+            const uint32_t bb = (p == 1 ? bl : bh) + (uint32_t)ks * 2u * LBO_B;
+            tc::mma_bf16(d, tc::make_sdesc(aa, 128, 768), tc::make_sdesc(bb, LBO_B, 128), id, (ks | p) != 0);
+          }
+        tc::mma_commit(&bar[c & 1u]);
+      }
+      if (kk >= 1) {   // epilogue of kappa2 = k20 + kk - 1 (buffer (c - 1) & 1)
+        const uint32_t cp = c - 1u;
+        tc::mbar_wait(&bar[cp & 1u], (cp >> 1) & 1u);
+        tc::fence_after_sync();
+        const int k2 = k20 + kk - 1;
+        const uint32_t kp = (uint32_t)(2 * k2 + half);
+        const uint32_t koff = (kp >> 3) * (uint32_t)g.LBO_G + (kp & 7u) * 16u;
+        for (int o0 = 0; o0 < NP; o0 += 16) {
+          uint32_t uu[16];
+          tc::tmem_ld16(tmem + (cp & 1u) * (uint32_t)N2 + lane_off + (uint32_t)(half * NP + o0), uu);
+          tc::tmem_wait_ld();
+          if (i < n) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(uu[8 * h + e]);
+              const uint32_t off = (uint32_t)((o0 >> 3) + h) * 128u + koff;
+              st_split8(grow + off, grow + g.g_half() + off, v);
+            }
+          }
+        }
+      }
+    }
+    cnt += (uint32_t)kg;
+    aph ^= 1u;
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(tmem, ncols);
+}
+
+// ------------------------------------------------------------------ k_px_yan: y-analysis
+// Item = (system b, M tile of 128 rows m = (kappa2 w + o) 2 + (re|im) of the T rows), K = i in chunks
+// of 32 rows converted fp32 -> bf16 hi/lo (MN-major A) into a double buffer while the previous
+// chunk's MMAs run.  B = F[i][(k1, x|y)], resident.  Epilogue: lane pairs (re, im) recombine
+//   c_r = T_r.Fx - T_i.Fy,  c_i = T_i.Fx + T_r.Fy      (e^{-i theta} = Fx + i Fy).
+constexpr int kYanKC = 32;
+struct PxYanSmem {
+  uint32_t A, Bf, bar, tptr, total;
+  __host__ __device__ PxYanSmem(const PxGeom& g) {
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
+    A = take(2u * 2u * 128u * kYanKC * 2u);
+    Bf = take(2u * (uint32_t)g.n * 48u * 2u);
+    bar = take(64);
+    tptr = bar + 32;
+    total = o;
+  }
+};
+
+__global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, const unsigned char* __restrict__ cst,
+                                                float2* __restrict__ chat, int n, int w, int B,
+                                                const int* __restrict__ status) {
+  const PxGeom g(n, w);
+  const PxConst C(g);
+  const PxYanSmem L(g);
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0], [1] MMA of A buffer; [2] B landed
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
+  const int nitems = B * g.MYT, nK = n / kYanKC, M = 40 * w;
+  const uint32_t a_half = 128u * kYanKC * 2u, SBO_Y = (uint32_t)(n / 8) * 128u;
+  auto next_item = [&](int it) {
+    while (it < nitems && status && status[it / g.MYT] != SYS_RUNNING) it += gridDim.x;
+    return it;
+  };
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
+    tc::fence_mbar_init();
+    tc::mbar_expect_tx(&bar[2], 2u * C.fy_half);
+    tc::bulk_g2s(sm + L.Bf, cst + C.FY, 2u * C.fy_half, &bar[2]);
+  }
+  if (warp == 0) tc::tmem_alloc(tptr, 64);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tptr;
+  const uint32_t base = tc::smem_u32(sm);
+  const uint32_t id = tc::make_idesc_bf16(128, 48, true, false);
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) tc::mbar_wait(&bar[2], 0);
+  uint32_t cnt = 0;   // K chunks issued by this CTA
+  for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + gridDim.x)) {
+    const int b = it / g.MYT, m0 = (it % g.MYT) * 128;
+    const float* Tb = T + (size_t)b * n * M + m0;
+    for (int kc = 0; kc <= nK; ++kc) {
+      const uint32_t c = cnt + (uint32_t)kc;
+      if (kc < nK) {
+        if (c >= 2) tc::mbar_wait(&bar[c & 1u], ((c - 2u) >> 1) & 1u);   // MMA c - 2 done with this buffer
+        unsigned char* ah = sm + L.A + (c & 1u) * 2u * a_half;
+        for (int t = tid; t < kYanKC * 16; t += blockDim.x) {
+          const int il = t >> 4, mg = t & 15;
+          const float4* src = reinterpret_cast<const float4*>(Tb + (size_t)(kc * kYanKC + il) * M + mg * 8);
+          const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
+          const float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+          const uint32_t off = (uint32_t)mg * 128u + (uint32_t)(il >> 3) * 2048u + (uint32_t)(il & 7) * 16u;
+          st_split8(ah + off, ah + a_half + off, v);
+        }
+      }
+      tc::fence_proxy_async_smem();
+      tc::fence_before_sync();
+      __syncthreads();
+      tc::fence_after_sync();
+      if (kc < nK && tid == 0) {
+        const uint32_t ah = base + L.A + (c & 1u) * 2u * a_half, al = ah + a_half;
+        const uint32_t bh = base + L.Bf, bl = bh + C.fy_half;
+        for (int ks = 0; ks < kYanKC / 16; ++ks)
+#pragma unroll
+          for (int p = 0; p < 3; ++p) {
+            const uint32_t aa = (p == 2 ? al : ah) + (uint32_t)ks * 4096u;
+            const uint32_t bb = (p == 1 ? bl : bh) + (uint32_t)((kc * kYanKC + ks * 16) / 8) * 128u;
+            tc::mma_bf16(tmem, tc::make_sdesc(aa, 2048, 128), tc::make_sdesc(bb, 128, SBO_Y), id, (kc | ks | p) != 0);
+          }
+        tc::mma_commit(&bar[c & 1u]);
+      }
+    }
+    // epilogue: all of this item's MMAs complete (the last commit covers the earlier ones)
+    const uint32_t cl = cnt + (uint32_t)nK - 1u;
+    tc::mbar_wait(&bar[cl & 1u], (cl >> 1) & 1u);
+    tc::fence_after_sync();
+    if (warp < 4) {
+      uint32_t v[48];
+      const uint32_t col = tmem + ((uint32_t)(warp * 32) << 16);
+      tc::tmem_ld16(col, *reinterpret_cast<uint32_t(*)[16]>(v));
+      tc::tmem_ld16(col + 16, *reinterpret_cast<uint32_t(*)[16]>(v + 16));
+      tc::tmem_ld16(col + 32, *reinterpret_cast<uint32_t(*)[16]>(v + 32));
+      tc::tmem_wait_ld();
+      const int m = m0 + warp * 32 + lane, pr = m >> 1, k2 = pr / w, o = pr - k2 * w;
+      const bool re = (lane & 1) == 0;
+#pragma unroll
+      for (int k1 = 0; k1 < kModes; ++k1) {
+        const float x = __uint_as_float(v[2 * k1]), y = __uint_as_float(v[2 * k1 + 1]);
+        const float px = __shfl_xor_sync(0xffffffffu, x, 1), py = __shfl_xor_sync(0xffffffffu, y, 1);
+        if (re && m < M) chat[((size_t)(k1 * kModes + k2) * B + b) * w + o] = make_float2(x - py, px + y);
+      }
+    }
+    cnt += (uint32_t)nK;
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (warp == 0) tc::tmem_dealloc(tmem, 64);
+}
+
+// ------------------------------------------------------------------ mode-diagonal mixing on tensor cores
+// per mode kappa: G[b][(o, re|im)] = sum_{(c, re|im)} C[b][(c, re|im)] * R'[(c, re|im)][(o, re|im)] / n^2,
+// R' the 2x2-real form of R[c][o](kappa) (prebuilt per mode); M = systems (<= 128 per item).
+struct MixSmem {
+  uint32_t A, B, bar, tptr, total;
+  __host__ __device__ MixSmem(int KM, int NM) {
+    uint32_t o = 0;
+    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
+    A = take(2u * 128 * KM * 2);
+    B = take(2u * NM * KM * 2);
+    bar = take(64);
+    tptr = bar + 32;
+    total = o;
+  }
+};
+
+// Mode-diagonal mixing, one work item = (mode kappa, 64 systems).  The complex product
+// g[b][o] = sum_c c[b][c] R[c][o] runs as one real GEMM with two A rows per system,
+//   row 2b   = (cr, -ci) per channel  ->  D = sum_c cr Rr - ci Ri = gr
+//   row 2b+1 = (ci,  cr) per channel  ->  D = sum_c ci Rr + cr Ri = gi
+// against B = (Rr, Ri) per channel (k_tc_prep), so the weight blob and N are not doubled.
+constexpr int kMixSys = 64;   // systems per work item (2 A rows each)
+
+__global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat, const unsigned char* __restrict__ mx,
+                                               float2* __restrict__ ghat, int w, int B, int cout, float inv_n2,
+                                               const int* status) {
+  const int KM = (2 * w + 15) & ~15, NM = (cout + 15) & ~15;
+  const MixSmem L(KM, NM);
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const uint32_t SBO = (KM / 8) * 128, a_half = 128u * KM * 2, b_half = (uint32_t)NM * KM * 2;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0] B load, [1] MMA
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nbc = (B + kMixSys - 1) / kMixSys, nitems = kModes2 * nbc;
+  auto prefetch = [&](int it) {
+    const int kk = it / nbc;
+    tc::mbar_expect_tx(&bar[0], 2 * b_half);
+    tc::bulk_g2s(sm + L.B, mx + (size_t)kk * 2 * b_half, 2 * b_half, &bar[0]);
+  };
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::fence_mbar_init();
+    if ((int)blockIdx.x < nitems) prefetch(blockIdx.x);   // weights do not depend on the predecessor
+  }
+  const uint32_t ncols = NM <= 32 ? 32u : (NM <= 64 ? 64u : 128u);
+  if (warp == 0) tc::tmem_alloc(tptr, ncols);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tptr;
+  const uint32_t id = tc::make_idesc_bf16(128, NM, false, false);
+  const uint32_t base = tc::smem_u32(sm);
+  pdl_wait();
+  pdl_trigger();
+  uint32_t ph = 0;
+  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    const int kk = it / nbc, b0 = (it % nbc) * kMixSys, nb = min(kMixSys, B - b0);
+    // A: rows (b, re|im), K = (c, re|im); all loads of a batch first
+    {
+      constexpr int kBatch = 8;
+      const int ntask = kMixSys * (KM / 8);
+      for (int t0 = tid; t0 < ntask; t0 += kBatch * blockDim.x) {
+        float2 x[kBatch][4];
+#pragma unroll
+        for (int z = 0; z < kBatch; ++z) {
+          const int t = t0 + z * blockDim.x, bl = t % kMixSys, kc = t / kMixSys;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int c = kc * 4 + q;
+            x[z][q] = (t < ntask && bl < nb && c < w) ? __ldg(chat + ((size_t)kk * B + b0 + bl) * w + c)
+                                                      : make_float2(0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int z = 0; z < kBatch; ++z) {
+          const int t = t0 + z * blockDim.x, bl = t % kMixSys, kc = t / kMixSys;
+          if (t >= ntask) break;
+          float vr[8], vi[8];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            vr[2 * q] = x[z][q].x;  vr[2 * q + 1] = -x[z][q].y;
+            vi[2 * q] = x[z][q].y;  vi[2 * q + 1] = x[z][q].x;
+          }
+          const uint32_t offr = tc::kmajor_off(2 * bl, kc * 8, SBO, 128), offi = tc::kmajor_off(2 * bl + 1, kc * 8, SBO, 128);
+          store_split8(sm + L.A + offr, sm + L.A + a_half + offr, vr);
+          store_split8(sm + L.A + offi, sm + L.A + a_half + offi, vi);
+        }
+      }
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    if (tid == 0) {
+      tc::mbar_wait(&bar[0], ph);
+      tc::fence_after_sync();
+      uint32_t acc = 0;
+      for (int s = 0; s < KM / 16; ++s)
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+          const uint32_t aa = base + L.A + (p == 2 ? a_half : 0u) + 256u * s, bb = base + L.B + (p == 1 ? b_half : 0u) + 256u * s;
+          tc::mma_bf16(tmem, tc::make_sdesc(aa, 128, SBO), tc::make_sdesc(bb, 128, SBO), id, acc);
+          acc = 1;
+        }
+      tc::mma_commit(&bar[1]);
+    }
+    tc::mbar_wait(&bar[1], ph);
+    tc::fence_after_sync();
+    if (tid == 0 && it + (int)gridDim.x < nitems) prefetch(it + gridDim.x);   // B consumed
+    {
+      // lane pair (2bl, 2bl+1) holds (gr, gi) of system bl: swap halves of each 8-column chunk so the
+      // even lane writes o in [c0, c0+4) and the odd lane o in [c0+4, c0+8) as float2 runs
+      const int row = warp * 32 + lane, bl = row >> 1, p = row & 1, b = b0 + bl;
+      const bool ok = bl < nb && (!status || status[b] == SYS_RUNNING);
+      for (int c0 = 0; c0 < cout; c0 += 8) {
+        uint32_t u[8];
+        tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c0, u);
+        tc::tmem_wait_ld();
+        float mine[4], other[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float keep = __uint_as_float(u[p ? 4 + q : q]);      // my half
+          const float give = __uint_as_float(u[p ? q : 4 + q]);      // partner's half
+          mine[q] = keep;
+          other[q] = __shfl_xor_sync(0xffffffffu, give, 1);
+        }
+        if (ok) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int o = c0 + 4 * p + q;
+            if (o < cout) {
+              const float gr = p ? other[q] : mine[q], gi = p ? mine[q] : other[q];
+              ghat[((size_t)kk * B + b) * cout + o] = make_float2(gr * inv_n2, gi * inv_n2);
+            }
+          }
+        }
+      }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    ph ^= 1;
+  }
+  tc::fence_after_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, ncols);
+}
+
+// ------------------------------------------------------------------ host side
+static int px_optin() {
+  static int v = -1;
+  if (v < 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+      v = 0;
+  }
+  return v;
+}
+static int px_sms() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+constexpr uint32_t kPxSmemLimit = 227u * 1024u;
+
+bool px_supported_shape(int n, int w) {
+  if (w < 1 || w > 128) return false;
+  if (!(n == 64 || (n % 128 == 0 && n >= 128 && n <= 512))) return false;
+  const PxGeom g(n, w);
+  return PxSmem(g, true).total <= kPxSmemLimit && PxSmem(g, false).total <= kPxSmemLimit &&
+         PxYsynSmem(g).total <= kPxSmemLimit && PxYanSmem(g).total <= kPxSmemLimit;
+}
+
+bool px_supported(int n, int w) { return px_supported_shape(n, w) && px_optin() >= (int)kPxSmemLimit; }
+
+size_t px_const_bytes(int n, int w) { return PxConst(PxGeom(n, w)).total; }
+size_t px_v_bytes(int n, int w, int B) { return PxGeom(n, w).v_bytes(B); }
+size_t px_g_bytes(int n, int w, int B) { return PxGeom(n, w).g_bytes(B); }
+size_t px_t_floats(int n, int w, int B) { return PxGeom(n, w).t_floats(B); }
+size_t px_mx_offset(int n, int w, int mix) { return PxConst(PxGeom(n, w)).MX[mix]; }
+
+cudaError_t prepare_px_kernels() {
+  static bool done = false;
+  if (done) return cudaSuccess;
+  const void* fns[6] = {(const void*)k_px_layer<true, false>, (const void*)k_px_layer<false, false>,
+                        (const void*)k_px_layer<false, true>, (const void*)k_px_ysyn, (const void*)k_px_yan,
+                        (const void*)k_px_layer<true, true>};
+  for (const void* f : fns) {
+    const cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPxSmemLimit);
+    if (e != cudaSuccess) return e;
+  }
+  done = true;
+  return cudaSuccess;
+}
+
+cudaError_t launch_px_prep(int n, int w, const float* W2, const float* W3, const float* R2, const float* R3,
+                           const float* Q, const float* F, unsigned char* out, cudaStream_t s) {
+  PxPrepArgs a{};
+  a.n = n; a.w = w; a.W[0] = W2; a.W[1] = W3;
+  a.Rm[0] = reinterpret_cast<const float2*>(R2); a.Rm[1] = reinterpret_cast<const float2*>(R3);
+  a.Rm[2] = reinterpret_cast<const float2*>(Q);
+  a.F = reinterpret_cast<const float2*>(F);
+  a.out = out;
+  k_px_prep<<<2 * px_sms(), 256, 0, s>>>(a);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_px_layer(const PxLayerHost& h, cudaStream_t s) {
+  PxLayerArgs a{};
+  a.n = h.n; a.w = h.w; a.B = h.B; a.layer = h.layer; a.use_gelu = h.use_gelu;
+  a.r = h.r; a.rr = h.rr; a.k = h.k; a.vin = h.vin; a.vout = h.vout; a.G = h.G; a.T = h.T; a.cst = h.cst;
+  a.bias = h.bias; a.w1e = h.w1e; a.dw = h.dw; a.p3 = h.p3; a.status = h.status;
+  const PxGeom g(h.n, h.w);
+  const bool first = h.layer == 0, proj = h.layer == 2;
+  const size_t smem = PxSmem(g, first).total;
+  const int grid = std::min(h.B * g.units, px_sms());
+  if (first) return launch_k(k_px_layer<true, false>, dim3(grid), dim3(kPxThreads), smem, s, a);
+  if (proj) return launch_k(k_px_layer<false, true>, dim3(grid), dim3(kPxThreads), smem, s, a);
+  return launch_k(k_px_layer<false, false>, dim3(grid), dim3(kPxThreads), smem, s, a);
+}
+
+cudaError_t launch_px_ysyn(const float* ghat, const unsigned char* cst, unsigned char* Gb, int n, int w, int B,
+                           const int* status, cudaStream_t s) {
+  const PxGeom g(n, w);
+  const int sms = px_sms();
+  // kappa2 groups per (system, M tile): enough items to cover the SMs twice where possible
+  const int base_items = B * g.nMT;
+  int kg = 1;
+  for (int cand : {20, 10, 5, 4, 2})
+    if (base_items * (kModes / cand) >= sms) { kg = cand; break; }
+  const PxYsynSmem L(g);
+  const int items = base_items * (kModes / kg);
+  const int by_tmem = (int)(512u / pow2_cols(4u * (uint32_t)g.NP));
+  const int per_sm = std::max(1, std::min(by_tmem, (int)((228u * 1024u) / (L.total + 1024u))));
+  const int grid = std::min(items, per_sm * sms);
+  return launch_k(k_px_ysyn, dim3(grid), dim3(256), (size_t)L.total, s, reinterpret_cast<const float2*>(ghat), cst, Gb,
+                  n, w, B, kg, status);
+}
+
+cudaError_t launch_px_yan(const float* T, const unsigned char* cst, float* chat, int n, int w, int B, const int* status,
+                          cudaStream_t s) {
+  const PxGeom g(n, w);
+  const PxYanSmem L(g);
+  const int items = B * g.MYT;
+  const int per_sm = std::max(1, std::min(3, (int)((228u * 1024u) / (L.total + 1024u))));
+  const int grid = std::min(items, per_sm * px_sms());
+  return launch_k(k_px_yan, dim3(grid), dim3(256), (size_t)L.total, s, T, cst, reinterpret_cast<float2*>(chat), n, w,
+                  B, status);
+}
+
+
+cudaError_t launch_mix_px(int mix, const float* chat, const unsigned char* cst, float* ghat, int n, int w, int B,
+                          float inv_n2, const int* status, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute((const void*)k_mix_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int cout = mix < 2 ? w : 1, KM = (2 * w + 15) & ~15, NM = (cout + 15) & ~15;
+  const size_t smem = MixSmem(KM, NM).total;
+  const int nitems = kModes2 * ((B + kMixSys - 1) / kMixSys);
+  const int per_sm = std::max(1, std::min(3, (int)((228u * 1024u) / (smem + 1024u))));
+  const int grid = std::min(nitems, per_sm * px_sms());
+  return launch_k(k_mix_tc, dim3(grid), dim3(128), smem, s, reinterpret_cast<const float2*>(chat),
+                  cst + px_mx_offset(n, w, mix), reinterpret_cast<float2*>(ghat), w, B, cout, inv_n2, status);
+}
+
+}  // namespace fcgno

@@ -528,15 +528,12 @@ def _solve_in_subprocess(env_extra, tag, maxit=12, batch=64):
 
 
 def test_opt_in_paths_match_default(lib):
-    # Opt-in variants compute the same per-system arithmetic as the default path:
-    #   FCGNO_LANES=2  -- the batch as two parallel graph branches (systems never interact): bitwise;
-    #   FCGNO_TC_WS=1  -- pipelined two-group layer kernel, same MMA and epilogue arithmetic: bitwise.
+    # Opt-in variant computing the same per-system arithmetic as the default path:
+    #   FCGNO_LANES=2  -- the batch as two parallel graph branches (systems never interact): bitwise.
     u0, h0 = _solve_in_subprocess({}, "default")
     u1, h1 = _solve_in_subprocess({"FCGNO_LANES": "2"}, "lanes")
-    u2, h2 = _solve_in_subprocess({"FCGNO_TC_WS": "1"}, "ws")
-    assert np.isfinite(u0).all() and h0.shape == h1.shape == h2.shape
+    assert np.isfinite(u0).all() and h0.shape == h1.shape
     assert np.array_equal(u0, u1) and np.array_equal(h0, h1, equal_nan=True)
-    assert np.array_equal(u0, u2) and np.array_equal(h0, h2, equal_nan=True)
 
 
 # ----------------------------------------------------------------------------- Notay ratio (NEXT-2)
