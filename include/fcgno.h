@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FCGNO_ABI_VERSION 4
+#define FCGNO_ABI_VERSION 5
 #define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
 #define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
 #define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
@@ -189,6 +189,34 @@ FCGNO_API int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* d_or_
                     const double* f, double* u, fcgno_solve_opts o, int32_t* iters,
                     int32_t* status, double* history, void* ws, size_t ws_bytes, void* stream);
 
+/* fcg_solve with Theorem-1 diagnostics (Theorem 1, Eq. final_loss; SURVEY
+ * §8(f) NEXT-2): as fcgno_fcg_solve, and at every iteration i < iters[b] of a running system, after
+ * w_i = B(r_i), with e_i = u_star - u_i (u_i the iterate; u_star a caller-supplied reference solution,
+ * e.g. a tight FCG(I) solve, so that e_i approximates A^{-1} r_i):
+ *   eps  [B][maxit] device or NULL: eps[b][i]   = ||w_i - e_i||_A / ||e_i||_A  (direct form)
+ *   err_a[B][maxit] device or NULL: err_a[b][i] = ||e_i||_A
+ * (at least one of them non-NULL).  Adds a state kernel, two stencil applications, two correctly
+ * rounded inner products and a scalar kernel per iteration.  profile_mask must be 0.
+ *   u_star   [B][n][n] fp64 device.  ws: fcgno_solve_diag_workspace_bytes(g, d_or_null, o) bytes. */
+FCGNO_API size_t fcgno_solve_diag_workspace_bytes(fcgno_grid g, const fcgno_no_desc* d_or_null, fcgno_solve_opts o);
+FCGNO_API int fcgno_fcg_solve_diag(const fcgno_problem* p, const fcgno_no_desc* d_or_null, const void* packed,
+                         const double* f, double* u, fcgno_solve_opts o, int32_t* iters, int32_t* status,
+                         double* history, const double* u_star, double* eps, double* err_a, void* ws,
+                         size_t ws_bytes, void* stream);
+
+/* Notay ratio of one preconditioner application (PAPER.md Eq. final_loss), per system:
+ *   eps[b] = || c B(r_b) - e_b ||_A / || e_b ||_A,   ||v||_A = sqrt((v, A v)),
+ * B the NO (d_or_null != NULL) or the identity, e = A^{-1} r supplied by the caller, c = 1, or with
+ * optimal_scale != 0 the minimiser c* = (B(r), A e) / (B(r), A B(r)) (FCG's iterates do not depend on
+ * the scale of B).  Direct form: d = c B(r) - e is formed first, then ||d||_A and ||e||_A, each from
+ * one stencil application and one correctly rounded inner product (R6), in the order of
+ * oracle/notay.py.
+ *   r, e [B][n][n] fp64 device; eps [B] fp64 device; ws: fcgno_notay_workspace_bytes(g, d_or_null). */
+FCGNO_API size_t fcgno_notay_workspace_bytes(fcgno_grid g, const fcgno_no_desc* d_or_null);
+FCGNO_API int fcgno_notay_ratio(const fcgno_problem* p, const fcgno_no_desc* d_or_null, const void* packed,
+                      const double* r, const double* e, int optimal_scale, double* eps, void* ws,
+                      size_t ws_bytes, void* stream);
+
 /* End-to-end convenience entry point with HOST buffers ([host], pageable or pinned): copies
  * k, f, u0 to the device, assembles, solves and copies u, iters, status (and history if
  * non-NULL) back.  `dev_ws` is a device workspace of fcgno_solve_host_workspace_bytes bytes;
@@ -205,6 +233,10 @@ FCGNO_API int fcgno_solve_host(fcgno_grid g, const double* k_host, const double*
 FCGNO_API int fcgno_profile_get(int cls, double* total_ms, int64_t* launches);
 FCGNO_API void fcgno_profile_reset(void);
 FCGNO_API const char* fcgno_profile_name(int cls);
+
+/* Diagnostics: the clock64 stamps of the tensor-core layer pipeline events of CTA 0's first 64 tiles
+ * of the last layer launch selected by FCGNO_PX_TRACE=<layer 1..3> ([tile][10] uint64, host). */
+FCGNO_API int fcgno_debug_px_trace(uint64_t* host, int count);
 
 /* Number of kernel launches the library issued in this process (diagnostics, bench.py). */
 FCGNO_API uint64_t fcgno_kernel_launches(void);

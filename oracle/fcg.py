@@ -48,8 +48,10 @@ def _round32(x):
     return np.asarray(x, dtype=np.float64).astype(np.float32).astype(np.float64)
 
 
-def fcg(apply_A, f, u0, m_max, tol, maxit, precond=None, schedule="paper", vec32=False):
+def fcg(apply_A, f, u0, m_max, tol, maxit, precond=None, schedule="paper", vec32=False, observe=None):
     """Algorithm 1 for one system.  apply_A(x) -> A x; precond(r) -> w (None = identity).
+    observe(i, w_i, u_i), when given, is called at every iteration after w_i = B(r_i) (diagnostics:
+    oracle/notay.py notay_curve); it does not change the iteration.
 
     vec32 (reading R21, SURVEY C.2 #28 "vectors and ring in fp32, dots accumulated in fp64"): the
     residual r, the preconditioned residual w and the stored directions p, s are kept in fp32; each
@@ -69,6 +71,8 @@ def fcg(apply_A, f, u0, m_max, tol, maxit, precond=None, schedule="paper", vec32
         w = r.copy() if precond is None else st(np.asarray(precond(r), dtype=np.float64))
         if not np.all(np.isfinite(w)):
             return dict(u=u, r=r, hist=np.array(hist), iters=i, status=NONFINITE)
+        if observe is not None:
+            observe(i, w, u)
         mi = m_schedule(i, m_max, schedule)
         window = list(range(len(P) - mi, len(P)))
         betas = {kk: dot(w, S[kk]) / G[kk] for kk in window}

@@ -16,6 +16,7 @@ import math
 import numpy as np
 
 from .dots import dot
+from .fcg import fcg
 
 
 def a_norm(apply_A, v) -> float:
@@ -37,3 +38,20 @@ def notay_ratio_scaled(apply_A, w, e) -> float:
     e = np.asarray(e, dtype=np.float64)
     c = dot(w, apply_A(e)) / dot(w, apply_A(w))
     return a_norm(apply_A, c * w - e) / a_norm(apply_A, e)
+
+
+def notay_curve(apply_A, f, u0, u_star, m_max, tol, maxit, precond=None, schedule="paper", vec32=False):
+    """Theorem 1's quantities along Algorithm 1 (Fig. 2/4's curves):
+    at every iteration i, after w_i = B(r_i), with e_i = u_star - u_i (u_star a reference solution, so
+    that e_i approximates A^{-1} r_i):
+      eps[i]   = ||w_i - e_i||_A / ||e_i||_A   (notay_ratio, Eq. final_loss's integrand)
+      err_a[i] = ||e_i||_A
+    Returns (fcg result dict, eps array, err_a array), both of length iters."""
+    eps, err = [], []
+
+    def observe(i, w, u):
+        e = np.asarray(u_star, dtype=np.float64) - u
+        eps.append(notay_ratio(apply_A, w, e))
+        err.append(a_norm(apply_A, e))
+    res = fcg(apply_A, f, u0, m_max, tol, maxit, precond=precond, schedule=schedule, vec32=vec32, observe=observe)
+    return res, np.array(eps), np.array(err)

@@ -423,6 +423,61 @@ int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, 
   return FCGNO_OK;
 }
 
+// ------------------------------------------------------------------ Notay ratio (Theorem-1 diagnostic)
+size_t fcgno_notay_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd) {
+  if (g.n < 2 || g.batch < 1 || (nd && check_desc(*nd) != FCGNO_OK)) return 0;
+  Carver c(nullptr);
+  const size_t BN = (size_t)g.batch * g.n * g.n;
+  for (int t = 0; t < 5; ++t) c.take<double>(BN);
+  c.take<double>((size_t)5 * g.batch);
+  c.take<dd>((size_t)g.batch * nblk_of(g.n));
+  c.take<unsigned>(g.batch);
+  if (nd) c.take<unsigned char>(fcgno_apply_no_workspace_bytes(g, *nd));
+  return c.bytes();
+}
+
+int fcgno_notay_ratio(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* r,
+                      const double* e, int optimal_scale, double* eps, void* ws, size_t ws_bytes, void* stream) {
+  if (!p || !r || !e || !eps || !ws || (nd && !packed)) return fail(FCGNO_EINVAL, "notay_ratio: NULL argument");
+  fcgno_grid g{p->n, p->B};
+  if (!aligned(ws) || ws_bytes < fcgno_notay_workspace_bytes(g, nd)) return fail(FCGNO_EWORKSPACE, "notay_ratio: workspace");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  const size_t BN = (size_t)p->B * p->n * p->n;
+  double* wv = c.take<double>(BN);
+  double* Ae = c.take<double>(BN);
+  double* Aw = c.take<double>(BN);
+  double* dv = c.take<double>(BN);
+  double* Ad = c.take<double>(BN);
+  double* sc = c.take<double>((size_t)5 * p->B);   // (e,Ae), (w,Aw), (w,Ae), c, (d,Ad)
+  dd* part = c.take<dd>((size_t)p->B * nblk_of(p->n));
+  unsigned* cnt = c.take<unsigned>(p->B);
+  const int B = p->B, n = p->n;
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * B, s));
+  const double* w = r;                               // identity: B(r) = r
+  if (nd) {
+    const size_t nb = fcgno_apply_no_workspace_bytes(g, *nd);
+    unsigned char* nws = c.take<unsigned char>(nb);
+    if (int rc = fcgno_apply_NO(p, *nd, packed, r, wv, nws, nb, stream)) return rc;
+    w = wv;
+  }
+  CK(launch_apply_A(p->k, e, Ae, n, B, p->kfast, s));
+  CK(launch_dot(e, Ae, sc, part, cnt, n, B, s));
+  const double* coef = nullptr;
+  if (optimal_scale) {   // c* = (w, A e) / (w, A w)
+    CK(launch_apply_A(p->k, w, Aw, n, B, p->kfast, s));
+    CK(launch_dot(w, Aw, sc + B, part, cnt, n, B, s));
+    CK(launch_dot(w, Ae, sc + 2 * B, part, cnt, n, B, s));
+    CK(launch_notay_coef(sc + 2 * B, sc + B, sc + 3 * B, B, s));
+    coef = sc + 3 * B;
+  }
+  CK(launch_notay_form(w, e, coef, dv, n, B, s));
+  CK(launch_apply_A(p->k, dv, Ad, n, B, p->kfast, s));
+  CK(launch_dot(dv, Ad, sc + 4 * B, part, cnt, n, B, s));
+  CK(launch_notay_final(sc + 4 * B, sc, eps, nullptr, nullptr, 1, nullptr, B, s));
+  return FCGNO_OK;
+}
+
 // ------------------------------------------------------------------ fcg_solve
 namespace {
 struct SolveWs {
@@ -432,7 +487,7 @@ struct SolveWs {
   double* wvec;
 };
 
-SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgno_solve_opts& o) {
+SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgno_solve_opts& o, bool diag = false) {
   SolveWs s{};
   const size_t N = (size_t)n * n;
   const int nblk = nblk_of(n);
@@ -460,6 +515,15 @@ SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgn
   d.iter = c.take<int>(2);
   d.active = d.iter + 1;
   if (nd) carve_no_any(c, n, B, *nd, &s.n32, &s.n64);
+  if (diag) {   // Theorem-1 diagnostics scratch (fcgno_fcg_solve_diag)
+    d.dg_e = c.take<double>(B * N);
+    d.dg_d = c.take<double>(B * N);
+    d.dg_Ae = c.take<double>(B * N);
+    d.dg_Ad = c.take<double>(B * N);
+    d.dg_sc = c.take<double>((size_t)2 * B);
+    d.dg_part = c.take<dd>((size_t)B * nblk);
+    d.dg_cnt = c.take<unsigned>(B);
+  }
   return s;
 }
 
@@ -554,6 +618,11 @@ int enqueue_iteration(const FcgDev& d, const fcgno_no_desc* nd, const void* pack
     if (launch_window_dots(d, s) != cudaSuccess) return -1;
     pe(PROF_WINDOW);
     ++count;
+  }
+  if (d.dg_ustar) {   // Theorem-1 diagnostics of w_i = B(r_i) (fcgno_fcg_solve_diag)
+    const int nd_l = enqueue_diag(d, s);
+    if (nd_l < 0) return -1;
+    count += nd_l;
   }
   pb(PROF_STENCIL);
   if (launch_pform_stencil(d, s) != cudaSuccess) return -1;
@@ -721,18 +790,50 @@ bool host_loop_forced() {
 }
 }  // namespace
 
-size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd, fcgno_solve_opts o) {
+namespace {
+struct DiagArgs { const double* u_star; double* eps; double* err_a; };
+
+size_t solve_ws_bytes(fcgno_grid g, const fcgno_no_desc* nd, const fcgno_solve_opts& o, bool diag) {
   if (g.n < 2 || g.batch < 1 || check_opts(o) != FCGNO_OK) return 0;
   if (nd && check_desc(*nd) != FCGNO_OK) return 0;
   Carver c(nullptr);
   const LaneSplit L = lane_split(g.batch);
-  for (int l = 0; l < L.n; ++l) carve_solve(c, g.n, L.nb[l], nd, o);
+  for (int l = 0; l < L.n; ++l) carve_solve(c, g.n, L.nb[l], nd, o, diag);
   return c.bytes();
+}
+
+int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* f, double* u,
+               fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, const DiagArgs* dg, void* ws,
+               size_t ws_bytes, void* stream);
+}  // namespace
+
+size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd, fcgno_solve_opts o) {
+  return solve_ws_bytes(g, nd, o, false);
+}
+
+size_t fcgno_solve_diag_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd, fcgno_solve_opts o) {
+  return solve_ws_bytes(g, nd, o, true);
 }
 
 int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* f, double* u,
                     fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, void* ws, size_t ws_bytes,
                     void* stream) {
+  return solve_impl(p, nd, packed, f, u, o, iters, status, history, nullptr, ws, ws_bytes, stream);
+}
+
+int fcgno_fcg_solve_diag(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* f,
+                         double* u, fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history,
+                         const double* u_star, double* eps, double* err_a, void* ws, size_t ws_bytes, void* stream) {
+  if (!u_star || (!eps && !err_a)) return fail(FCGNO_EINVAL, "fcg_solve_diag: u_star and eps or err_a are required");
+  if (o.profile_mask) return fail(FCGNO_EINVAL, "fcg_solve_diag: profiling is not available with diagnostics");
+  const DiagArgs dg{u_star, eps, err_a};
+  return solve_impl(p, nd, packed, f, u, o, iters, status, history, &dg, ws, ws_bytes, stream);
+}
+
+namespace {
+int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* f, double* u,
+               fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, const DiagArgs* dg, void* ws,
+               size_t ws_bytes, void* stream) {
   if (!p || !f || !u || !iters || !status || !ws) return fail(FCGNO_EINVAL, "fcg_solve: NULL argument");
   if (int e = check_opts(o)) return e;
   if (nd) {
@@ -742,7 +843,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     if (int e = check_no_smem(*nd, p->n)) return e;
   }
   fcgno_grid g{p->n, p->B};
-  if (!aligned(ws) || ws_bytes < fcgno_solve_workspace_bytes(g, nd, o)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
+  if (!aligned(ws) || ws_bytes < solve_ws_bytes(g, nd, o, dg != nullptr)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
   if (nd) {
     if (nd->precision == FCGNO_FP64) CK(prepare_no_kernels<double>());
     else { CK(prepare_no_kernels<float>()); CK(prepare_px_kernels()); }
@@ -761,7 +862,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     ln.p.k = p->k + b0 * N;
     if (p->khat32) ln.p.khat32 = p->khat32 + (size_t)b0 * kModes2 * 2;
     if (p->khat64) ln.p.khat64 = p->khat64 + (size_t)b0 * kModes2 * 2;
-    ln.sw = carve_solve(c, p->n, nb, nd, o);
+    ln.sw = carve_solve(c, p->n, nb, nd, o, dg != nullptr);
     FcgDev& d = ln.sw.d;
     d.n = p->n; d.B = nb; d.N = p->n * p->n; d.nblk = nblk_of(p->n);
     d.m = o.m; d.maxit = o.maxit; d.schedule = o.schedule; d.tol = o.tol;
@@ -769,6 +870,11 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
     d.k = ln.p.k; d.kfast = p->kfast ? 1 : 0; d.f = f + b0 * N; d.u = u + b0 * N; d.w = nd ? ln.sw.wvec : d.r;
     d.status = status + b0; d.iters = iters + b0;
     d.hist = history ? history + (size_t)b0 * (o.maxit + 1) : nullptr;
+    if (dg) {
+      d.dg_ustar = dg->u_star + b0 * N;
+      d.dg_eps = dg->eps ? dg->eps + (size_t)b0 * o.maxit : nullptr;
+      d.dg_erra = dg->err_a ? dg->err_a + (size_t)b0 * o.maxit : nullptr;
+    }
   }
 
   // Private streams (graph capture is not allowed on the legacy default stream), ordered after
@@ -812,6 +918,7 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
       const SolveWs& sw = lanes[l].sw;
       if ((e = cudaMemsetAsync(d.cnt, 0, sizeof(unsigned) * (3 * d.B + 2), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if ((e = cudaMemsetAsync(d.iter, 0, 2 * sizeof(int), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
+      if (d.dg_cnt && (e = cudaMemsetAsync(d.dg_cnt, 0, sizeof(unsigned) * d.B, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if (nd && sw.n32.Gb) {   // tensor-core constant operands (every blob byte the kernels read is written by them)
         NoDev<float> no = make_nodev<float>(&lanes[l].p, *nd, packed, sw.n32, p->F32, lanes[l].p.khat32);
         if ((e = prepare_no_constants(no, s)) != cudaSuccess) { rc = cuda_fail(e, "tc constants"); break; }
@@ -908,6 +1015,13 @@ int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* nd, const void*
   // order the caller's stream after the solve (resources are released by `res`)
   if (cudaEventRecord(ev_in, s) == cudaSuccess) cudaStreamWaitEvent(caller, ev_in, 0);
   return rc;
+}
+}  // namespace
+
+int fcgno_debug_px_trace(uint64_t* host, int count) {
+  if (!host || count < 0) return fail(FCGNO_EINVAL, "debug_px_trace: bad arguments");
+  CK(px_trace_read(reinterpret_cast<unsigned long long*>(host), count));
+  return FCGNO_OK;
 }
 
 int fcgno_profile_get(int cls, double* total_ms, int64_t* launches) {

@@ -42,6 +42,14 @@ struct FcgDev {
   int* iter;                  // global iteration counter
   int* active;                // systems still running (set by init, then by the last update CTA)
   unsigned* gcnt;             // [2] systems arrived in this update / of them still running
+  // Theorem-1 diagnostics (fcgno_fcg_solve_diag; all nullptr otherwise)
+  const double* dg_ustar;     // [B][N] reference solution u*
+  double* dg_eps;             // [B][maxit] eps_i = ||w_i - e_i||_A / ||e_i||_A
+  double* dg_erra;            // [B][maxit] ||e_i||_A, e_i = u* - u_i
+  double *dg_e, *dg_d, *dg_Ae, *dg_Ad;   // [B][N] scratch
+  double* dg_sc;              // [2][B] (e, A e), (d, A d)
+  dd* dg_part;                // [B][nblk] dot partials
+  unsigned* dg_cnt;           // [B] dot counters
 };
 
 // Packed NO weights (element offsets into the packed array of T; complex = 2 T).
@@ -107,6 +115,7 @@ cudaError_t launch_px_ysyn(const float* ghat, const unsigned char* cst, unsigned
                            const int* status, cudaStream_t s);
 cudaError_t launch_px_yan(const float* T, const unsigned char* cst, float* chat, int n, int w, int B, const int* status,
                           cudaStream_t s);
+cudaError_t px_trace_read(unsigned long long* host, int count);
 cudaError_t launch_mix_px(int mix, const float* chat, const unsigned char* cst, float* ghat, int n, int w, int B,
                           float inv_n2, const int* status, cudaStream_t s);
 
@@ -148,6 +157,13 @@ template <typename T>
 size_t no_max_smem(int n, int w);   // largest dynamic smem any NO kernel needs for (n, w)
 
 uint64_t& launch_counter();
+
+// Theorem-1 / Notay diagnostics (diag_kernels.cu)
+cudaError_t launch_notay_form(const double* w, const double* e, const double* c, double* d, int n, int B, cudaStream_t s);
+cudaError_t launch_notay_coef(const double* wAe, const double* wAw, double* c, int B, cudaStream_t s);
+cudaError_t launch_notay_final(const double* dAd, const double* eAe, double* eps, double* err_a, const int* iter,
+                               size_t stride, const int* status, int B, cudaStream_t s);
+int enqueue_diag(const FcgDev& d, cudaStream_t s);
 
 // Launch with programmatic stream serialization (PDL), unless FCGNO_PDL=0.
 bool pdl_enabled();

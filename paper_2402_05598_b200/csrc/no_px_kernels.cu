@@ -21,11 +21,14 @@
 // Precision: 3xBF16 split (hi*hi + hi*lo + lo*hi, fp32 accumulation), ~1e-5 relative L2 for the NO.
 //
 // k_px_layer is warp-specialised, one CTA per SM over its tiles: warp 0 issues the bulk loads (V
-// tile or layer 1's fp64 r/k, G rows) into a 2-stage ring; warp 1 issues the MMAs (D1 of tile t
-// into one of two TMEM accumulators, then the x-analysis of tile t-1); warps 3-6 run epilogue 1
-// (thread = pixel) and write v' in place into the stage the tile arrived in; warp 2 bulk-stores it
-// and releases the stage; warps 7-10 run epilogue 2 (thread = channel) into T.
+// tile or layer 1's fp64 r/k; G rows by TMA tensor copy) into a 2-stage ring; warp 1 issues the MMAs
+// (D1 of tile t into one of two TMEM accumulators, then the x-analysis of tile t-1); warps 3-14 run
+// epilogue 1 (three warpgroups splitting the channel columns, thread = pixel) and write v' in place
+// into the stage the tile arrived in; warp 2 bulk-stores it and releases the stage; warps 15-18 run
+// epilogue 2 (thread = channel) into T.
 #include <algorithm>
+
+#include <cuda.h>
 
 #include "internal.h"
 #include "px_layout.cuh"
@@ -172,31 +175,59 @@ __global__ void __launch_bounds__(256) k_px_prep(const PxPrepArgs a) {
 }
 
 // ------------------------------------------------------------------ k_px_layer
-constexpr int kPxThreads = 11 * 32;
+// Diagnostics (FCGNO_PX_TRACE=<layer 1..3>): clock64 stamps of the pipeline events of CTA 0's first
+// kPxTraceTiles tiles, read back with fcgno_debug_px_trace (scripts/px_trace.py).
+constexpr int kPxTraceTiles = 64, kPxTraceEv = 10;
+__device__ unsigned long long g_px_trace[kPxTraceTiles * kPxTraceEv];
+#define PX_TRACE(t, ev)                                                                  \
+  do {                                                                                   \
+    if (a.trace && blockIdx.x == 0 && (t) < kPxTraceTiles)                               \
+      g_px_trace[(t) * kPxTraceEv + (ev)] = clock64();                                   \
+  } while (0)
+constexpr int kPxE1Groups = 3;                                 // epilogue-1 warpgroups (column split)
+constexpr int kPxE1Warps = 4 * kPxE1Groups;
+// warp roles: 0 V loads, 1 D1 MMAs, 2 G loads, 3 x-analysis MMAs, 4-15 epilogue 1, 16-19 epilogue 2
+constexpr int kPxE1First = 4, kPxE2First = kPxE1First + kPxE1Warps;
+constexpr int kPxThreads = (kPxE2First + 4) * 32;
 constexpr int kPxMaxSys = 4096;
+constexpr uint32_t kPxSmemLimit = 227u * 1024u;
 
+// Shared-memory plan: NST V stages (the tile's v' is written back in place) and GST G stages, 3 each
+// when they fit the 227 KB opt-in limit, else 2.
 struct PxSmem {
-  uint32_t ST, GS, RK, WB, FB, bias, w1e, dw, bar, tptr, runb, total, stage_bytes, gs_bytes;
+  uint32_t ST, GS, RK, WB, FB, bias, w1e, dw, pj, bar, tptr, runb, total, stage_bytes, gs_bytes;
+  int NST, GST;
   __host__ __device__ PxSmem(const PxGeom& g, bool first) {
+    stage_bytes = 2u * g.stage_half();
+    gs_bytes = (uint32_t)g.RT * 12u * (uint32_t)g.LBO_G;   // per stage: RT rows x [hi 6 k-groups | lo 6]
+    for (NST = 3; NST >= 2; --NST) {
+      for (GST = 3; GST >= 2; --GST) {
+        plan(g, first);
+        if (total <= kPxSmemLimit) return;
+      }
+    }
+    NST = GST = 2;
+    plan(g, first);
+  }
+  __host__ __device__ void plan(const PxGeom& g, bool first) {
     uint32_t o = 0;
     auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
-    stage_bytes = 2u * g.stage_half();
-    ST = take(2 * stage_bytes);
-    gs_bytes = (uint32_t)g.RT * 12u * (uint32_t)g.LBO_G;   // per stage: RT rows x [hi 6 k-groups | lo 6]
-    GS = take(2 * gs_bytes);
-    RK = take(first ? 2u * 2048u : 16u);
+    ST = take((uint32_t)NST * stage_bytes);
+    GS = take((uint32_t)GST * gs_bytes);
+    RK = take(first ? (uint32_t)NST * 2048u : 16u);
     WB = take(first ? 16u : 2u * (uint32_t)g.NP * g.NP * 2u);
     FB = take((uint32_t)g.nF * 2u * 128u * 48u * 2u);
     bias = take(128 * 4);
     w1e = take(256 * 4);
     dw = take(128 * 4);
+    pj = take(3u * kPxE1Groups * 128u * 4u);   // layer 3: per-group projection partials, per stage
     bar = take(256);
-    tptr = bar + 192;
+    tptr = bar + 248;
     runb = take(kPxMaxSys / 8);
     total = o;
-    // the x-analysis reads its A (the stage tile, MN-major, M = 128 channels) over 16 channel groups:
+    // the x-analysis reads its A (a stage tile, MN-major, M = 128 channels) over 16 channel groups:
     // rows o >= NP read whatever follows (their results are ignored), which must lie inside the smem
-    const uint32_t reach = ST + stage_bytes + g.stage_half() + 16u * 2048u;
+    const uint32_t reach = ST + (uint32_t)(NST - 1) * stage_bytes + g.stage_half() + 16u * 2048u;
     if (reach > total) total = reach;
   }
 };
@@ -206,7 +237,7 @@ struct PxLayerArgs {
   const double* r; const double* rr; const double* k;   // layer 1 inputs (fp64)
   const unsigned char* vin;                              // V blobs (layers 2, 3)
   unsigned char* vout;                                   // V blobs of the next layer (layers 1, 2)
-  const unsigned char* G;                                // G rows
+  const unsigned char* G;                                // G (interleaved rows; read by TMA through gmap)
   float* T;                                              // T rows
   const unsigned char* cst;                              // PxConst
   const float* bias;                                     // [w]
@@ -214,19 +245,34 @@ struct PxLayerArgs {
   const float* dw;                                       // layer 3: projection (D W4) [w]
   float* p3;                                             // layer 3: sum_o dw[o] v3[o] per pixel [B][n][n]
   const int* status;
+  int trace;                                             // diagnostics: record g_px_trace
 };
 
+// Pipeline (per CTA, tiles t of its row units in order; s = t % NST, gs = t % GST, d = t % 2):
+//   warp 0  V loads     wait empty[s]   -> bulk-copy V(t) (layer 1: fp64 r, k) into stage s  -> full[s]
+//   warp 2  G loads     wait gempty[gs] -> TMA-gather the tile's G row(s) into G stage gs    -> gfull[gs]
+//   warp 1  D1 MMAs     D1(t) = bypass + x-synthesis into TMEM buffer d once full[s], gfull[gs] and
+//                       d1empty[d] allow (commit -> d1full[d], gempty[gs])
+//   warps 4-15 E1       v' = GELU(D1 + b) -> smem stage s in place (A of the x-analysis) and HBM (next
+//                       layer's V, 16-byte coalesced stores); layer 3: the projection sum instead of HBM
+//                       (-> d1empty[d], vfull[s])
+//   warp 3  D2 MMAs     D2 += x-analysis of tile t once vfull[s] (commit -> empty[s]; last column block
+//                       of the row -> d2full); a second MMA issuer, so the stage is released without
+//                       waiting behind the next tile's D1 instructions
+//   warps 16-19 E2      D2 -> T rows (fp32, coalesced over o)
 template <bool FIRST, bool PROJ>
-__global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a) {
+__global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a, const __grid_constant__ CUtensorMap gmap) {
   const PxGeom g(a.n, a.w);
   const PxConst C(g);
   const PxSmem L(g, FIRST);
+  const int NST = L.NST, GST = L.GST;
   extern __shared__ __align__(1024) unsigned char sm[];
   const int n = a.n, N = n * n, w = a.w, NP = g.NP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bar);
-  uint64_t *full = bars, *empty = bars + 2, *d1full = bars + 4, *d1empty = bars + 6, *vfull = bars + 8,
-           *d2full = bars + 10, *d2empty = bars + 12, *cstb = bars + 14;
+  uint64_t *full = bars, *empty = bars + 3, *vfull = bars + 6, *gfull = bars + 9, *gempty = bars + 12,
+           *d1full = bars + 15, *d1empty = bars + 17, *d2full = bars + 19, *d2empty = bars + 21, *cstb = bars + 23;
+  constexpr int kNumBars = 24;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
   float* sbias = reinterpret_cast<float*>(sm + L.bias);
   float* sw1e = reinterpret_cast<float*>(sm + L.w1e);
@@ -238,11 +284,11 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
 
   // ---- prologue (overlaps the predecessor's tail under programmatic dependent launch)
   if (tid == 0) {
-    // full, d1full, d2full, cstb: one arrival (expect_tx / MMA commit); empty: MMA commit + storer;
-    // d1empty, vfull, d2empty: the 128 epilogue threads
-    for (int q = 0; q < 15; ++q) {
-      const bool epi = (q >= 6 && q < 10) || (q >= 12 && q < 14);
-      tc::mbar_init(&bars[q], epi ? 128u : (q == 2 || q == 3) ? 2u : 1u);
+    // d1empty, vfull: the epilogue-1 threads; d2empty: the 128 epilogue-2 threads; all others one
+    // arrival (expect_tx or an MMA commit)
+    for (int q = 0; q < kNumBars; ++q) {
+      const bool e1 = (q >= 6 && q < 9) || (q >= 17 && q < 19), e2 = q >= 21 && q < 23;
+      tc::mbar_init(&bars[q], e1 ? 32u * kPxE1Warps : e2 ? 128u : 1u);
     }
     tc::fence_mbar_init();
     const uint32_t fbytes = (uint32_t)g.nF * 2u * C.f_half;
@@ -252,9 +298,9 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
   }
   {   // stages and G stages zeroed: padding channel groups and k-group 5 (k' 40..47) must read as zeros
     uint4* z = reinterpret_cast<uint4*>(sm + L.ST);
-    for (uint32_t t = tid; t < (2u * L.stage_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
+    for (uint32_t t = tid; t < ((uint32_t)NST * L.stage_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
     z = reinterpret_cast<uint4*>(sm + L.GS);
-    for (uint32_t t = tid; t < (2u * L.gs_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
+    for (uint32_t t = tid; t < ((uint32_t)GST * L.gs_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
   }
   for (int o = tid; o < 128; o += blockDim.x) {
     sbias[o] = o < w ? a.bias[o] : 0.f;
@@ -286,89 +332,64 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
     while (u < nunits && !running(u)) u += gridDim.x;
     return u;
   };
+  const uint32_t base = tc::smem_u32(sm);
+  const uint32_t sth0 = base + L.ST, fb0 = base + L.FB, gs0 = base + L.GS, wb0 = base + L.WB;
+  const uint32_t sh = g.stage_half(), fh = C.f_half, LG = (uint32_t)g.LBO_G, KCG = (uint32_t)g.KCG;
 
-  if (warp == 0) {
-    // ================= producer: bulk loads of the tile inputs into the 2-stage ring
+  if (warp == 0 || warp == 2) {
+    // ================= producers: V tiles (warp 0) and G rows (warp 2)
     if (lane == 0) {
       int t = 0;
       for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x)) {
         const int b = u / g.units, ul = u % g.units;
         for (int cb = 0; cb < g.CB; ++cb, ++t) {
-          const int s = t & 1;
-          const uint32_t ph = (uint32_t)(t >> 1) & 1u;
-          tc::mbar_wait(&empty[s], ph ^ 1u);
-          const int tt = ul * g.CB + cb;
-          tc::mbar_expect_tx(&full[s], (uint32_t)g.RT * 2u * g.g_half() + (FIRST ? 2048u : 2u * g.v_half()));
-          unsigned char* st = sm + L.ST + (uint32_t)s * L.stage_bytes;
-          if (FIRST) {
-            const size_t e = (size_t)b * N + (size_t)tt * 128;
-            tc::bulk_g2s(sm + L.RK + s * 2048, a.r + e, 1024u, &full[s]);
-            tc::bulk_g2s(sm + L.RK + s * 2048 + 1024, a.k + e, 1024u, &full[s]);
+          if (warp == 0) {
+            const int s = t % NST;
+            tc::mbar_wait(&empty[s], ((uint32_t)(t / NST) & 1u) ^ 1u);
+            PX_TRACE(t, 0);
+            const int tt = ul * g.CB + cb;
+            unsigned char* st = sm + L.ST + (uint32_t)s * L.stage_bytes;
+            if (FIRST) {
+              const size_t e = (size_t)b * N + (size_t)tt * 128;
+              tc::mbar_expect_tx(&full[s], 2048u);
+              tc::bulk_g2s(sm + L.RK + s * 2048, a.r + e, 1024u, &full[s]);
+              tc::bulk_g2s(sm + L.RK + s * 2048 + 1024, a.k + e, 1024u, &full[s]);
+            } else {
+              const unsigned char* src = a.vin + ((size_t)b * g.TPS + tt) * 2 * g.v_half();
+              tc::mbar_expect_tx(&full[s], 2u * g.v_half());
+              tc::bulk_g2s(st, src, g.v_half(), &full[s]);
+              tc::bulk_g2s(st + g.stage_half(), src + g.v_half(), g.v_half(), &full[s]);
+            }
           } else {
-            const unsigned char* src = a.vin + ((size_t)b * g.TPS + tt) * 2 * g.v_half();
-            tc::bulk_g2s(st, src, g.v_half(), &full[s]);
-            tc::bulk_g2s(st + g.stage_half(), src + g.v_half(), g.v_half(), &full[s]);
-          }
-          for (int r = 0; r < g.RT; ++r) {
-            const unsigned char* gsrc = a.G + ((size_t)b * n + ul * g.RT + r) * 2 * g.g_half();
-            unsigned char* gdst = sm + L.GS + (uint32_t)s * L.gs_bytes + (uint32_t)r * 12u * g.LBO_G;
-            tc::bulk_g2s(gdst, gsrc, g.g_half(), &full[s]);
-            tc::bulk_g2s(gdst + 6u * g.LBO_G, gsrc + g.g_half(), g.g_half(), &full[s]);
+            const int gs = t % GST;
+            tc::mbar_wait(&gempty[gs], ((uint32_t)(t / GST) & 1u) ^ 1u);
+            tc::mbar_expect_tx(&gfull[gs], (uint32_t)g.RT * 2u * g.g_half());
+            for (int r = 0; r < g.RT; ++r) {   // G row i: hi and lo boxes of the interleaved layout
+              unsigned char* gdst = sm + L.GS + (uint32_t)gs * L.gs_bytes + (uint32_t)r * 12u * g.LBO_G;
+              const int i = ul * g.RT + r;
+              tc::tma_load_5d(gdst, &gmap, 0, i, 0, 0, 2 * b, &gfull[gs]);
+              tc::tma_load_5d(gdst + 6u * g.LBO_G, &gmap, 0, i, 0, 0, 2 * b + 1, &gfull[gs]);
+            }
           }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (one thread)
+    // ================= D1 MMAs (one thread): bypass + x-synthesis
     if (lane == 0) {
       tc::mbar_wait(cstb, 0);
       const uint32_t id1 = tc::make_idesc_bf16(128, NP, false, false);   // V (K-major) . W (K-major)
       const uint32_t id2 = tc::make_idesc_bf16(128, NP, false, true);    // F (K-major) . G (MN-major)
-      const uint32_t id3 = tc::make_idesc_bf16(128, 48, true, true);     // v'^T (MN-major) . F (MN-major)
-      const uint32_t base = tc::smem_u32(sm);
-      const uint32_t sth0 = base + L.ST, fb0 = base + L.FB, gs0 = base + L.GS, wb0 = base + L.WB;
-      const uint32_t sh = g.stage_half(), fh = C.f_half, LG = (uint32_t)g.LBO_G, KCG = (uint32_t)g.KCG;
-      // x-analysis of tile tq (its v' is in stage tq & 1) into D2 buffer uiq & 1
-      auto issue_d3 = [&](int tq, int cbq, int uiq) {
-        const int s = tq & 1, b2 = uiq & 1;
-        tc::mbar_wait(&vfull[s], (uint32_t)(tq >> 1) & 1u);
-        if (cbq == 0) tc::mbar_wait(&d2empty[b2], ((uint32_t)(uiq >> 1) & 1u) ^ 1u);
-        tc::fence_after_sync();
-        const uint32_t sth = sth0 + (uint32_t)s * L.stage_bytes, stl = sth + sh;
-        const uint32_t d2 = tmem + 2u * NP + (uint32_t)b2 * g.D2W;
-        if (g.RT == 2) {        // two rows: pixels 0-63 -> columns [0, 48), pixels 64-127 -> [48, 96)
-          for (int r = 0; r < 2; ++r)
-            for (int ks = 0; ks < 4; ++ks)
-#pragma unroll
-              for (int p = 0; p < 3; ++p) {
-                const int kk = r * 4 + ks;
-                const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)kk * 256u;
-                const uint32_t bb = fb0 + (p == 1 ? fh : 0u) + (uint32_t)kk * 2u * 768u;
-                tc::mma_bf16(d2 + (uint32_t)r * 48u, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3,
-                             (ks | p) != 0);
-              }
-        } else {
-          const uint32_t fbc = fb0 + (uint32_t)cbq * 2u * fh;
-          for (int ks = 0; ks < 8; ++ks)
-#pragma unroll
-            for (int p = 0; p < 3; ++p) {
-              const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)ks * 256u;
-              const uint32_t bb = fbc + (p == 1 ? fh : 0u) + (uint32_t)ks * 2u * 768u;
-              tc::mma_bf16(d2, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3, (cbq | ks | p) != 0);
-            }
-        }
-        tc::mma_commit(&empty[s]);                       // stage tq consumed by the MMAs
-        if (cbq == g.CB - 1) tc::mma_commit(&d2full[b2]);
-      };
-      int t = 0, ui = 0, pt = -1, pcb = 0, pui = 0;
-      for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x), ++ui) {
+      int t = 0;
+      for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x)) {
         for (int cb = 0; cb < g.CB; ++cb, ++t) {
-          const int s = t & 1;
-          const uint32_t ph = (uint32_t)(t >> 1) & 1u;
-          tc::mbar_wait(&full[s], ph);
-          tc::mbar_wait(&d1empty[s], ph ^ 1u);
+          const int s = t % NST, gs = t % GST, d = t & 1;
+          tc::mbar_wait(&full[s], (uint32_t)(t / NST) & 1u);
+          tc::mbar_wait(&gfull[gs], (uint32_t)(t / GST) & 1u);
+          tc::mbar_wait(&d1empty[d], ((uint32_t)(t >> 1) & 1u) ^ 1u);
+          PX_TRACE(t, 1);
           tc::fence_after_sync();
-          const uint32_t d1 = tmem + (uint32_t)s * NP;
+          const uint32_t d1 = tmem + (uint32_t)d * NP;
           const uint32_t sth = sth0 + (uint32_t)s * L.stage_bytes, stl = sth + sh;
           uint32_t acc = 0;
           if (!FIRST) {   // bypass: K = channels, 16 per step
@@ -381,7 +402,7 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
                 acc = 1;
               }
           }
-          const uint32_t gsb = gs0 + (uint32_t)s * L.gs_bytes;
+          const uint32_t gsb = gs0 + (uint32_t)gs * L.gs_bytes;
           for (int r = 0; r < g.RT; ++r) {   // x-synthesis: K = k' (40 of 48), per row of the tile
             const uint32_t fbr = fb0 + (uint32_t)(g.RT == 2 ? 1 + r : cb) * 2u * fh;
             const uint32_t gh = gsb + (uint32_t)r * 12u * LG, gl = gh + 6u * LG;
@@ -394,38 +415,59 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
                 acc = 1;
               }
           }
-          tc::mma_commit(&d1full[s]);
-          if (pt >= 0) issue_d3(pt, pcb, pui);
-          pt = t; pcb = cb; pui = ui;
+          tc::mma_commit(&d1full[d]);
+          tc::mma_commit(&gempty[gs]);
+          PX_TRACE(t, 2);
         }
       }
-      if (pt >= 0) issue_d3(pt, pcb, pui);
     }
-  } else if (warp == 2) {
-    // ================= storer: v' tile -> next layer's V blob, then release the stage
+  } else if (warp == 3) {
+    // ================= x-analysis MMAs (one thread): D2[o][k'] += sum_p v'[p][o] F[p][k']
     if (lane == 0) {
-      int t = 0;
-      for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x)) {
-        const int b = u / g.units, ul = u % g.units;
+      tc::mbar_wait(cstb, 0);
+      const uint32_t id3 = tc::make_idesc_bf16(128, 48, true, true);     // v'^T (MN-major) . F (MN-major)
+      int t = 0, ui = 0;
+      for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x), ++ui) {
+        const int b2 = ui & 1;
         for (int cb = 0; cb < g.CB; ++cb, ++t) {
-          const int s = t & 1;
-          tc::mbar_wait(&vfull[s], (uint32_t)(t >> 1) & 1u);
-          if (!PROJ) {
-            const unsigned char* st = sm + L.ST + (uint32_t)s * L.stage_bytes;
-            unsigned char* dst = a.vout + ((size_t)b * g.TPS + ul * g.CB + cb) * 2 * g.v_half();
-            bulk_s2g(dst, st, g.v_half());
-            bulk_s2g(dst + g.v_half(), st + g.stage_half(), g.v_half());
-            bulk_commit();
-            bulk_wait_read0();
+          const int s = t % NST;
+          tc::mbar_wait(&vfull[s], (uint32_t)(t / NST) & 1u);
+          if (cb == 0) tc::mbar_wait(&d2empty[b2], ((uint32_t)(ui >> 1) & 1u) ^ 1u);
+          tc::fence_after_sync();
+          const uint32_t sth = sth0 + (uint32_t)s * L.stage_bytes, stl = sth + sh;
+          const uint32_t d2 = tmem + 2u * NP + (uint32_t)b2 * g.D2W;
+          if (g.RT == 2) {        // two rows: pixels 0-63 -> columns [0, 48), pixels 64-127 -> [48, 96)
+            for (int r = 0; r < 2; ++r)
+              for (int ks = 0; ks < 4; ++ks)
+#pragma unroll
+                for (int p = 0; p < 3; ++p) {
+                  const int kk = r * 4 + ks;
+                  const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)kk * 256u;
+                  const uint32_t bb = fb0 + (p == 1 ? fh : 0u) + (uint32_t)kk * 2u * 768u;
+                  tc::mma_bf16(d2 + (uint32_t)r * 48u, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3,
+                               (ks | p) != 0);
+                }
+          } else {
+            const uint32_t fbc = fb0 + (uint32_t)cb * 2u * fh;
+            for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+              for (int p = 0; p < 3; ++p) {
+                const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)ks * 256u;
+                const uint32_t bb = fbc + (p == 1 ? fh : 0u) + (uint32_t)ks * 2u * 768u;
+                tc::mma_bf16(d2, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3, (cb | ks | p) != 0);
+              }
           }
-          tc::mbar_arrive(&empty[s]);
+          tc::mma_commit(&empty[s]);                       // stage t consumed
+          PX_TRACE(t, 5);
+          if (cb == g.CB - 1) tc::mma_commit(&d2full[b2]);
         }
       }
-      bulk_wait0();
     }
-  } else if (warp <= 6) {
-    // ================= epilogue 1: thread = pixel p of the tile (TMEM lane p)
-    const int q4 = warp & 3, p = q4 * 32 + lane;
+  } else if (warp < kPxE2First) {
+    // ================= epilogue 1: thread = pixel p of the tile (TMEM lane p); warpgroup eg takes the
+    // 16-column chunks eg, eg + 3, ... of the NP channels
+    const int q4 = warp & 3, p = q4 * 32 + lane, eg = (warp - kPxE1First) / 4;
+    float* pj = reinterpret_cast<float*>(sm + L.pj);
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const uint32_t poff = (uint32_t)(p >> 3) * 128u + (uint32_t)(p & 7) * 16u;
     int t = 0;
@@ -438,22 +480,23 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
         inv_s = sr > 0.0 ? 1.0 / sr : 0.0;
       }
       for (int cb = 0; cb < g.CB; ++cb, ++t) {
-        const int s = t & 1;
-        const uint32_t ph = (uint32_t)(t >> 1) & 1u;
-        tc::mbar_wait(&d1full[s], ph);
+        const int s = t % NST, d = t & 1;
+        tc::mbar_wait(&d1full[d], (uint32_t)(t >> 1) & 1u);
+        if (lane == 0 && q4 == 0 && eg == 0) PX_TRACE(t, 3);
         tc::fence_after_sync();
         if (FIRST) {   // the lift's 2-channel bypass W1 (E [r/||r||, k] + bE) on the CUDA cores
-          tc::mbar_wait(&full[s], ph);
+          tc::mbar_wait(&full[s], (uint32_t)(t / NST) & 1u);
           const double* rk = reinterpret_cast<const double*>(sm + L.RK + s * 2048);
           rh = (float)(rk[p] * inv_s);
           kf = (float)rk[128 + p];
         }
         unsigned char* sth = sm + L.ST + (uint32_t)s * L.stage_bytes;
         unsigned char* stl = sth + g.stage_half();
+        unsigned char* gv = PROJ ? nullptr : a.vout + ((size_t)b * g.TPS + ul * g.CB + cb) * 2 * g.v_half();
         float pacc = 0.f;
-        for (int c0 = 0; c0 < NP; c0 += 16) {
+        for (int c0 = 16 * eg; c0 < NP; c0 += 16 * kPxE1Groups) {
           uint32_t uu[16];
-          tc::tmem_ld16(tmem + (uint32_t)s * NP + lane_off + (uint32_t)c0, uu);
+          tc::tmem_ld16(tmem + (uint32_t)d * NP + lane_off + (uint32_t)c0, uu);
           tc::tmem_wait_ld();
           float v[16];
 #pragma unroll
@@ -466,15 +509,33 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const uint32_t off = (uint32_t)(c0 / 8 + h) * 2048u + poff;
-            st_split8(sth + off, stl + off, v + 8 * h);
+            const int cg = c0 / 8 + h;
+            const uint32_t off = (uint32_t)cg * 2048u + poff;
+            uint4 hv, lv;
+            tc::split8(v + 8 * h, hv, lv);
+            *reinterpret_cast<uint4*>(sth + off) = hv;
+            *reinterpret_cast<uint4*>(stl + off) = lv;
+            if (!PROJ && cg < g.CGS) {   // the next layer's V blob (16-byte stores, 512 B per warp)
+              *reinterpret_cast<uint4*>(gv + off) = hv;
+              *reinterpret_cast<uint4*>(gv + g.v_half() + off) = lv;
+            }
           }
         }
         tc::fence_before_sync();
-        tc::mbar_arrive(&d1empty[s]);
+        tc::mbar_arrive(&d1empty[d]);
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&vfull[s]);
-        if (PROJ) a.p3[(size_t)b * N + (size_t)(ul * g.CB + cb) * 128 + p] = pacc;
+        if (lane == 0 && q4 == 0) PX_TRACE(t, eg == 0 ? 4 : (eg == 1 ? 9 : 8));
+        if (PROJ) {   // sum_o (D W4)[o] v3[o]: the groups' partials added in a fixed order
+          pj[((size_t)s * kPxE1Groups + eg) * 128 + p] = pacc;
+          tc::named_sync(1, 32u * kPxE1Warps);
+          if (eg == 0) {
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < kPxE1Groups; ++q) acc += pj[((size_t)s * kPxE1Groups + q) * 128 + p];
+            a.p3[(size_t)b * N + (size_t)(ul * g.CB + cb) * 128 + p] = acc;
+          }
+        }
       }
     }
   } else {
@@ -502,6 +563,7 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a)
       }
       tc::fence_before_sync();
       tc::mbar_arrive(&d2empty[b2]);
+      if (lane == 0 && q4 == 0) PX_TRACE(ui, 7);
     }
   }
   tc::fence_before_sync();
@@ -569,7 +631,6 @@ __global__ void __launch_bounds__(256, 1) k_px_ysyn(const float2* __restrict__ g
     }
     const int i = mt * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    unsigned char* grow = Gb + ((size_t)b * n + (i < n ? i : 0)) * 2 * g.g_half();
     for (int kk = 0; kk <= kg; ++kk) {
       const uint32_t c = cnt + (uint32_t)kk;
       if (kk < kg) {   // B for kappa2 = k20 + kk into buffer c & 1
@@ -613,22 +674,24 @@ __global__ void __launch_bounds__(256, 1) k_px_ysyn(const float2* __restrict__ g
         const uint32_t cp = c - 1u;
         tc::mbar_wait(&bar[cp & 1u], (cp >> 1) & 1u);
         tc::fence_after_sync();
-        const int k2 = k20 + kk - 1;
-        const uint32_t kp = (uint32_t)(2 * k2 + half);
-        const uint32_t koff = (kp >> 3) * (uint32_t)g.LBO_G + (kp & 7u) * 16u;
-        for (int o0 = 0; o0 < NP; o0 += 16) {
-          uint32_t uu[16];
-          tc::tmem_ld16(tmem + (cp & 1u) * (uint32_t)N2 + lane_off + (uint32_t)(half * NP + o0), uu);
+        const int k2 = k20 + kk - 1, kgi = k2 >> 2, pair = k2 & 3;   // k' = 2 k2 + q: k-group k2/4, pair k2%4
+        const uint32_t dcol = tmem + (cp & 1u) * (uint32_t)N2 + lane_off;
+        for (int og = half; og < NP / 8; og += 2) {   // 32 bytes per (row, o-group): [k' = 2 k2 | 2 k2 + 1]
+          uint32_t re[8], im[8];
+          tmem_ld8(dcol + (uint32_t)(og * 8), re);
+          tmem_ld8(dcol + (uint32_t)(NP + og * 8), im);
           tc::tmem_wait_ld();
           if (i < n) {
+            float vr[8], vi[8];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              float v[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) v[e] = __uint_as_float(uu[8 * h + e]);
-              const uint32_t off = (uint32_t)((o0 >> 3) + h) * 128u + koff;
-              st_split8(grow + off, grow + g.g_half() + off, v);
-            }
+            for (int e = 0; e < 8; ++e) { vr[e] = __uint_as_float(re[e]); vi[e] = __uint_as_float(im[e]); }
+            uint4 hr, lr, hi, li;
+            tc::split8(vr, hr, lr);
+            tc::split8(vi, hi, li);
+            uint4* dh = reinterpret_cast<uint4*>(Gb + g.g_off(b, 0, kgi, og, pair, i));
+            uint4* dl = reinterpret_cast<uint4*>(Gb + g.g_off(b, 1, kgi, og, pair, i));
+            dh[0] = hr; dh[1] = hi;
+            dl[0] = lr; dl[1] = li;
           }
         }
       }
@@ -930,7 +993,6 @@ static int px_sms() {
   return v;
 }
 
-constexpr uint32_t kPxSmemLimit = 227u * 1024u;
 
 bool px_supported_shape(int n, int w) {
   if (w < 1 || w > 128) return false;
@@ -975,18 +1037,54 @@ cudaError_t launch_px_prep(int n, int w, const float* W2, const float* W3, const
   return cudaGetLastError();
 }
 
+// TMA tensor map of the interleaved G layout (px_layout.cuh): dims (innermost first) 8 x u32 (32 B),
+// n rows, 4 pairs, 5 x NP/8 (k-group, o-group), 2 B (system, hi|lo); box = one row's hi or lo blob.
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static cudaError_t make_g_map(CUtensorMap* m, const unsigned char* G, const PxGeom& g, int B) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t n = (cuuint64_t)g.n, kog = 5ull * (g.NP / 8);
+  const cuuint64_t dims[5] = {8, n, 4, kog, 2ull * B};
+  const cuuint64_t strides[4] = {32, 32 * n, 128 * n, 128 * n * kog};
+  const cuuint32_t box[5] = {8, 1, 4, (cuuint32_t)kog, 1};
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, const_cast<unsigned char*>(G), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 cudaError_t launch_px_layer(const PxLayerHost& h, cudaStream_t s) {
   PxLayerArgs a{};
   a.n = h.n; a.w = h.w; a.B = h.B; a.layer = h.layer; a.use_gelu = h.use_gelu;
   a.r = h.r; a.rr = h.rr; a.k = h.k; a.vin = h.vin; a.vout = h.vout; a.G = h.G; a.T = h.T; a.cst = h.cst;
   a.bias = h.bias; a.w1e = h.w1e; a.dw = h.dw; a.p3 = h.p3; a.status = h.status;
+  static int trace_layer = -1;
+  if (trace_layer < 0) { const char* e = getenv("FCGNO_PX_TRACE"); trace_layer = e ? atoi(e) : 0; }
+  a.trace = trace_layer == h.layer + 1;
   const PxGeom g(h.n, h.w);
   const bool first = h.layer == 0, proj = h.layer == 2;
   const size_t smem = PxSmem(g, first).total;
   const int grid = std::min(h.B * g.units, px_sms());
-  if (first) return launch_k(k_px_layer<true, false>, dim3(grid), dim3(kPxThreads), smem, s, a);
-  if (proj) return launch_k(k_px_layer<false, true>, dim3(grid), dim3(kPxThreads), smem, s, a);
-  return launch_k(k_px_layer<false, false>, dim3(grid), dim3(kPxThreads), smem, s, a);
+  alignas(64) CUtensorMap gmap;
+  if (const cudaError_t e = make_g_map(&gmap, h.G, g, h.B)) return e;
+  if (first) return launch_k(k_px_layer<true, false>, dim3(grid), dim3(kPxThreads), smem, s, a, gmap);
+  if (proj) return launch_k(k_px_layer<false, true>, dim3(grid), dim3(kPxThreads), smem, s, a, gmap);
+  return launch_k(k_px_layer<false, false>, dim3(grid), dim3(kPxThreads), smem, s, a, gmap);
 }
 
 cudaError_t launch_px_ysyn(const float* ghat, const unsigned char* cst, unsigned char* Gb, int n, int w, int B,
@@ -1034,6 +1132,10 @@ cudaError_t launch_mix_px(int mix, const float* chat, const unsigned char* cst, 
   const int grid = std::min(nitems, per_sm * px_sms());
   return launch_k(k_mix_tc, dim3(grid), dim3(128), smem, s, reinterpret_cast<const float2*>(chat),
                   cst + px_mx_offset(n, w, mix), reinterpret_cast<float2*>(ghat), w, B, cout, inv_n2, status);
+}
+
+cudaError_t px_trace_read(unsigned long long* host, int count) {
+  return cudaMemcpyFromSymbol(host, g_px_trace, sizeof(unsigned long long) * std::min(count, kPxTraceTiles * kPxTraceEv));
 }
 
 }  // namespace fcgno

@@ -8,8 +8,12 @@
 //   V tile  [hi | lo], each [cgroup c/8][pgroup p/8][p%8][c%8] (2048 B per cgroup): the K-major A of
 //           the next layer's bypass GEMM and, read MN-major, the A of this layer's x-analysis.
 //           Only CGS = ceil(w/8) channel groups are stored; the stage's padding groups are zeros.
-//   G row   [hi | lo], each [k'/8][o/8][k'%8][o%8] for k' = (kappa2, re|im) < 40 (5 k-groups):
-//           the MN-major B of the x-synthesis (N = o, K = k'); k-group 5 (k' 40..47) is zero in smem.
+//   G       y-synthesised spectral term, the MN-major B of the x-synthesis (N = o, K = k' = (kappa2,
+//           re|im) < 40, 5 k-groups; k-group 5 (k' 40..47) is zero in smem).  In smem a row is
+//           [k'/8][o/8][k'%8][o%8]; in HBM the rows of a system are interleaved at 32-byte granularity,
+//           [b][hi|lo][k'/8, o/8][k'%8 / 2][row i][32 B], so the y-synthesis writes 1 KB runs per warp
+//           (32 consecutive rows) and the layer gathers one row with a 5-D TMA tensor copy whose box
+//           lands in smem in exactly the row's canonical order.
 //   T row   fp32 [kappa2][o][re|im] (40 w floats): x-analysed activations, read by the y-analysis.
 #pragma once
 #include <cstddef>
@@ -41,6 +45,10 @@ struct PxGeom {
   __host__ __device__ size_t v_bytes(int B) const { return (size_t)B * TPS * 2 * v_half(); }
   __host__ __device__ size_t g_bytes(int B) const { return (size_t)B * n * 2 * g_half(); }
   __host__ __device__ size_t t_floats(int B) const { return (size_t)B * n * 40 * w + 256; }   // + over-read pad
+  // byte offset of the 32-byte piece (system b, hi|lo hl, k-group kg, o-group og, k'%8 pair, row i) of G
+  __host__ __device__ size_t g_off(int b, int hl, int kg, int og, int pair, int i) const {
+    return (((((size_t)b * 2 + hl) * 5 + kg) * (NP / 8) + og) * 4 + pair) * (size_t)n * 32 + (size_t)i * 32;
+  }
 };
 
 // Constant operand blobs, built once per NO apply / solve by k_px_prep ([hi][lo] each):

@@ -64,12 +64,18 @@ EXPORTS = {
     "fcgno_apply_NO": (_i, [_vp, NoDesc, _vp, _vp, _vp, _vp, _sz, _vp]),
     "fcgno_solve_workspace_bytes": (_sz, [Grid, _P(NoDesc), SolveOpts]),
     "fcgno_fcg_solve": (_i, [_vp, _P(NoDesc), _vp, _vp, _vp, SolveOpts, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_solve_diag_workspace_bytes": (_sz, [Grid, _P(NoDesc), SolveOpts]),
+    "fcgno_fcg_solve_diag": (_i, [_vp, _P(NoDesc), _vp, _vp, _vp, SolveOpts, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
+                                  _vp]),
+    "fcgno_notay_workspace_bytes": (_sz, [Grid, _P(NoDesc)]),
+    "fcgno_notay_ratio": (_i, [_vp, _P(NoDesc), _vp, _vp, _vp, _i, _vp, _vp, _sz, _vp]),
     "fcgno_solve_host_workspace_bytes": (_sz, [Grid, _P(NoDesc), SolveOpts]),
     "fcgno_solve_host": (_i, [Grid, _vp, _vp, _vp, _P(NoDesc), _vp, SolveOpts, _vp, _vp, _vp, _vp, _sz, _vp]),
     "fcgno_profile_get": (_i, [_i, _P(ctypes.c_double), _P(ctypes.c_int64)]),
     "fcgno_profile_reset": (None, []),
     "fcgno_profile_name": (ctypes.c_char_p, [_i]),
     "fcgno_kernel_launches": (ctypes.c_uint64, []),
+    "fcgno_debug_px_trace": (_i, [_vp, _i]),
     "fcgno_last_error": (ctypes.c_char_p, []),
     "fcgno_abi_version": (_i, []),
 }
@@ -299,17 +305,40 @@ class HostSolver:
 def notay_ratio(problem: Problem, r: torch.Tensor, e: torch.Tensor, no: NeuralOperator | None = None,
                 stream=None, optimal_scale: bool = False) -> torch.Tensor:
     """Theorem-1 / Notay diagnostic (PAPER.md Eq. final_loss):
-    eps_b = ||B(r_b) - e_b||_A / ||e_b||_A with e = A^{-1} r supplied by the caller.
+    eps_b = ||c B(r_b) - e_b||_A / ||e_b||_A with e = A^{-1} r supplied by the caller and c = 1, or the
+    minimiser c* (optimal_scale).  fcgno_notay_ratio, computed entirely in the library's kernels."""
+    _require(r, problem.shape, "r")
+    _require(e, problem.shape, "e")
+    desc = ctypes.byref(no.desc) if no is not None else None
+    ws = _workspace(_lib.fcgno_notay_workspace_bytes(problem.grid, desc), problem.device, stream)
+    eps = _on(stream, lambda: torch.empty(problem.B, dtype=torch.float64, device=problem.device))
+    _check(_lib.fcgno_notay_ratio(problem._h, desc, _ptr(no.packed) if no is not None else None, _ptr(r), _ptr(e),
+                                  int(bool(optimal_scale)), _ptr(eps), _ptr(ws), ws.numel(), _stream(stream)))
+    return eps
 
-    Composed from the library's entry points: w = apply_NO(r) (identity: w = r), A w and A e
-    (apply_A), and the correctly rounded dots (w, Aw), (w, Ae), (e, Ae) (batched_dot), so that
-    ||w - e||_A^2 = (w, Aw) - 2 (w, Ae) + (e, Ae); only that scalar combination of B numbers is done
-    here.  optimal_scale: min over c of ||c B(r) - e||_A / ||e||_A = sqrt(1 - (w,Ae)^2 / ((w,Aw)(e,Ae))),
-    the scale-free form (FCG's iterates do not depend on the scale of B)."""
-    w = no.apply(problem, r, stream) if no is not None else r
-    Aw = problem.apply_A(w, stream=stream)
-    Ae = problem.apply_A(e, stream=stream)
-    ww, we, ee = problem.dot(w, Aw, stream), problem.dot(w, Ae, stream), problem.dot(e, Ae, stream)
-    if optimal_scale:
-        return torch.sqrt(torch.clamp(1.0 - we * we / (ww * ee), min=0.0))
-    return torch.sqrt(torch.clamp(ww - 2.0 * we + ee, min=0.0) / ee)
+
+def fcg_solve_diag(problem: Problem, f: torch.Tensor, u_star: torch.Tensor, u0: torch.Tensor | None = None, *,
+                   m: int, tol: float, maxit: int, no: NeuralOperator | None = None,
+                   schedule: int = SCHEDULE_PAPER, check_every: int = 16, vec_fp32: bool = False):
+    """fcg_solve with per-iteration Theorem-1 diagnostics (fcgno_fcg_solve_diag): returns
+    (SolveResult, eps[B][maxit], err_a[B][maxit]) with eps[b][i] = ||w_i - e_i||_A / ||e_i||_A and
+    err_a[b][i] = ||e_i||_A, e_i = u_star - u_i, for i < iters[b] (NaN beyond)."""
+    _require(f, problem.shape, "f")
+    _require(u_star, problem.shape, "u_star")
+    opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), 0, int(bool(vec_fp32)))
+    desc = ctypes.byref(no.desc) if no is not None else None
+    nbytes = _lib.fcgno_solve_diag_workspace_bytes(problem.grid, desc, opts)
+    if nbytes == 0:
+        raise ValueError("bad solve options")
+    dev = problem.device
+    ws = _workspace(nbytes, dev)
+    u = torch.zeros_like(f) if u0 is None else u0.clone()
+    iters = torch.empty(problem.B, dtype=torch.int32, device=dev)
+    status = torch.empty(problem.B, dtype=torch.int32, device=dev)
+    hist = torch.full((problem.B, maxit + 1), float("nan"), dtype=torch.float64, device=dev)
+    eps = torch.full((problem.B, max(maxit, 1)), float("nan"), dtype=torch.float64, device=dev)
+    err_a = torch.full((problem.B, max(maxit, 1)), float("nan"), dtype=torch.float64, device=dev)
+    _check(_lib.fcgno_fcg_solve_diag(problem._h, desc, _ptr(no.packed) if no is not None else None, _ptr(f), _ptr(u),
+                                     opts, _ptr(iters), _ptr(status), _ptr(hist), _ptr(u_star), _ptr(eps),
+                                     _ptr(err_a), _ptr(ws), ws.numel(), _stream()))
+    return SolveResult(u, iters, status, hist), eps, err_a

@@ -47,14 +47,19 @@ def line_map(func):
 def main():
     rep, kname, func = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
+    which = int(sys.argv[5]) if len(sys.argv) > 5 else 0   # n-th captured launch whose name matches
     txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
-    rows, cur, hdr = [], None, None
+    rows, cur, hdr, seen = [], None, None, -1
     for r in csv.reader(io.StringIO(txt)):
         if not r:
             continue
         if r[0] == "Kernel Name":
             cur = r[1]
+            if kname in cur:
+                seen += 1
+            if seen != which:
+                cur = None
             continue
         if r[0] == "Address":
             hdr = r
