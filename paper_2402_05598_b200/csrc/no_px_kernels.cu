@@ -573,134 +573,190 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
 }
 
 // ------------------------------------------------------------------ k_px_ysyn: y-synthesis
-// Item = (system b, M tile of 128 rows i, group of KG consecutive kappa2).  For each kappa2 the B
-// operand Gh[(k1, p)][(q, o)] (K = 48, N = 2 NP) is built from the mixed spectrum g[kappa][b][o]:
+// Work = (system b, M tile of 128 rows i, kappa2) steps; a CTA takes items (b, M tile, group of KG
+// consecutive kappa2) and walks their steps in order.  For each kappa2 the B operand
+// Gh[(k1, p)][(q, o)] (K = 48, N = 2 NP) is built from the mixed spectrum g[kappa][b][o]:
 //   rows (k1, 0): (gr | gi),  rows (k1, 1): (gi | -gr)    so that  D[i][(q,o)] = (Gr | Gi)[i][kappa2][o]
 // with Fp[i][(k1,0)] = cos, Fp[i][(k1,1)] = -sin: Gr = sum gr cos - gi sin, Gi = sum gi cos + gr sin
-// (g e^{+i theta}).  The epilogue writes the G rows' bf16 hi/lo chunks of k' = 2 kappa2 + q.
+// (g e^{+i theta}).  Warp-specialised: warps 0-7 build B(step) into a double buffer (thread = (o, half
+// of the kappa1 range), all its loads in flight at once), warp 8 issues the MMAs into a double-buffered
+// TMEM accumulator, warps 9-16 write the G rows' bf16 hi/lo pieces (32 bytes per (row, o-group),
+// consecutive rows adjacent: 1 KB per warp store).
+constexpr int kYsynBuild = 8, kYsynEpi = 8, kYsynThreads = (kYsynBuild + 1 + kYsynEpi) * 32;
 struct PxYsynSmem {
-  uint32_t A, Bb, bar, tptr, total, b_half;
+  uint32_t A, Bb, bar, tptr, runb, total, b_half;
   __host__ __device__ PxYsynSmem(const PxGeom& g) {
     uint32_t o = 0;
     auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
-    A = take(2u * 128u * 48u * 2u);
+    A = take((uint32_t)g.nMT * 2u * 128u * 48u * 2u);   // every M tile's Fp blob, resident
     b_half = 2u * (uint32_t)g.NP * 48u * 2u;
     Bb = take(2u * 2u * b_half);
-    bar = take(64);
-    tptr = bar + 32;
+    bar = take(128);
+    tptr = bar + 120;
+    runb = take(kPxMaxSys / 8);
     total = o;
   }
 };
 
-__global__ void __launch_bounds__(256, 1) k_px_ysyn(const float2* __restrict__ ghat, const unsigned char* __restrict__ cst,
-                                                    unsigned char* __restrict__ Gb, int n, int w, int B, int kg,
-                                                    const int* __restrict__ status) {
+__global__ void __launch_bounds__(kYsynThreads, 1) k_px_ysyn(const float2* __restrict__ ghat, const unsigned char* __restrict__ cst,
+                                                             unsigned char* __restrict__ Gb, int n, int w, int B, int kg,
+                                                             const int* __restrict__ status) {
   const PxGeom g(n, w);
   const PxConst C(g);
   const PxYsynSmem L(g);
   extern __shared__ __align__(1024) unsigned char sm[];
   const int NP = g.NP, N2 = 2 * NP, nkg = kModes / kg;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0], [1] MMA into D buffer; [2] A landed
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);
+  uint64_t *bfull = bar, *bfree = bar + 2, *dfull = bar + 4, *dfree = bar + 6, *abar = bar + 8;
   uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
   const int nitems = B * g.nMT * nkg;
   const uint32_t LBO_B = (uint32_t)(N2 / 8) * 128u, ncols = pow2_cols(2u * N2);
+  uint32_t* runb = reinterpret_cast<uint32_t*>(sm + L.runb);   // running-system bitmask (B <= kPxMaxSys)
+  const bool cached = status && B <= kPxMaxSys;
+  if (cached)
+    for (int q = warp; q < (B + 31) / 32; q += blockDim.x / 32) {
+      const int sb = q * 32 + lane;
+      const unsigned bits = __ballot_sync(0xffffffffu, sb < B && __ldcg(status + sb) == SYS_RUNNING);
+      if (lane == 0) runb[q] = bits;
+    }
   auto next_item = [&](int it) {
-    while (it < nitems && status && status[it / (g.nMT * nkg)] != SYS_RUNNING) it += gridDim.x;
+    if (!status) return it;
+    while (it < nitems) {
+      const int sb = it / (g.nMT * nkg);
+      if (cached ? ((runb[sb >> 5] >> (sb & 31)) & 1u) != 0 : __ldcg(status + sb) == SYS_RUNNING) break;
+      it += gridDim.x;
+    }
     return it;
   };
   if (tid == 0) {
-    for (int q = 0; q < 3; ++q) tc::mbar_init(&bar[q], 1);
+    for (int q = 0; q < 9; ++q) tc::mbar_init(&bar[q], q < 2 ? 32u * kYsynBuild : (q >= 6 && q < 8) ? 32u * kYsynEpi : 1u);
     tc::fence_mbar_init();
+    tc::mbar_expect_tx(abar, (uint32_t)g.nMT * 2u * C.fp_half);
+    tc::bulk_g2s(sm + L.A, cst + C.FP, (uint32_t)g.nMT * 2u * C.fp_half, abar);
   }
   if (warp == 0) tc::tmem_alloc(tptr, ncols);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = *tptr;
-  const uint32_t base = tc::smem_u32(sm);
-  const uint32_t id = tc::make_idesc_bf16(128, N2, false, false);
   pdl_wait();
   pdl_trigger();
-  uint32_t cnt = 0, aph = 0;   // MMA groups issued by this CTA; A loads
-  for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + gridDim.x)) {
-    const int b = it / (g.nMT * nkg), mt = (it / nkg) % g.nMT, k20 = (it % nkg) * kg;
-    if (tid == 0) {
-      tc::mbar_expect_tx(&bar[2], 2u * C.fp_half);
-      tc::bulk_g2s(sm + L.A, cst + C.FP + (size_t)mt * 2 * C.fp_half, 2u * C.fp_half, &bar[2]);
-    }
-    const int i = mt * 128 + (warp & 3) * 32 + lane, half = warp >> 2;
-    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    for (int kk = 0; kk <= kg; ++kk) {
-      const uint32_t c = cnt + (uint32_t)kk;
-      if (kk < kg) {   // B for kappa2 = k20 + kk into buffer c & 1
+
+  if (warp < kYsynBuild) {
+    // ================= B builders
+    const int bt = tid;
+    uint32_t c = 0;
+    for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + gridDim.x)) {
+      const int b = it / (g.nMT * nkg), k20 = (it % nkg) * kg;
+      for (int kk = 0; kk < kg; ++kk, ++c) {
         const int k2 = k20 + kk;
+        tc::mbar_wait(&bfree[c & 1u], ((c >> 1) & 1u) ^ 1u);
         unsigned char* bh = sm + L.Bb + (c & 1u) * 2u * L.b_half;
-        for (int t = tid; t < N2 * 6; t += blockDim.x) {
-          const int nn = t % N2, kgp = t / N2, q = nn / NP, o = nn % NP;
-          float v[8];
+        for (int t = bt; t < 2 * NP; t += 32 * kYsynBuild) {   // task = (o, kappa1 half: k-groups 3h .. 3h+2)
+          const int o = t % NP, hh = t / NP;
+          float2 gg[12];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int k1 = kgp * 4 + e;
-            float2 gg = make_float2(0.f, 0.f);
-            if (k1 < kModes && o < w) gg = __ldg(ghat + ((size_t)(k1 * kModes + k2) * B + b) * w + o);
-            v[2 * e] = q == 0 ? gg.x : gg.y;
-            v[2 * e + 1] = q == 0 ? gg.y : -gg.x;
+          for (int e = 0; e < 12; ++e) {
+            const int k1 = hh * 12 + e;
+            gg[e] = (k1 < kModes && o < w) ? __ldg(ghat + ((size_t)(k1 * kModes + k2) * B + b) * w + o) : make_float2(0.f, 0.f);
           }
-          const uint32_t off = (uint32_t)(nn >> 3) * 128u + (uint32_t)kgp * LBO_B + (uint32_t)(nn & 7) * 16u;
-          st_split8(bh + off, bh + L.b_half + off, v);
+#pragma unroll
+          for (int kq = 0; kq < 3; ++kq) {
+            const int kgp = hh * 3 + kq;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              float v[8];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 z = gg[kq * 4 + e];
+                v[2 * e] = q == 0 ? z.x : z.y;
+                v[2 * e + 1] = q == 0 ? z.y : -z.x;
+              }
+              const int nn = q * NP + o;
+              const uint32_t off = (uint32_t)(nn >> 3) * 128u + (uint32_t)kgp * LBO_B + (uint32_t)(nn & 7) * 16u;
+              st_split8(bh + off, bh + L.b_half + off, v);
+            }
+          }
         }
+        tc::fence_proxy_async_smem();
+        tc::mbar_arrive(&bfull[c & 1u]);
       }
-      tc::fence_proxy_async_smem();
-      tc::fence_before_sync();
-      __syncthreads();
-      tc::fence_after_sync();
-      if (kk < kg && tid == 0) {
-        if (kk == 0) { tc::mbar_wait(&bar[2], aph); }
-        tc::fence_after_sync();
-        const uint32_t bh = base + L.Bb + (c & 1u) * 2u * L.b_half, bl = bh + L.b_half;
-        const uint32_t ah = base + L.A, al = ah + C.fp_half;
-        const uint32_t d = tmem + (c & 1u) * (uint32_t)N2;
-        for (int ks = 0; ks < 3; ++ks)
+    }
+  } else if (warp == kYsynBuild) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      tc::mbar_wait(abar, 0);
+      const uint32_t id = tc::make_idesc_bf16(128, N2, false, false);
+      const uint32_t base = tc::smem_u32(sm);
+      uint32_t c = 0;
+      for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + gridDim.x)) {
+        const int mt = (it / nkg) % g.nMT;
+        const uint32_t ah = base + L.A + (uint32_t)mt * 2u * C.fp_half, al = ah + C.fp_half;
+        for (int kk = 0; kk < kg; ++kk, ++c) {
+          tc::mbar_wait(&bfull[c & 1u], (c >> 1) & 1u);
+          tc::mbar_wait(&dfree[c & 1u], ((c >> 1) & 1u) ^ 1u);
+          tc::fence_after_sync();
+          const uint32_t bh = base + L.Bb + (c & 1u) * 2u * L.b_half, bl = bh + L.b_half;
+          const uint32_t d = tmem + (c & 1u) * (uint32_t)N2;
+          for (int ks = 0; ks < 3; ++ks)
 #pragma unroll
-          for (int p = 0; p < 3; ++p) {
-            const uint32_t aa = (p == 2 ? al : ah) + (uint32_t)ks * 256u;
-            const uint32_t bb = (p == 1 ? bl : bh) + (uint32_t)ks * 2u * LBO_B;
-            tc::mma_bf16(d, tc::make_sdesc(aa, 128, 768), tc::make_sdesc(bb, LBO_B, 128), id, (ks | p) != 0);
-          }
-        tc::mma_commit(&bar[c & 1u]);
-      }
-      if (kk >= 1) {   // epilogue of kappa2 = k20 + kk - 1 (buffer (c - 1) & 1)
-        const uint32_t cp = c - 1u;
-        tc::mbar_wait(&bar[cp & 1u], (cp >> 1) & 1u);
-        tc::fence_after_sync();
-        const int k2 = k20 + kk - 1, kgi = k2 >> 2, pair = k2 & 3;   // k' = 2 k2 + q: k-group k2/4, pair k2%4
-        const uint32_t dcol = tmem + (cp & 1u) * (uint32_t)N2 + lane_off;
-        for (int og = half; og < NP / 8; og += 2) {   // 32 bytes per (row, o-group): [k' = 2 k2 | 2 k2 + 1]
-          uint32_t re[8], im[8];
-          tmem_ld8(dcol + (uint32_t)(og * 8), re);
-          tmem_ld8(dcol + (uint32_t)(NP + og * 8), im);
-          tc::tmem_wait_ld();
-          if (i < n) {
-            float vr[8], vi[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) { vr[e] = __uint_as_float(re[e]); vi[e] = __uint_as_float(im[e]); }
-            uint4 hr, lr, hi, li;
-            tc::split8(vr, hr, lr);
-            tc::split8(vi, hi, li);
-            uint4* dh = reinterpret_cast<uint4*>(Gb + g.g_off(b, 0, kgi, og, pair, i));
-            uint4* dl = reinterpret_cast<uint4*>(Gb + g.g_off(b, 1, kgi, og, pair, i));
-            dh[0] = hr; dh[1] = hi;
-            dl[0] = lr; dl[1] = li;
-          }
+            for (int p = 0; p < 3; ++p) {
+              const uint32_t aa = (p == 2 ? al : ah) + (uint32_t)ks * 256u;
+              const uint32_t bb = (p == 1 ? bl : bh) + (uint32_t)ks * 2u * LBO_B;
+              tc::mma_bf16(d, tc::make_sdesc(aa, 128, 768), tc::make_sdesc(bb, LBO_B, 128), id, (ks | p) != 0);
+            }
+          tc::mma_commit(&dfull[c & 1u]);
+          tc::mma_commit(&bfree[c & 1u]);
         }
       }
     }
-    cnt += (uint32_t)kg;
-    aph ^= 1u;
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
+  } else {
+    // ================= epilogue: thread = row i of the M tile; the two warpgroups split the o-groups
+    const int ew = warp - (kYsynBuild + 1), q4 = warp & 3, half = ew / 4;
+    const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
+    uint32_t c = 0;
+    for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + gridDim.x)) {
+      const int b = it / (g.nMT * nkg), mt = (it / nkg) % g.nMT, k20 = (it % nkg) * kg;
+      const int i = mt * 128 + q4 * 32 + lane;
+      for (int kk = 0; kk < kg; ++kk, ++c) {
+        tc::mbar_wait(&dfull[c & 1u], (c >> 1) & 1u);
+        tc::fence_after_sync();
+        const int k2 = k20 + kk, kgi = k2 >> 2, pair = k2 & 3;   // k' = 2 k2 + q: k-group k2/4, pair k2%4
+        const uint32_t dcol = tmem + (c & 1u) * (uint32_t)N2 + lane_off;
+        // 32 bytes per (row, o-group): [k' = 2 k2 | 2 k2 + 1]; the TMEM loads of 3 o-groups issued together
+        for (int og0 = half; og0 < NP / 8; og0 += 6) {
+          uint32_t re[3][8], im[3][8];
+#pragma unroll
+          for (int z = 0; z < 3; ++z) {
+            const int og = og0 + 2 * z;
+            if (og < NP / 8) {
+              tmem_ld8(dcol + (uint32_t)(og * 8), re[z]);
+              tmem_ld8(dcol + (uint32_t)(NP + og * 8), im[z]);
+            }
+          }
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int z = 0; z < 3; ++z) {
+            const int og = og0 + 2 * z;
+            if (i < n && og < NP / 8) {
+              float vr[8], vi[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) { vr[e] = __uint_as_float(re[z][e]); vi[e] = __uint_as_float(im[z][e]); }
+              uint4 hr, lr, hi, li;
+              tc::split8(vr, hr, lr);
+              tc::split8(vi, hi, li);
+              uint4* dh = reinterpret_cast<uint4*>(Gb + g.g_off(b, 0, kgi, og, pair, i));
+              uint4* dl = reinterpret_cast<uint4*>(Gb + g.g_off(b, 1, kgi, og, pair, i));
+              dh[0] = hr; dh[1] = hi;
+              dl[0] = lr; dl[1] = li;
+            }
+          }
+        }
+        tc::fence_before_sync();
+        tc::mbar_arrive(&dfree[c & 1u]);
+      }
+    }
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -709,11 +765,12 @@ __global__ void __launch_bounds__(256, 1) k_px_ysyn(const float2* __restrict__ g
 }
 
 // ------------------------------------------------------------------ k_px_yan: y-analysis
-// Item = (system b, M tile of 128 rows m = (kappa2 w + o) 2 + (re|im) of the T rows), K = i in chunks
-// of 32 rows converted fp32 -> bf16 hi/lo (MN-major A) into a double buffer while the previous
-// chunk's MMAs run.  B = F[i][(k1, x|y)], resident.  Epilogue: lane pairs (re, im) recombine
-//   c_r = T_r.Fx - T_i.Fy,  c_i = T_i.Fx + T_r.Fy      (e^{-i theta} = Fx + i Fy).
-constexpr int kYanKC = 32;
+// Item = (system b, M tile of 128 rows m = (kappa2 w + o) 2 + (re|im) of the T rows), K = i in chunks of
+// 64 rows.  Each thread holds its part of the next chunk in registers (8 x 16-byte loads in flight)
+// while the current one is converted fp32 -> bf16 hi/lo (MN-major A) into a double buffer and the
+// previous chunk's MMAs run: one block barrier per chunk.  B = F[i][(k1, x|y)], resident.
+// Epilogue: lane pairs (re, im) recombine  c_r = T_r.Fx - T_i.Fy,  c_i = T_i.Fx + T_r.Fy  (e^{-i theta}).
+constexpr int kYanKC = 64, kYanTasks = kYanKC * 16 / 256;   // 16-row... 8-float tasks per thread per chunk
 struct PxYanSmem {
   uint32_t A, Bf, bar, tptr, total;
   __host__ __device__ PxYanSmem(const PxGeom& g) {
@@ -722,7 +779,7 @@ struct PxYanSmem {
     A = take(2u * 2u * 128u * kYanKC * 2u);
     Bf = take(2u * (uint32_t)g.n * 48u * 2u);
     bar = take(64);
-    tptr = bar + 32;
+    tptr = bar + 56;
     total = o;
   }
 };
@@ -735,12 +792,12 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
   const PxYanSmem L(g);
   extern __shared__ __align__(1024) unsigned char sm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0], [1] MMA of A buffer; [2] B landed
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);   // [0,1] MMA of A buffer; [2] B landed
   uint32_t* tptr = reinterpret_cast<uint32_t*>(sm + L.tptr);
   const int nitems = B * g.MYT, nK = n / kYanKC, M = 40 * w;
   const uint32_t a_half = 128u * kYanKC * 2u, SBO_Y = (uint32_t)(n / 8) * 128u;
   auto next_item = [&](int it) {
-    while (it < nitems && status && status[it / g.MYT] != SYS_RUNNING) it += gridDim.x;
+    while (it < nitems && status && __ldcg(status + it / g.MYT) != SYS_RUNNING) it += gridDim.x;
     return it;
   };
   if (tid == 0) {
@@ -759,43 +816,58 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
   pdl_wait();
   pdl_trigger();
   if (tid == 0) tc::mbar_wait(&bar[2], 0);
-  uint32_t cnt = 0;   // K chunks issued by this CTA
+  // the CTA's chunk sequence (item, kc); registers x hold the next chunk's loads
+  float4 x[kYanTasks][2];
+  int lit = next_item(blockIdx.x), lkc = 0;
+  auto load = [&]() {
+    if (lit < nitems) {
+      const int b = lit / g.MYT, m0 = (lit % g.MYT) * 128;
+      const float* src = T + ((size_t)b * n + (size_t)lkc * kYanKC) * M + m0;
+#pragma unroll
+      for (int z = 0; z < kYanTasks; ++z) {
+        const int t = tid + z * 256, il = t >> 4, mg = t & 15;
+        const float4* p = reinterpret_cast<const float4*>(src + (size_t)il * M + mg * 8);
+        x[z][0] = __ldg(p);
+        x[z][1] = __ldg(p + 1);
+      }
+      if (++lkc == nK) { lkc = 0; lit = next_item(lit + gridDim.x); }
+    }
+  };
+  load();
+  uint32_t c = 0;
   for (int it = next_item(blockIdx.x); it < nitems; it = next_item(it + gridDim.x)) {
     const int b = it / g.MYT, m0 = (it % g.MYT) * 128;
-    const float* Tb = T + (size_t)b * n * M + m0;
-    for (int kc = 0; kc <= nK; ++kc) {
-      const uint32_t c = cnt + (uint32_t)kc;
-      if (kc < nK) {
-        if (c >= 2) tc::mbar_wait(&bar[c & 1u], ((c - 2u) >> 1) & 1u);   // MMA c - 2 done with this buffer
-        unsigned char* ah = sm + L.A + (c & 1u) * 2u * a_half;
-        for (int t = tid; t < kYanKC * 16; t += blockDim.x) {
-          const int il = t >> 4, mg = t & 15;
-          const float4* src = reinterpret_cast<const float4*>(Tb + (size_t)(kc * kYanKC + il) * M + mg * 8);
-          const float4 x0 = __ldg(src), x1 = __ldg(src + 1);
-          const float v[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-          const uint32_t off = (uint32_t)mg * 128u + (uint32_t)(il >> 3) * 2048u + (uint32_t)(il & 7) * 16u;
-          st_split8(ah + off, ah + a_half + off, v);
-        }
+    for (int kc = 0; kc < nK; ++kc, ++c) {
+      if (c >= 2) tc::mbar_wait(&bar[c & 1u], ((c - 2u) >> 1) & 1u);    // MMA c - 2 done with A buffer c & 1
+      unsigned char* ah = sm + L.A + (c & 1u) * 2u * a_half;
+#pragma unroll
+      for (int z = 0; z < kYanTasks; ++z) {
+        const int t = tid + z * 256, il = t >> 4, mg = t & 15;
+        const float v[8] = {x[z][0].x, x[z][0].y, x[z][0].z, x[z][0].w, x[z][1].x, x[z][1].y, x[z][1].z, x[z][1].w};
+        const uint32_t off = (uint32_t)mg * 128u + (uint32_t)(il >> 3) * 2048u + (uint32_t)(il & 7) * 16u;
+        st_split8(ah + off, ah + a_half + off, v);
       }
+      load();                                                            // next chunk in flight from here
       tc::fence_proxy_async_smem();
       tc::fence_before_sync();
       __syncthreads();
       tc::fence_after_sync();
-      if (kc < nK && tid == 0) {
-        const uint32_t ah = base + L.A + (c & 1u) * 2u * a_half, al = ah + a_half;
+      if (tid == 0) {
+        const uint32_t aah = base + L.A + (c & 1u) * 2u * a_half, aal = aah + a_half;
         const uint32_t bh = base + L.Bf, bl = bh + C.fy_half;
         for (int ks = 0; ks < kYanKC / 16; ++ks)
 #pragma unroll
           for (int p = 0; p < 3; ++p) {
-            const uint32_t aa = (p == 2 ? al : ah) + (uint32_t)ks * 4096u;
+            const uint32_t aa = (p == 2 ? aal : aah) + (uint32_t)ks * 4096u;
             const uint32_t bb = (p == 1 ? bl : bh) + (uint32_t)((kc * kYanKC + ks * 16) / 8) * 128u;
             tc::mma_bf16(tmem, tc::make_sdesc(aa, 2048, 128), tc::make_sdesc(bb, 128, SBO_Y), id, (kc | ks | p) != 0);
           }
         tc::mma_commit(&bar[c & 1u]);
       }
     }
-    // epilogue: all of this item's MMAs complete (the last commit covers the earlier ones)
-    const uint32_t cl = cnt + (uint32_t)nK - 1u;
+    // epilogue: all of this item's MMAs complete (the last commit covers the earlier ones); the next
+    // item's first MMA is issued only after the next chunk's block barrier
+    const uint32_t cl = c - 1u;
     tc::mbar_wait(&bar[cl & 1u], (cl >> 1) & 1u);
     tc::fence_after_sync();
     if (warp < 4) {
@@ -809,15 +881,12 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
       const bool re = (lane & 1) == 0;
 #pragma unroll
       for (int k1 = 0; k1 < kModes; ++k1) {
-        const float x = __uint_as_float(v[2 * k1]), y = __uint_as_float(v[2 * k1 + 1]);
-        const float px = __shfl_xor_sync(0xffffffffu, x, 1), py = __shfl_xor_sync(0xffffffffu, y, 1);
-        if (re && m < M) chat[((size_t)(k1 * kModes + k2) * B + b) * w + o] = make_float2(x - py, px + y);
+        const float xv = __uint_as_float(v[2 * k1]), yv = __uint_as_float(v[2 * k1 + 1]);
+        const float px = __shfl_xor_sync(0xffffffffu, xv, 1), py = __shfl_xor_sync(0xffffffffu, yv, 1);
+        if (re && m < M) chat[((size_t)(k1 * kModes + k2) * B + b) * w + o] = make_float2(xv - py, px + yv);
       }
     }
-    cnt += (uint32_t)nK;
     tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -1091,18 +1160,14 @@ cudaError_t launch_px_ysyn(const float* ghat, const unsigned char* cst, unsigned
                            const int* status, cudaStream_t s) {
   const PxGeom g(n, w);
   const int sms = px_sms();
-  // kappa2 groups per (system, M tile): enough items to cover the SMs twice where possible
+  // one kappa2 per item: the Fp blobs are resident, so finer items only improve the balance
   const int base_items = B * g.nMT;
-  int kg = 1;
-  for (int cand : {20, 10, 5, 4, 2})
-    if (base_items * (kModes / cand) >= sms) { kg = cand; break; }
+  const int kg = 1;
   const PxYsynSmem L(g);
   const int items = base_items * (kModes / kg);
-  const int by_tmem = (int)(512u / pow2_cols(4u * (uint32_t)g.NP));
-  const int per_sm = std::max(1, std::min(by_tmem, (int)((228u * 1024u) / (L.total + 1024u))));
-  const int grid = std::min(items, per_sm * sms);
-  return launch_k(k_px_ysyn, dim3(grid), dim3(256), (size_t)L.total, s, reinterpret_cast<const float2*>(ghat), cst, Gb,
-                  n, w, B, kg, status);
+  const int grid = std::min(items, sms);
+  return launch_k(k_px_ysyn, dim3(grid), dim3(kYsynThreads), (size_t)L.total, s, reinterpret_cast<const float2*>(ghat),
+                  cst, Gb, n, w, B, kg, status);
 }
 
 cudaError_t launch_px_yan(const float* T, const unsigned char* cst, float* chat, int n, int w, int B, const int* status,
