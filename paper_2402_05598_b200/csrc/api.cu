@@ -109,6 +109,7 @@ struct NoWs {
   T *rpart, *v0, *v1, *chat, *ghat;
   unsigned char *vb0, *vb1, *Gb, *cst;   // tensor-core path blobs (fp32 NO only)
   float *Tb, *p3;
+  double* rinv;
   size_t vb_bytes, gb_bytes;
 };
 template <typename T>
@@ -118,6 +119,7 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
   r.rpart = c.take<T>((size_t)B * ngroups_of(n) * kModes2 * 2);
   r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
   if (use_px(n, w, sizeof(T) == sizeof(float))) {
+    r.rinv = c.take<double>(B);
     r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
     r.vb_bytes = px_v_bytes(n, w, B);
     r.gb_bytes = px_g_bytes(n, w, B);
@@ -154,7 +156,7 @@ NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* 
   no.k = p->k; no.pk = static_cast<const T*>(packed); no.L = no_layout(d.width);
   no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
   no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
-  no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb; no.cst = w.cst; no.p3 = w.p3;
+  no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb; no.cst = w.cst; no.p3 = w.p3; no.rinv = w.rinv;
   no.tc = (sizeof(T) == sizeof(float)) && w.Gb != nullptr;
   return no;
 }

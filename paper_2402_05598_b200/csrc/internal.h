@@ -73,6 +73,7 @@ struct NoDev {
   const T* F;                 // twiddles [n][kModes] complex: exp(-2 pi i kappa j / n)
   const T* khat;              // [B][400] complex DFT_M(k)
   T* rpart;                   // [B][ngroups][400] complex partial DFT_M(r/s)
+  double* rinv;               // [B] 1/||r|| (written by the input DFT; tensor-core path)
   int ngroups;                // row groups of the input DFT
   T* v0;                      // [B][w][N]
   T* v1;                      // [B][w][N]
@@ -90,7 +91,7 @@ struct NoDev {
 // Tensor-core (pixel-major) SNO path, no_px_kernels.cu.
 struct PxLayerHost {
   int n, w, B, layer, use_gelu;              // layer 0, 1, 2 = SNO layers 1-3
-  const double *r, *rr, *k;                  // layer 1 inputs
+  const double *r, *rr, *k;                  // layer 1 inputs (rr: 1/||r|| per system, from the input DFT)
   const unsigned char* vin;                  // V blobs (layers 2, 3)
   unsigned char* vout;                       // V blobs written (layers 1, 2)
   const unsigned char* G;                    // G rows (y-synthesised spectral term)

@@ -56,7 +56,7 @@ template <typename T, bool FROM_R>
 __global__ void __launch_bounds__(256) k_dft_rows(const double* __restrict__ x, const double* __restrict__ rr,
                                                   const typename Cplx<T>::type* __restrict__ F,
                                                   typename Cplx<T>::type* __restrict__ part, int n, int ngroups,
-                                                  const int* __restrict__ status) {
+                                                  const int* __restrict__ status, double* __restrict__ rinv) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename Cplx<T>::type;
@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(256) k_dft_rows(const double* __restrict__ x, 
   if (FROM_R) {
     const double s = sqrt(rr[b]);
     inv = s > 0.0 ? 1.0 / s : 0.0;
+    if (rinv && g == 0 && threadIdx.x == 0) rinv[b] = inv;   // 1/||r|| for the tensor-core layer 1
   }
   const double* xb = x + (size_t)b * N + (size_t)i0 * n;
   for (int t = threadIdx.x; t < rows * n; t += blockDim.x) X[t] = (T)(xb[t] * inv);
@@ -124,7 +125,7 @@ template <typename T>
 cudaError_t launch_khat(const double* k, const T* F, T* part, T* khat, int n, int B, int ngroups, cudaStream_t s) {
   using T2 = typename Cplx<T>::type;
   k_dft_rows<T, false><<<dim3(ngroups, B), 256, dft_smem(n, sizeof(T)), s>>>(
-      k, nullptr, reinterpret_cast<const T2*>(F), reinterpret_cast<T2*>(part), n, ngroups, nullptr);
+      k, nullptr, reinterpret_cast<const T2*>(F), reinterpret_cast<T2*>(part), n, ngroups, nullptr, nullptr);
   k_reduce_groups<T><<<B, 256, 0, s>>>(reinterpret_cast<const T2*>(part), reinterpret_cast<T2*>(khat), ngroups);
   launch_counter() += 2;
   return cudaGetLastError();
@@ -768,7 +769,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   // 1. DFT_M of r/||r|| (row-group partials)
   pb(PROF_NO_INPUT);
   launch_k(k_dft_rows<T, true>, dim3(no.ngroups, B), dim3(256), dft_smem(n, sizeof(T)), s, r, rr, F,
-           reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status);
+           reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status, no.rinv);
   ++launches;
   // 2. layer-1 mixing with the lift folded in
   launch_k(k_lift_mix<T>, dim3(B, (w + kLiftCh - 1) / kLiftCh), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
@@ -795,7 +796,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     if (tc_path) {
       PxLayerHost h{};
       h.n = n; h.w = w; h.B = B; h.use_gelu = no.use_gelu; h.layer = l;
-      h.r = r; h.rr = rr; h.k = no.k;
+      h.r = r; h.rr = no.rinv; h.k = no.k;
       h.cst = no.cst;
       h.bias = reinterpret_cast<const float*>(pk + (l == 0 ? no.L.b1 : no.L.b[l - 1]));
       h.w1e = reinterpret_cast<const float*>(pk + no.L.W1E);

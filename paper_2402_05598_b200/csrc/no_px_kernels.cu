@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256) k_px_prep(const PxPrepArgs a) {
   const PxGeom g(a.n, a.w);
   const PxConst C(g);
   const int n = a.n, w = a.w;
-  const int nF = g.nF * 128 * 6, nW = 2 * g.NP * g.KCG, nFP = g.nMT * 128 * 6, nFY = 48 * (n / 8);
+  const int nF = g.nF * 128 * 5, nW = 2 * g.NP * g.KCG, nFP = g.nMT * 128 * 6, nFY = 48 * (n / 8);
   int nMX[3], tot = nF + nW + nFP + nFY;
   for (int l = 0; l < 3; ++l) { nMX[l] = kModes2 * C.NM[l] * (C.KM / 8); tot += nMX[l]; }
   for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(256) k_px_prep(const PxPrepArgs a) {
     unsigned char* dst;
     uint32_t half, off;
     int u = t;
-    if (u < nF) {                                  // F[f][p][k'] K-major (M = p, K = k')
-      const int f = u / (128 * 6), rem = u % (128 * 6), p = rem % 128, kg = rem / 128;
+    if (u < nF) {                                  // F[f][k'/8][p/8][p%8][k'%8] (k' < 40)
+      const int f = u / (128 * 5), rem = u % (128 * 5), p = rem % 128, kg = rem / 128;
       const int j = n < 128 ? p % n : f * 128 + p;
       const int row = n < 128 ? p / n : 0;
       const bool keep = n >= 128 || f == 0 || (f == 1 && row == 0) || (f == 2 && row == 1);
@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) k_px_prep(const PxPrepArgs a) {
         if (keep && kp < 2 * kModes) { const float2 z = a.F[(size_t)j * kModes + (kp >> 1)]; v[q] = (kp & 1) ? z.y : z.x; }
       }
       dst = a.out + C.F + (size_t)f * 2 * C.f_half; half = C.f_half;
-      off = (uint32_t)(p >> 3) * 768u + (uint32_t)kg * 128u + (uint32_t)(p & 7) * 16u;
+      off = (uint32_t)kg * 2048u + (uint32_t)(p >> 3) * 128u + (uint32_t)(p & 7) * 16u;
     } else if ((u -= nF) < nW) {                   // W[l][o][c] K-major B (N = o, K = c)
       const int l = u / (g.NP * g.KCG), rem = u % (g.NP * g.KCG), o = rem % g.NP, cg = rem / g.NP;
 #pragma unroll
@@ -193,38 +193,40 @@ constexpr int kPxMaxSys = 4096;
 constexpr uint32_t kPxSmemLimit = 227u * 1024u;
 
 // Shared-memory plan: NST V stages (the tile's v' is written back in place) and GST G stages, 3 each
-// when they fit the 227 KB opt-in limit, else 2.
+// when they fit the 227 KB opt-in limit, else 2.  Padding channel group CGS (w odd-eighths) and G's
+// k-group 5 (k' 40..47) are read from one shared zero block (per-step descriptor LBO), not stored.
 struct PxSmem {
-  uint32_t ST, GS, RK, WB, FB, bias, w1e, dw, pj, bar, tptr, runb, total, stage_bytes, gs_bytes;
+  uint32_t ST, GS, RK, WB, FB, ZB, misc, bias, w1e, dw, bar, tptr, runb, pj, total, stage_bytes, gs_bytes;
   int NST, GST;
-  __host__ __device__ PxSmem(const PxGeom& g, bool first) {
+  __host__ __device__ PxSmem(const PxGeom& g, bool first, bool proj) {
     stage_bytes = 2u * g.stage_half();
-    gs_bytes = (uint32_t)g.RT * 12u * (uint32_t)g.LBO_G;   // per stage: RT rows x [hi 6 k-groups | lo 6]
+    gs_bytes = (uint32_t)g.RT * 10u * (uint32_t)g.LBO_G;   // per stage: RT rows x [hi 5 k-groups | lo 5]
     for (NST = 3; NST >= 2; --NST) {
       for (GST = 3; GST >= 2; --GST) {
-        plan(g, first);
+        plan(g, first, proj);
         if (total <= kPxSmemLimit) return;
       }
     }
     NST = GST = 2;
-    plan(g, first);
+    plan(g, first, proj);
   }
-  __host__ __device__ void plan(const PxGeom& g, bool first) {
+  __host__ __device__ void plan(const PxGeom& g, bool first, bool proj) {
     uint32_t o = 0;
-    auto take = [&](uint32_t bytes) { const uint32_t at = o; o = (o + bytes + 1023) & ~1023u; return at; };
-    ST = take((uint32_t)NST * stage_bytes);
-    GS = take((uint32_t)GST * gs_bytes);
-    RK = take(first ? (uint32_t)NST * 2048u : 16u);
-    WB = take(first ? 16u : 2u * (uint32_t)g.NP * g.NP * 2u);
-    FB = take((uint32_t)g.nF * 2u * 128u * 48u * 2u);
-    bias = take(128 * 4);
-    w1e = take(256 * 4);
-    dw = take(128 * 4);
-    pj = take(3u * kPxE1Groups * 128u * 4u);   // layer 3: per-group projection partials, per stage
-    bar = take(256);
+    auto take = [&](uint32_t bytes, uint32_t al) { const uint32_t at = (o + al - 1) & ~(al - 1); o = at + bytes; return at; };
+    ST = take((uint32_t)NST * stage_bytes, 1024);
+    GS = take((uint32_t)GST * gs_bytes, 1024);
+    RK = first ? take((uint32_t)NST * 2048u, 128) : 0u;
+    WB = first ? 0u : take(2u * (uint32_t)g.NP * g.NP * 2u, 1024);
+    FB = take((uint32_t)g.nF * 2u * 5u * 2048u, 1024);
+    ZB = take(2048, 1024);                     // zero block (after every descriptor start: LBO > 0)
+    bias = take(128 * 4, 16);
+    w1e = first ? take(256 * 4, 16) : 0u;
+    dw = proj ? take(128 * 4, 16) : 0u;
+    bar = take(256, 16);
     tptr = bar + 248;
-    runb = take(kPxMaxSys / 8);
-    total = o;
+    runb = take(kPxMaxSys / 8, 16);
+    pj = proj ? take(2u * kPxE1Groups * 128u * 4u, 16) : 0u;   // layer 3: per-group projection partials
+    total = (o + 15) & ~15u;
     // the x-analysis reads its A (a stage tile, MN-major, M = 128 channels) over 16 channel groups:
     // rows o >= NP read whatever follows (their results are ignored), which must lie inside the smem
     const uint32_t reach = ST + (uint32_t)(NST - 1) * stage_bytes + g.stage_half() + 16u * 2048u;
@@ -234,7 +236,7 @@ struct PxSmem {
 
 struct PxLayerArgs {
   int n, w, B, layer, use_gelu;
-  const double* r; const double* rr; const double* k;   // layer 1 inputs (fp64)
+  const double* r; const double* rr; const double* k;   // layer 1 inputs (fp64; rr = 1/||r|| per system)
   const unsigned char* vin;                              // V blobs (layers 2, 3)
   unsigned char* vout;                                   // V blobs of the next layer (layers 1, 2)
   const unsigned char* G;                                // G (interleaved rows; read by TMA through gmap)
@@ -264,7 +266,7 @@ template <bool FIRST, bool PROJ>
 __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a, const __grid_constant__ CUtensorMap gmap) {
   const PxGeom g(a.n, a.w);
   const PxConst C(g);
-  const PxSmem L(g, FIRST);
+  const PxSmem L(g, FIRST, PROJ);
   const int NST = L.NST, GST = L.GST;
   extern __shared__ __align__(1024) unsigned char sm[];
   const int n = a.n, N = n * n, w = a.w, NP = g.NP;
@@ -296,11 +298,11 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
     tc::bulk_g2s(sm + L.FB, a.cst + C.F, fbytes, cstb);
     if (!FIRST) tc::bulk_g2s(sm + L.WB, a.cst + C.W[a.layer - 1], 2u * C.w_half, cstb);
   }
-  {   // stages and G stages zeroed: padding channel groups and k-group 5 (k' 40..47) must read as zeros
+  {   // stages zeroed (layer-1 tiles are produced in place) and the zero block
     uint4* z = reinterpret_cast<uint4*>(sm + L.ST);
     for (uint32_t t = tid; t < ((uint32_t)NST * L.stage_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
-    z = reinterpret_cast<uint4*>(sm + L.GS);
-    for (uint32_t t = tid; t < ((uint32_t)GST * L.gs_bytes) / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
+    z = reinterpret_cast<uint4*>(sm + L.ZB);
+    for (uint32_t t = tid; t < 2048u / 16u; t += blockDim.x) z[t] = make_uint4(0, 0, 0, 0);
   }
   for (int o = tid; o < 128; o += blockDim.x) {
     sbias[o] = o < w ? a.bias[o] : 0.f;
@@ -333,7 +335,7 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
     return u;
   };
   const uint32_t base = tc::smem_u32(sm);
-  const uint32_t sth0 = base + L.ST, fb0 = base + L.FB, gs0 = base + L.GS, wb0 = base + L.WB;
+  const uint32_t sth0 = base + L.ST, fb0 = base + L.FB, gs0 = base + L.GS, wb0 = base + L.WB, zb0 = base + L.ZB;
   const uint32_t sh = g.stage_half(), fh = C.f_half, LG = (uint32_t)g.LBO_G, KCG = (uint32_t)g.KCG;
 
   if (warp == 0 || warp == 2) {
@@ -365,10 +367,10 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
             tc::mbar_wait(&gempty[gs], ((uint32_t)(t / GST) & 1u) ^ 1u);
             tc::mbar_expect_tx(&gfull[gs], (uint32_t)g.RT * 2u * g.g_half());
             for (int r = 0; r < g.RT; ++r) {   // G row i: hi and lo boxes of the interleaved layout
-              unsigned char* gdst = sm + L.GS + (uint32_t)gs * L.gs_bytes + (uint32_t)r * 12u * g.LBO_G;
+              unsigned char* gdst = sm + L.GS + (uint32_t)gs * L.gs_bytes + (uint32_t)r * 10u * g.LBO_G;
               const int i = ul * g.RT + r;
               tc::tma_load_5d(gdst, &gmap, 0, i, 0, 0, 2 * b, &gfull[gs]);
-              tc::tma_load_5d(gdst + 6u * g.LBO_G, &gmap, 0, i, 0, 0, 2 * b + 1, &gfull[gs]);
+              tc::tma_load_5d(gdst + 5u * g.LBO_G, &gmap, 0, i, 0, 0, 2 * b + 1, &gfull[gs]);
             }
           }
         }
@@ -392,26 +394,28 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
           const uint32_t d1 = tmem + (uint32_t)d * NP;
           const uint32_t sth = sth0 + (uint32_t)s * L.stage_bytes, stl = sth + sh;
           uint32_t acc = 0;
-          if (!FIRST) {   // bypass: K = channels, 16 per step
+          if (!FIRST) {   // bypass: K = channels, 16 per step (an odd last group pairs with the zero block)
             for (uint32_t ks = 0; ks < KCG / 2; ++ks)
 #pragma unroll
               for (int p = 0; p < 3; ++p) {
                 const uint32_t aa = (p == 2 ? stl : sth) + ks * 4096u;
+                const uint32_t lbo = (2 * ks + 1 < (uint32_t)g.CGS) ? 2048u : zb0 - aa;
                 const uint32_t bb = wb0 + (p == 1 ? C.w_half : 0u) + ks * 256u;
-                tc::mma_bf16(d1, tc::make_sdesc(aa, 2048, 128), tc::make_sdesc(bb, 128, KCG * 128u), id1, acc);
+                tc::mma_bf16(d1, tc::make_sdesc(aa, lbo, 128), tc::make_sdesc(bb, 128, KCG * 128u), id1, acc);
                 acc = 1;
               }
           }
           const uint32_t gsb = gs0 + (uint32_t)gs * L.gs_bytes;
-          for (int r = 0; r < g.RT; ++r) {   // x-synthesis: K = k' (40 of 48), per row of the tile
+          for (int r = 0; r < g.RT; ++r) {   // x-synthesis: K = k' (40 of 48; k-group 5 from the zero block)
             const uint32_t fbr = fb0 + (uint32_t)(g.RT == 2 ? 1 + r : cb) * 2u * fh;
-            const uint32_t gh = gsb + (uint32_t)r * 12u * LG, gl = gh + 6u * LG;
+            const uint32_t gh = gsb + (uint32_t)r * 10u * LG, gl = gh + 5u * LG;
             for (int ks = 0; ks < 3; ++ks)
 #pragma unroll
               for (int p = 0; p < 3; ++p) {
-                const uint32_t aa = fbr + (p == 2 ? fh : 0u) + (uint32_t)ks * 256u;
+                const uint32_t aa = fbr + (p == 2 ? fh : 0u) + (uint32_t)ks * 4096u;
                 const uint32_t bb = (p == 1 ? gl : gh) + (uint32_t)ks * 2u * LG;
-                tc::mma_bf16(d1, tc::make_sdesc(aa, 128, 768), tc::make_sdesc(bb, LG, 128), id2, acc);
+                tc::mma_bf16(d1, tc::make_sdesc(aa, ks < 2 ? 2048u : zb0 - aa, 128), tc::make_sdesc(bb, ks < 2 ? LG : zb0 - bb, 128),
+                             id2, acc);
                 acc = 1;
               }
           }
@@ -443,8 +447,8 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
                 for (int p = 0; p < 3; ++p) {
                   const int kk = r * 4 + ks;
                   const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)kk * 256u;
-                  const uint32_t bb = fb0 + (p == 1 ? fh : 0u) + (uint32_t)kk * 2u * 768u;
-                  tc::mma_bf16(d2 + (uint32_t)r * 48u, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3,
+                  const uint32_t bb = fb0 + (p == 1 ? fh : 0u) + (uint32_t)kk * 256u;
+                  tc::mma_bf16(d2 + (uint32_t)r * 48u, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 128, 2048), id3,
                                (ks | p) != 0);
                 }
           } else {
@@ -453,8 +457,8 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
 #pragma unroll
               for (int p = 0; p < 3; ++p) {
                 const uint32_t aa = (p == 2 ? stl : sth) + (uint32_t)ks * 256u;
-                const uint32_t bb = fbc + (p == 1 ? fh : 0u) + (uint32_t)ks * 2u * 768u;
-                tc::mma_bf16(d2, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 768, 128), id3, (cb | ks | p) != 0);
+                const uint32_t bb = fbc + (p == 1 ? fh : 0u) + (uint32_t)ks * 256u;
+                tc::mma_bf16(d2, tc::make_sdesc(aa, 128, 2048), tc::make_sdesc(bb, 128, 2048), id3, (cb | ks | p) != 0);
               }
           }
           tc::mma_commit(&empty[s]);                       // stage t consumed
@@ -471,16 +475,17 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
     const uint32_t lane_off = (uint32_t)(q4 * 32) << 16;
     const uint32_t poff = (uint32_t)(p >> 3) * 128u + (uint32_t)(p & 7) * 16u;
     int t = 0;
-    for (int u = next_unit(blockIdx.x); u < nunits; u = next_unit(u + gridDim.x)) {
+    int u = next_unit(blockIdx.x);
+    double inv_next = (FIRST && u < nunits) ? __ldg(a.rr + u / g.units) : 0.0;   // 1/||r|| of the next unit, in flight
+    for (int un; u < nunits; u = un) {
       const int b = u / g.units, ul = u % g.units;
+      un = next_unit(u + gridDim.x);
       float rh = 0.f, kf = 0.f;
-      double inv_s = 0.0;
-      if (FIRST) {
-        const double sr = sqrt(a.rr[b]);
-        inv_s = sr > 0.0 ? 1.0 / sr : 0.0;
-      }
+      const double inv_s = inv_next;
+      if (FIRST && un < nunits) inv_next = __ldg(a.rr + un / g.units);
       for (int cb = 0; cb < g.CB; ++cb, ++t) {
         const int s = t % NST, d = t & 1;
+        if (lane == 0 && q4 == 0 && eg == 0) PX_TRACE(t, 6);
         tc::mbar_wait(&d1full[d], (uint32_t)(t >> 1) & 1u);
         if (lane == 0 && q4 == 0 && eg == 0) PX_TRACE(t, 3);
         tc::fence_after_sync();
@@ -513,11 +518,13 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
             const uint32_t off = (uint32_t)cg * 2048u + poff;
             uint4 hv, lv;
             tc::split8(v + 8 * h, hv, lv);
-            *reinterpret_cast<uint4*>(sth + off) = hv;
-            *reinterpret_cast<uint4*>(stl + off) = lv;
-            if (!PROJ && cg < g.CGS) {   // the next layer's V blob (16-byte stores, 512 B per warp)
-              *reinterpret_cast<uint4*>(gv + off) = hv;
-              *reinterpret_cast<uint4*>(gv + g.v_half() + off) = lv;
+            if (cg < g.CGS) {   // stage (in place) and the next layer's V blob (16-byte stores, 512 B per warp)
+              *reinterpret_cast<uint4*>(sth + off) = hv;
+              *reinterpret_cast<uint4*>(stl + off) = lv;
+              if (!PROJ) {
+                *reinterpret_cast<uint4*>(gv + off) = hv;
+                *reinterpret_cast<uint4*>(gv + g.v_half() + off) = lv;
+              }
             }
           }
         }
@@ -527,12 +534,12 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
         tc::mbar_arrive(&vfull[s]);
         if (lane == 0 && q4 == 0) PX_TRACE(t, eg == 0 ? 4 : (eg == 1 ? 9 : 8));
         if (PROJ) {   // sum_o (D W4)[o] v3[o]: the groups' partials added in a fixed order
-          pj[((size_t)s * kPxE1Groups + eg) * 128 + p] = pacc;
+          pj[((size_t)d * kPxE1Groups + eg) * 128 + p] = pacc;
           tc::named_sync(1, 32u * kPxE1Warps);
           if (eg == 0) {
             float acc = 0.f;
 #pragma unroll
-            for (int q = 0; q < kPxE1Groups; ++q) acc += pj[((size_t)s * kPxE1Groups + q) * 128 + p];
+            for (int q = 0; q < kPxE1Groups; ++q) acc += pj[((size_t)d * kPxE1Groups + q) * 128 + p];
             a.p3[(size_t)b * N + (size_t)(ul * g.CB + cb) * 128 + p] = acc;
           }
         }
@@ -1067,7 +1074,8 @@ bool px_supported_shape(int n, int w) {
   if (w < 1 || w > 128) return false;
   if (!(n == 64 || (n % 128 == 0 && n >= 128 && n <= 512))) return false;
   const PxGeom g(n, w);
-  return PxSmem(g, true).total <= kPxSmemLimit && PxSmem(g, false).total <= kPxSmemLimit &&
+  return PxSmem(g, true, false).total <= kPxSmemLimit && PxSmem(g, false, false).total <= kPxSmemLimit &&
+         PxSmem(g, false, true).total <= kPxSmemLimit &&
          PxYsynSmem(g).total <= kPxSmemLimit && PxYanSmem(g).total <= kPxSmemLimit;
 }
 
@@ -1147,7 +1155,7 @@ cudaError_t launch_px_layer(const PxLayerHost& h, cudaStream_t s) {
   a.trace = trace_layer == h.layer + 1;
   const PxGeom g(h.n, h.w);
   const bool first = h.layer == 0, proj = h.layer == 2;
-  const size_t smem = PxSmem(g, first).total;
+  const size_t smem = PxSmem(g, first, proj).total;
   const int grid = std::min(h.B * g.units, px_sms());
   alignas(64) CUtensorMap gmap;
   if (const cudaError_t e = make_g_map(&gmap, h.G, g, h.B)) return e;

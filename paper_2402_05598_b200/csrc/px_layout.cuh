@@ -41,7 +41,9 @@ struct PxGeom {
   }
   __host__ __device__ uint32_t v_half() const { return (uint32_t)CGS * 2048u; }      // stored hi (= lo) of a V tile
   __host__ __device__ uint32_t g_half() const { return 5u * (uint32_t)LBO_G; }      // stored hi (= lo) of a G row
-  __host__ __device__ uint32_t stage_half() const { return (uint32_t)KCG * 2048u; }  // smem hi (= lo) of a stage tile
+  // smem hi (= lo) of a stage tile: the stored channel groups only; the bypass GEMM reads an odd last
+  // group's partner (channels CGS*8 .. KCG*8) from a shared zero block instead
+  __host__ __device__ uint32_t stage_half() const { return (uint32_t)CGS * 2048u; }
   __host__ __device__ size_t v_bytes(int B) const { return (size_t)B * TPS * 2 * v_half(); }
   __host__ __device__ size_t g_bytes(int B) const { return (size_t)B * n * 2 * g_half(); }
   __host__ __device__ size_t t_floats(int B) const { return (size_t)B * n * 40 * w + 256; }   // + over-read pad
@@ -52,9 +54,10 @@ struct PxGeom {
 };
 
 // Constant operand blobs, built once per NO apply / solve by k_px_prep ([hi][lo] each):
-//   F[f]    twiddles F[p][k'] = (cos, -sin)(2 pi kappa2 j(p) / n), K-major A (M = p, K = k' 48):
-//           the x-synthesis basis and, read MN-major, the x-analysis B.  n = 64: f = 0 unmasked,
-//           f = 1 / 2 zero outside the tile's first / second row (per-row synthesis).
+//   F[f]    twiddles F[p][k'] = (cos, -sin)(2 pi kappa2 j(p) / n) for k' < 40, k-group-major
+//           [k'/8][p/8][p%8][k'%8] (5 k-groups of 2048 B; k' 40..47 read from the layer's zero block):
+//           the x-synthesis A (K-major, M = p) and, read MN-major, the x-analysis B.  n = 64: f = 0
+//           unmasked, f = 1 / 2 zero outside the tile's first / second row (per-row synthesis).
 //   W[l]    layer weights W[o][c] (layers 2, 3), K-major B (N = o, K = c), NP x NP.
 //   FP[mt]  y-synthesis A: Fp[i][(kappa1, re|im)], K-major (M = i, K = 48), per 128-row M tile.
 //   FY      y-analysis B: F[i][(kappa1, x|y)], K-major (N = 48, K = i).
@@ -66,7 +69,7 @@ struct PxConst {
   __host__ __device__ PxConst(const PxGeom& g) {
     size_t o = 0;
     auto take = [&](size_t bytes) { const size_t at = o; o = (o + bytes + 1023) & ~size_t(1023); return at; };
-    f_half = 128u * 48u * 2u;
+    f_half = 5u * 2048u;
     F = take((size_t)g.nF * 2 * f_half);
     w_half = (uint32_t)g.NP * g.NP * 2u;
     W[0] = take(2 * (size_t)w_half);

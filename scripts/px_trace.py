@@ -33,7 +33,7 @@ F._check(F._lib.fcgno_debug_px_trace(buf.ctypes.data_as(ctypes.c_void_p), 640))
 t = buf.reshape(64, 10).astype(np.float64)
 t0 = t[0, 0]
 mhz = 1965.0
-names = ["ld_issue", "mma_full", "d1_commit", "e1_start", "e1g0_done", "mma3", "st_done", "e2_done", "e1g2_done",
+names = ["ld_issue", "mma_full", "d1_commit", "e1_start", "e1g0_done", "mma3", "e1_pre", "e2_done", "e1g2_done",
          "e1g1_done"]
 print("tile " + " ".join(f"{n:>10s}" for n in names))
 for i in range(24):
