@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FCGNO_ABI_VERSION 5
+#define FCGNO_ABI_VERSION 6
 #define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
 #define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
 #define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
@@ -216,6 +216,25 @@ FCGNO_API size_t fcgno_notay_workspace_bytes(fcgno_grid g, const fcgno_no_desc* 
 FCGNO_API int fcgno_notay_ratio(const fcgno_problem* p, const fcgno_no_desc* d_or_null, const void* packed,
                       const double* r, const double* e, int optimal_scale, double* eps, void* ws,
                       size_t ws_bytes, void* stream);
+
+/* Classical stationary preconditioners of the paper's comparison (§3.3.1): k sweeps
+ * from x^0 = 0 with b = r of
+ *   FCGNO_PRECOND_JACOBI   Jacobi, Eq. 15: x <- x + D(A)^{-1} (r - A x)
+ *   FCGNO_PRECOND_SGS_RB   symmetric Gauss-Seidel, x <- x + L(A)^{-1} (r - A x), x <- x + U(A)^{-1} (r - A x),
+ *                          with L, U the triangular parts of A in red-black node order (colour (i + j) mod 2,
+ *                          red first; R22): each triangular solve is two colour half sweeps
+ * every update x_e <- x_e + (r_e - (A x)_e) / a_ee in the canonical stencil order (R23), fp64.
+ *   sweeps 1..64.  fcgno_apply_stationary: w = B(r) for every system (r, w [B][n][n] fp64 device,
+ *   w != r; ws of fcgno_stationary_workspace_bytes(g) bytes).  fcgno_fcg_solve_stationary:
+ *   Algorithm 1 with w_i = B(r_i); arguments as fcgno_fcg_solve. */
+typedef enum { FCGNO_PRECOND_JACOBI = 1, FCGNO_PRECOND_SGS_RB = 2 } fcgno_precond_kind;
+FCGNO_API size_t fcgno_stationary_workspace_bytes(fcgno_grid g);
+FCGNO_API int fcgno_apply_stationary(const fcgno_problem* p, int kind, int sweeps, const double* r, double* w, void* ws,
+                           size_t ws_bytes, void* stream);
+FCGNO_API size_t fcgno_solve_stationary_workspace_bytes(fcgno_grid g, fcgno_solve_opts o);
+FCGNO_API int fcgno_fcg_solve_stationary(const fcgno_problem* p, int kind, int sweeps, const double* f, double* u,
+                               fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, void* ws,
+                               size_t ws_bytes, void* stream);
 
 /* End-to-end convenience entry point with HOST buffers ([host], pageable or pinned): copies
  * k, f, u0 to the device, assembles, solves and copies u, iters, status (and history if

@@ -20,10 +20,11 @@ from .no import (K_MODES, mode_indices, analysis, synthesis, gelu, unpack_weight
                  param_count)
 from .fcg import m_schedule, fcg, cg, CONVERGED, MAXIT, BREAKDOWN, NONFINITE, RUNNING
 from .notay import a_norm, notay_ratio, notay_ratio_scaled, notay_curve
+from .classical import diagonal, jacobi, sgs
 
 __all__ = [
     "h_of", "harmonic", "faces", "apply_A", "dense_A", "two_product", "dot", "norm2",
     "K_MODES", "mode_indices", "analysis", "synthesis", "gelu", "unpack_weights", "no_forward",
     "param_count", "m_schedule", "fcg", "cg", "CONVERGED", "MAXIT", "BREAKDOWN", "NONFINITE",
-    "RUNNING", "a_norm", "notay_ratio", "notay_ratio_scaled", "notay_curve",
+    "RUNNING", "a_norm", "notay_ratio", "notay_ratio_scaled", "notay_curve", "diagonal", "jacobi", "sgs",
 ]

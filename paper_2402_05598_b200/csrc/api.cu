@@ -489,7 +489,8 @@ struct SolveWs {
   double* wvec;
 };
 
-SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgno_solve_opts& o, bool diag = false) {
+SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgno_solve_opts& o, bool diag = false,
+                    bool stationary = false) {
   SolveWs s{};
   const size_t N = (size_t)n * n;
   const int nblk = nblk_of(n);
@@ -499,7 +500,11 @@ SolveWs carve_solve(Carver& c, int n, int B, const fcgno_no_desc* nd, const fcgn
   const size_t es = o.vec_fp32 ? sizeof(float) : sizeof(double);
   d.vec32 = o.vec_fp32 ? 1 : 0;
   d.r = reinterpret_cast<double*>(c.take<unsigned char>(es * B * N));
-  s.wvec = nd ? reinterpret_cast<double*>(c.take<unsigned char>(es * B * N)) : nullptr;
+  s.wvec = (nd || stationary) ? reinterpret_cast<double*>(c.take<unsigned char>(es * B * N)) : nullptr;
+  if (stationary) {   // classical preconditioner sweep iterates (fp64)
+    d.st_xa = c.take<double>(B * N);
+    d.st_xb = c.take<double>(B * N);
+  }
   d.r64 = (nd && o.vec_fp32) ? c.take<double>(B * N) : nullptr;
   d.ring_p = reinterpret_cast<double*>(c.take<unsigned char>(es * (o.m + 1) * B * N));
   d.ring_s = reinterpret_cast<double*>(c.take<unsigned char>(es * (o.m + 1) * B * N));
@@ -616,6 +621,12 @@ int enqueue_iteration(const FcgDev& d, const fcgno_no_desc* nd, const void* pack
     if (e != cudaSuccess) return -1;
     count += nl;
   } else {
+    if (d.st_kind) {   // w = Jacobi(k) / SGS(k) r, then the window dots of w
+      if (launch_stationary(d.k, d.r, d.st_xa, d.st_xb, const_cast<double*>(d.w), d.vec32 != 0, d.n, d.B, d.kfast != 0,
+                            d.st_kind, d.st_sweeps, d.status, s) != cudaSuccess)
+        return -1;
+      count += d.st_kind == FCGNO_PRECOND_JACOBI ? d.st_sweeps : 4 * d.st_sweeps;
+    }
     pb(PROF_WINDOW);
     if (launch_window_dots(d, s) != cudaSuccess) return -1;
     pe(PROF_WINDOW);
@@ -794,20 +805,62 @@ bool host_loop_forced() {
 
 namespace {
 struct DiagArgs { const double* u_star; double* eps; double* err_a; };
+struct StationaryArgs { int kind, sweeps; };
 
-size_t solve_ws_bytes(fcgno_grid g, const fcgno_no_desc* nd, const fcgno_solve_opts& o, bool diag) {
+size_t solve_ws_bytes(fcgno_grid g, const fcgno_no_desc* nd, const fcgno_solve_opts& o, bool diag, bool stationary = false) {
   if (g.n < 2 || g.batch < 1 || check_opts(o) != FCGNO_OK) return 0;
   if (nd && check_desc(*nd) != FCGNO_OK) return 0;
   Carver c(nullptr);
   const LaneSplit L = lane_split(g.batch);
-  for (int l = 0; l < L.n; ++l) carve_solve(c, g.n, L.nb[l], nd, o, diag);
+  for (int l = 0; l < L.n; ++l) carve_solve(c, g.n, L.nb[l], nd, o, diag, stationary);
   return c.bytes();
 }
 
 int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* f, double* u,
                fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, const DiagArgs* dg, void* ws,
-               size_t ws_bytes, void* stream);
+               size_t ws_bytes, void* stream, const StationaryArgs* st = nullptr);
+
+int check_stationary(int kind, int sweeps) {
+  if (kind != FCGNO_PRECOND_JACOBI && kind != FCGNO_PRECOND_SGS_RB) return fail(FCGNO_EINVAL, "unknown classical preconditioner %d", kind);
+  if (sweeps < 1 || sweeps > 64) return fail(FCGNO_EINVAL, "sweeps=%d outside [1, 64]", sweeps);
+  return FCGNO_OK;
+}
 }  // namespace
+
+size_t fcgno_solve_stationary_workspace_bytes(fcgno_grid g, fcgno_solve_opts o) {
+  return solve_ws_bytes(g, nullptr, o, false, true);
+}
+
+int fcgno_fcg_solve_stationary(const fcgno_problem* p, int kind, int sweeps, const double* f, double* u,
+                               fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, void* ws,
+                               size_t ws_bytes, void* stream) {
+  if (int e = check_stationary(kind, sweeps)) return e;
+  const StationaryArgs st{kind, sweeps};
+  return solve_impl(p, nullptr, nullptr, f, u, o, iters, status, history, nullptr, ws, ws_bytes, stream, &st);
+}
+
+size_t fcgno_stationary_workspace_bytes(fcgno_grid g) {
+  if (g.n < 2 || g.batch < 1) return 0;
+  Carver c(nullptr);
+  c.take<double>((size_t)g.batch * g.n * g.n);
+  c.take<double>((size_t)g.batch * g.n * g.n);
+  return c.bytes();
+}
+
+int fcgno_apply_stationary(const fcgno_problem* p, int kind, int sweeps, const double* r, double* w, void* ws,
+                           size_t ws_bytes, void* stream) {
+  if (!p || !r || !w || !ws) return fail(FCGNO_EINVAL, "apply_stationary: NULL argument");
+  if (r == w) return fail(FCGNO_EINVAL, "apply_stationary: w must not alias r");
+  if (int e = check_stationary(kind, sweeps)) return e;
+  fcgno_grid g{p->n, p->B};
+  if (!aligned(ws) || ws_bytes < fcgno_stationary_workspace_bytes(g)) return fail(FCGNO_EWORKSPACE, "apply_stationary: workspace");
+  Carver c(ws);
+  double* xa = c.take<double>((size_t)p->B * p->n * p->n);
+  double* xb = c.take<double>((size_t)p->B * p->n * p->n);
+  CK(launch_stationary(p->k, r, xa, xb, w, false, p->n, p->B, p->kfast, kind, sweeps, nullptr,
+                       static_cast<cudaStream_t>(stream)));
+  return FCGNO_OK;
+}
 
 size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* nd, fcgno_solve_opts o) {
   return solve_ws_bytes(g, nd, o, false);
@@ -835,7 +888,7 @@ int fcgno_fcg_solve_diag(const fcgno_problem* p, const fcgno_no_desc* nd, const 
 namespace {
 int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* packed, const double* f, double* u,
                fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, const DiagArgs* dg, void* ws,
-               size_t ws_bytes, void* stream) {
+               size_t ws_bytes, void* stream, const StationaryArgs* sta) {
   if (!p || !f || !u || !iters || !status || !ws) return fail(FCGNO_EINVAL, "fcg_solve: NULL argument");
   if (int e = check_opts(o)) return e;
   if (nd) {
@@ -845,7 +898,7 @@ int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* pack
     if (int e = check_no_smem(*nd, p->n)) return e;
   }
   fcgno_grid g{p->n, p->B};
-  if (!aligned(ws) || ws_bytes < solve_ws_bytes(g, nd, o, dg != nullptr)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
+  if (!aligned(ws) || ws_bytes < solve_ws_bytes(g, nd, o, dg != nullptr, sta != nullptr)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
   if (nd) {
     if (nd->precision == FCGNO_FP64) CK(prepare_no_kernels<double>());
     else { CK(prepare_no_kernels<float>()); CK(prepare_px_kernels()); }
@@ -864,12 +917,13 @@ int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* pack
     ln.p.k = p->k + b0 * N;
     if (p->khat32) ln.p.khat32 = p->khat32 + (size_t)b0 * kModes2 * 2;
     if (p->khat64) ln.p.khat64 = p->khat64 + (size_t)b0 * kModes2 * 2;
-    ln.sw = carve_solve(c, p->n, nb, nd, o, dg != nullptr);
+    ln.sw = carve_solve(c, p->n, nb, nd, o, dg != nullptr, sta != nullptr);
     FcgDev& d = ln.sw.d;
     d.n = p->n; d.B = nb; d.N = p->n * p->n; d.nblk = nblk_of(p->n);
     d.m = o.m; d.maxit = o.maxit; d.schedule = o.schedule; d.tol = o.tol;
     d.scale = double(p->n + 1) * double(p->n + 1);
-    d.k = ln.p.k; d.kfast = p->kfast ? 1 : 0; d.f = f + b0 * N; d.u = u + b0 * N; d.w = nd ? ln.sw.wvec : d.r;
+    d.k = ln.p.k; d.kfast = p->kfast ? 1 : 0; d.f = f + b0 * N; d.u = u + b0 * N; d.w = (nd || sta) ? ln.sw.wvec : d.r;
+    if (sta) { d.st_kind = sta->kind; d.st_sweeps = sta->sweeps; }
     d.status = status + b0; d.iters = iters + b0;
     d.hist = history ? history + (size_t)b0 * (o.maxit + 1) : nullptr;
     if (dg) {

@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kStThreads, 4) k_apply_A(const double* __restr
   st_fill_end();
   const StWalk<RG> w(g);
   const double none[RG] = {};
-  st_walk_any<RG>(fast, g, w, n, scale, sx, sk, sbnd, none, [&](bool ok, int e, double, double v, double) {
+  st_walk_any<RG>(fast, g, w, n, scale, sx, sk, sbnd, none, [&](bool ok, int e, double, double v, double, double) {
     if (ok) yb[e] = v;
   });
 }
@@ -91,6 +91,83 @@ cudaError_t launch_apply_A(const double* k, const double* x, double* y, int n, i
   if (e != cudaSuccess) return e;
   ++launch_counter();
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ classical stationary preconditioners
+// Jacobi(k) (Eq. 15) and symmetric Gauss-Seidel(k) in red-black order (readings
+// R22-R24) as stencil sweeps over the 2-D tiles.  One launch = one sweep over the nodes of `colour`
+// (-1: every node, a Jacobi sweep x -> xout; 0 / 1: a red / black half sweep, in place):
+//   x_e <- x_e + (z_e - (A x)_e) / a_ee                  (R23; x = 0 on the first sweep)
+// and, on the last sweep, w = the new x at every node, stored in the FCG vector type V.
+template <int RG, bool PAIRS, typename V>
+__global__ void __launch_bounds__(kStThreads, 4) k_stationary(const double* __restrict__ k, const V* __restrict__ z,
+                                                              const double* x, double* xout, V* __restrict__ w, int n,
+                                                              double scale, int fast, int colour, int first,
+                                                              const int* __restrict__ status) {
+  pdl_wait();
+  pdl_trigger();
+  ST_SMEM;
+  const int b = blockIdx.y;
+  if (status && status[b] != SYS_RUNNING) return;
+  const size_t N = (size_t)n * n;
+  const StGeo g = st_geo(n);
+  st_copy<PAIRS>(g, n, k + b * N, sk);
+  if (first) {
+    for (int t = threadIdx.x; t < (kStR + 2) * kStSP; t += blockDim.x) sx[t] = 0.0;
+  } else {
+    st_copy<PAIRS>(g, n, x + b * N, sx);
+  }
+  st_fill_end();
+  const StWalk<RG> wk(g);
+  double zx[RG];
+  st_rows<RG, V>(g, wk, n, z + b * N, zx);
+  double* xo = xout + b * N;
+  V* wo = w ? w + b * N : nullptr;
+  st_walk_any<RG>(fast != 0, g, wk, n, scale, sx, sk, sbnd, zx, [&](bool ok, int e, double xc, double ax, double zv, double aee) {
+    if (!ok) return;
+    const int i = e / n, j = e - i * n;
+    const bool upd = colour < 0 || ((i + j) & 1) == colour;
+    const double v = upd ? __dadd_rn(xc, __ddiv_rn(__dsub_rn(zv, ax), aee)) : xc;
+    if (upd || first) xo[e] = v;
+    if (wo) wo[e] = (V)v;
+  });
+}
+
+template <typename V>
+static cudaError_t launch_stationary_t(const double* k, const V* z, double* xa, double* xb, V* w, int n, int B,
+                                       bool kfast, int kind, int sweeps, const int* status, cudaStream_t s) {
+  const dim3 grid((unsigned)st_tiles(n), (unsigned)B);
+  const double scale = double(n + 1) * double(n + 1);
+  cudaError_t e = cudaSuccess;
+  if (kind == 1) {   // Jacobi: sweeps x_{s-1} -> x_s, ping-pong
+    for (int sw = 0; sw < sweeps && e == cudaSuccess; ++sw) {
+      const double* xin = (sw & 1) ? xa : xb;
+      double* xo = (sw & 1) ? xb : xa;
+      ST_LAUNCH(e, n, V, k_stationary, grid, s, k, z, xin, xo, sw == sweeps - 1 ? w : nullptr, n, scale, kfast ? 1 : 0,
+                -1, sw == 0 ? 1 : 0, status);
+      ++launch_counter();
+    }
+  } else {           // red-black SGS: per sweep L^-1 (red, black) then U^-1 (black, red), in place
+    const int seq[4] = {0, 1, 1, 0};
+    for (int sw = 0; sw < sweeps && e == cudaSuccess; ++sw)
+      for (int h = 0; h < 4 && e == cudaSuccess; ++h) {
+        const bool last = sw == sweeps - 1 && h == 3;
+        ST_LAUNCH(e, n, V, k_stationary, grid, s, k, z, xa, xa, last ? w : nullptr, n, scale, kfast ? 1 : 0, seq[h],
+                  (sw == 0 && h == 0) ? 1 : 0, status);
+        ++launch_counter();
+      }
+  }
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stationary(const double* k, const void* z, double* xa, double* xb, void* w, bool v32, int n, int B,
+                              bool kfast, int kind, int sweeps, const int* status, cudaStream_t s) {
+  if (v32)
+    return launch_stationary_t<float>(k, static_cast<const float*>(z), xa, xb, static_cast<float*>(w), n, B, kfast, kind,
+                                      sweeps, status, s);
+  return launch_stationary_t<double>(k, static_cast<const double*>(z), xa, xb, static_cast<double*>(w), n, B, kfast,
+                                     kind, sweeps, status, s);
 }
 
 // ------------------------------------------------------------------ batched dot
@@ -179,7 +256,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k_init_residual(FcgDev d) {
   double fx[RG];
   st_rows(g, w, n, d.f + b * N, fx);
   double s = 0.0, c = 0.0;
-  st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, fx, [&](bool ok, int e, double, double v, double fv) {
+  st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, fx, [&](bool ok, int e, double, double v, double fv, double) {
     const double rv = ok ? rnd<V>(__dsub_rn(fv, v)) : 0.0;   // stored value (R21)
     if (ok) {
       rb[e] = (V)rv;
@@ -320,7 +397,7 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   st_rows<RG, V>(g, w, n, reinterpret_cast<const V*>(d.r) + b * N, rx);
   V* sout = reinterpret_cast<V*>(d.ring_s) + ((size_t)slot * d.B + b) * N;
   double s0 = 0.0, c0 = 0.0, s1 = 0.0, c1 = 0.0;
-  st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, rx, [&](bool ok, int e, double pv, double sv, double rv) {
+  st_walk_any<RG>(fast, g, w, n, d.scale, sx, sk, sbnd, rx, [&](bool ok, int e, double pv, double sv, double rv, double) {
     const double sr = rnd<V>(sv);   // s as stored (R21)
     if (ok) sout[e] = (V)sr;
     const double p = ok ? pv : 0.0, q = ok ? sr : 0.0;

@@ -42,6 +42,9 @@ struct FcgDev {
   int* iter;                  // global iteration counter
   int* active;                // systems still running (set by init, then by the last update CTA)
   unsigned* gcnt;             // [2] systems arrived in this update / of them still running
+  // classical preconditioner (fcgno_fcg_solve_stationary): kind 1 Jacobi, 2 red-black SGS, 0 none
+  int st_kind, st_sweeps;
+  double *st_xa, *st_xb;      // [B][N] sweep iterates
   // Theorem-1 diagnostics (fcgno_fcg_solve_diag; all nullptr otherwise)
   const double* dg_ustar;     // [B][N] reference solution u*
   double* dg_eps;             // [B][maxit] eps_i = ||w_i - e_i||_A / ||e_i||_A
@@ -136,6 +139,9 @@ cudaError_t launch_dot(const double* x, const double* y, double* out, dd* part, 
 cudaError_t launch_check_k(const double* k, size_t count, int* bad, cudaStream_t s);
 cudaError_t launch_init_residual(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_window_dots(const FcgDev& d, cudaStream_t s);
+// classical preconditioners (kind 1 = Jacobi, 2 = red-black SGS); z, w of the FCG vector type (v32)
+cudaError_t launch_stationary(const double* k, const void* z, double* xa, double* xb, void* w, bool v32, int n, int B,
+                              bool kfast, int kind, int sweeps, const int* status, cudaStream_t s);
 cudaError_t launch_pform_stencil(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_update(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_flush_x(const FcgDev& d, cudaStream_t s);

@@ -22,6 +22,7 @@ if not os.path.exists(LIB_PATH):
 _lib = ctypes.CDLL(LIB_PATH)
 
 FP32, FP64 = 0, 1
+JACOBI, SGS_RB = 1, 2   # classical preconditioners (fcgno_precond_kind)
 SCHEDULE_PAPER, SCHEDULE_SLIDING = 0, 1
 RUNNING, CONVERGED, MAXIT, BREAKDOWN, NONFINITE = 0, 1, 2, 3, 4
 K_MODES = 20
@@ -68,6 +69,10 @@ EXPORTS = {
     "fcgno_fcg_solve_diag": (_i, [_vp, _P(NoDesc), _vp, _vp, _vp, SolveOpts, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz,
                                   _vp]),
     "fcgno_notay_workspace_bytes": (_sz, [Grid, _P(NoDesc)]),
+    "fcgno_stationary_workspace_bytes": (_sz, [Grid]),
+    "fcgno_apply_stationary": (_i, [_vp, _i, _i, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_solve_stationary_workspace_bytes": (_sz, [Grid, SolveOpts]),
+    "fcgno_fcg_solve_stationary": (_i, [_vp, _i, _i, _vp, _vp, SolveOpts, _vp, _vp, _vp, _vp, _sz, _vp]),
     "fcgno_notay_ratio": (_i, [_vp, _P(NoDesc), _vp, _vp, _vp, _i, _vp, _vp, _sz, _vp]),
     "fcgno_solve_host_workspace_bytes": (_sz, [Grid, _P(NoDesc), SolveOpts]),
     "fcgno_solve_host": (_i, [Grid, _vp, _vp, _vp, _P(NoDesc), _vp, SolveOpts, _vp, _vp, _vp, _vp, _sz, _vp]),
@@ -342,3 +347,35 @@ def fcg_solve_diag(problem: Problem, f: torch.Tensor, u_star: torch.Tensor, u0: 
                                      opts, _ptr(iters), _ptr(status), _ptr(hist), _ptr(u_star), _ptr(eps),
                                      _ptr(err_a), _ptr(ws), ws.numel(), _stream()))
     return SolveResult(u, iters, status, hist), eps, err_a
+
+
+def apply_stationary(problem: Problem, r: torch.Tensor, kind: int, sweeps: int, stream=None) -> torch.Tensor:
+    """w = Jacobi(sweeps) r (kind JACOBI, Eq. 15) or red-black symmetric Gauss-Seidel(sweeps) r (SGS_RB),
+    from x^0 = 0 (PAPER.md:338-354; fcgno_apply_stationary)."""
+    _require(r, problem.shape, "r")
+    w = _on(stream, lambda: torch.empty_like(r))
+    ws = _workspace(_lib.fcgno_stationary_workspace_bytes(problem.grid), problem.device, stream)
+    _check(_lib.fcgno_apply_stationary(problem._h, int(kind), int(sweeps), _ptr(r), _ptr(w), _ptr(ws), ws.numel(),
+                                       _stream(stream)))
+    return w
+
+
+def fcg_solve_stationary(problem: Problem, f: torch.Tensor, u0: torch.Tensor | None = None, *, kind: int,
+                         sweeps: int, m: int, tol: float, maxit: int, schedule: int = SCHEDULE_PAPER,
+                         check_every: int = 16, vec_fp32: bool = False) -> SolveResult:
+    """Algorithm 1 with the classical preconditioner B = Jacobi(sweeps) / SGS_RB(sweeps)
+    (fcgno_fcg_solve_stationary)."""
+    _require(f, problem.shape, "f")
+    opts = SolveOpts(int(m), int(maxit), float(tol), int(schedule), int(check_every), 0, int(bool(vec_fp32)))
+    nbytes = _lib.fcgno_solve_stationary_workspace_bytes(problem.grid, opts)
+    if nbytes == 0:
+        raise ValueError("bad solve options")
+    dev = problem.device
+    ws = _workspace(nbytes, dev)
+    u = torch.zeros_like(f) if u0 is None else u0.clone()
+    iters = torch.empty(problem.B, dtype=torch.int32, device=dev)
+    status = torch.empty(problem.B, dtype=torch.int32, device=dev)
+    hist = torch.full((problem.B, maxit + 1), float("nan"), dtype=torch.float64, device=dev)
+    _check(_lib.fcgno_fcg_solve_stationary(problem._h, int(kind), int(sweeps), _ptr(f), _ptr(u), opts, _ptr(iters),
+                                           _ptr(status), _ptr(hist), _ptr(ws), ws.numel(), _stream()))
+    return SolveResult(u, iters, status, hist)

@@ -643,3 +643,38 @@ def test_graph_cache_reuse_with_other_buffers(lib):
             for b in range(B):
                 ref = _oracle_fcg(k[b], f[b], 5, 1e-8, 3000)
                 assert host(s.iters)[b] == ref["iters"] and np.array_equal(host(u)[b], ref["u"])
+
+
+# ----------------------------------------------------------------------------- classical preconditioners (NEXT-3)
+@pytest.mark.parametrize("kind,sweeps", [("jacobi", 1), ("jacobi", 4), ("sgs", 1), ("sgs", 3)])
+@pytest.mark.parametrize("n,B", [(17, 2), (64, 3), (300, 1)])
+def test_stationary_apply_bitwise(lib, kind, sweeps, n, B):
+    # Jacobi(k) (Eq. 15) and red-black SGS(k) (R22-R23) through fcgno_apply_stationary,
+    # bit for bit against the oracle's sweeps (same update, same stencil order, IEEE division)
+    k = sy.lognormal_k(n, B, 0.1, 4.0, 131)
+    r = sy.normal_field(n, B, 132)
+    prob = lib.Problem(dev(k))
+    got = host(lib.apply_stationary(prob, dev(r), lib.JACOBI if kind == "jacobi" else lib.SGS_RB, sweeps))
+    for b in range(B):
+        ref = orc.jacobi(k[b], r[b], sweeps) if kind == "jacobi" else orc.sgs(k[b], r[b], sweeps, "rb")
+        assert np.array_equal(got[b], ref), float(np.max(np.abs(got[b] - ref)))
+
+
+@pytest.mark.parametrize("kind,sweeps,vec32", [("jacobi", 4, False), ("sgs", 1, False), ("sgs", 4, False),
+                                               ("jacobi", 4, True)])
+def test_fcg_stationary_bitwise(lib, kind, sweeps, vec32):
+    # FCG(m) preconditioned by Jacobi(k) / red-black SGS(k): histories, iterates, counts bit for bit
+    cfg = sy.CONFIGS[2]
+    k, f = sy.make_k(cfg), sy.make_f(cfg)
+    prob = lib.Problem(dev(k))
+    kd = lib.JACOBI if kind == "jacobi" else lib.SGS_RB
+    res = lib.fcg_solve_stationary(prob, dev(f), kind=kd, sweeps=sweeps, m=cfg["m"], tol=cfg["tol"], maxit=3000,
+                                   vec_fp32=vec32)
+    iters, status, hist, u = host(res.iters), host(res.status), host(res.history), host(res.u)
+    for b in (0, cfg["batch"] - 1):
+        P = (lambda r: orc.jacobi(k[b], r, sweeps)) if kind == "jacobi" else (lambda r: orc.sgs(k[b], r, sweeps, "rb"))
+        ref = orc.fcg(lambda x: orc.apply_A(k[b], x), f[b], np.zeros_like(f[b]), cfg["m"], cfg["tol"], 3000,
+                      precond=P, vec32=vec32)
+        it = ref["iters"]
+        assert iters[b] == it and status[b] == ref["status"] == lib.CONVERGED
+        assert np.array_equal(hist[b, :it + 1], ref["hist"]) and np.array_equal(u[b], ref["u"])
