@@ -831,8 +831,8 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
       const int b = lit / g.MYT, m0 = (lit % g.MYT) * 128;
       const float* src = T + ((size_t)b * n + (size_t)lkc * kYanKC) * M + m0;
 #pragma unroll
-      for (int z = 0; z < kYanTasks; ++z) {
-        const int t = tid + z * 256, il = t >> 4, mg = t & 15;
+      for (int z = 0; z < kYanTasks; ++z) {   // task t = (row il, 8-float group mg): lanes cover 8 rows x 4 groups
+        const int t = tid + z * 256, il = (t >> 7) * 8 + (t & 7), mg = (t >> 3) & 15;
         const float4* p = reinterpret_cast<const float4*>(src + (size_t)il * M + mg * 8);
         x[z][0] = __ldg(p);
         x[z][1] = __ldg(p + 1);
@@ -848,10 +848,10 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
       if (c >= 2) tc::mbar_wait(&bar[c & 1u], ((c - 2u) >> 1) & 1u);    // MMA c - 2 done with A buffer c & 1
       unsigned char* ah = sm + L.A + (c & 1u) * 2u * a_half;
 #pragma unroll
-      for (int z = 0; z < kYanTasks; ++z) {
-        const int t = tid + z * 256, il = t >> 4, mg = t & 15;
+      for (int z = 0; z < kYanTasks; ++z) {   // a warp's 32 chunks are 512 contiguous bytes (no bank conflicts)
+        const int t = tid + z * 256, ih = t >> 7, il7 = t & 7, mg = (t >> 3) & 15;
         const float v[8] = {x[z][0].x, x[z][0].y, x[z][0].z, x[z][0].w, x[z][1].x, x[z][1].y, x[z][1].z, x[z][1].w};
-        const uint32_t off = (uint32_t)mg * 128u + (uint32_t)(il >> 3) * 2048u + (uint32_t)(il & 7) * 16u;
+        const uint32_t off = (uint32_t)mg * 128u + (uint32_t)ih * 2048u + (uint32_t)il7 * 16u;
         st_split8(ah + off, ah + a_half + off, v);
       }
       load();                                                            // next chunk in flight from here
@@ -886,11 +886,13 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
       tc::tmem_wait_ld();
       const int m = m0 + warp * 32 + lane, pr = m >> 1, k2 = pr / w, o = pr - k2 * w;
       const bool re = (lane & 1) == 0;
+      float2* dst = chat + ((size_t)k2 * B + b) * w + o;            // mode (k1, k2) at dst + k1 * 20 B w
+      const size_t kstride = (size_t)kModes * B * w;
 #pragma unroll
       for (int k1 = 0; k1 < kModes; ++k1) {
         const float xv = __uint_as_float(v[2 * k1]), yv = __uint_as_float(v[2 * k1 + 1]);
         const float px = __shfl_xor_sync(0xffffffffu, xv, 1), py = __shfl_xor_sync(0xffffffffu, yv, 1);
-        if (re && m < M) chat[((size_t)(k1 * kModes + k2) * B + b) * w + o] = make_float2(xv - py, px + yv);
+        if (re && m < M) dst[k1 * kstride] = make_float2(xv - py, px + yv);
       }
     }
     tc::fence_before_sync();
