@@ -622,9 +622,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float
   double rv[kWinPre][kPerThread];
   if (mi > 0) window_prefetch<V>(d, b, blk, it, mi, rv);
   for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)t * a.B + b];   // mode-major
-  for (int t = threadIdx.x; t < kModes * n; t += blockDim.x) {
-    const int j = t / kModes, k = t - j * kModes;
-    Fs[k * n + j] = __ldg(a.F + t);
+  for (int t = threadIdx.x; t < kModes * n; t += blockDim.x) {   // transposed: consecutive threads, consecutive j
+    const int k = t / n, j = t - k * n;
+    Fs[t] = __ldg(a.F + (size_t)j * kModes + k);
   }
   // the bypass term sum_o dw[o] v3[o] was reduced by layer 3 (k_tc_layer, fused projection)
   for (int t = threadIdx.x; t < kTile; t += blockDim.x) outs[t] = (e0 + t < N) ? a.p3[(size_t)b * N + e0 + t] : 0.f;
