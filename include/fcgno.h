@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FCGNO_ABI_VERSION 6
+#define FCGNO_ABI_VERSION 7
 #define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
 #define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
 #define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
@@ -78,10 +78,17 @@ typedef struct {
  *   E[w][2], bE[w],
  *   for l = 1..4: W_l[w_out][w_in], b_l[w], R_l[w_in][w_out][20][20][2 (re,im)],
  *   D[w], bD                                  total 3w + 4(w^2 + w + 800 w^2) + w + 1 doubles. */
+/* SNO basis: FCGNO_BASIS_FOURIER, the paper's (App. A): the truncated 2-D
+ * DFT on the modes {-10..9}^2 (R7-R8); FCGNO_BASIS_CHEBYSHEV: 20 Chebyshev polynomials per
+ * dimension, T_k at the Gauss-Chebyshev nodes, i.e. the DCT-II pair (analysis D^-1 S^T, synthesis S) on
+ * the index grid, with real mode-diagonal mixing (the blob's real parts of R; R25). */
+typedef enum { FCGNO_BASIS_FOURIER = 0, FCGNO_BASIS_CHEBYSHEV = 1 } fcgno_basis;
+
 typedef struct {
   int32_t width;      /* w >= 1 (32 / 48 / 85 in the paper's Table 5) */
   int32_t precision;  /* FCGNO_FP32 (production) or FCGNO_FP64 (trajectory-parity mode) */
   int32_t use_gelu;   /* 1; 0 = test-only linear mode */
+  int32_t basis;      /* fcgno_basis */
 } fcgno_no_desc;
 
 typedef struct {

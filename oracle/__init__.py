@@ -17,7 +17,7 @@ against the paper: pinned only by properties and closed forms).
 from .stencil import h_of, harmonic, faces, apply_A, dense_A
 from .dots import two_product, dot, norm2
 from .no import (K_MODES, mode_indices, analysis, synthesis, gelu, unpack_weights, no_forward,
-                 param_count)
+                 param_count, cheb_basis, analysis_cheb, synthesis_cheb)
 from .fcg import m_schedule, fcg, cg, CONVERGED, MAXIT, BREAKDOWN, NONFINITE, RUNNING
 from .notay import a_norm, notay_ratio, notay_ratio_scaled, notay_curve
 from .classical import diagonal, jacobi, sgs
@@ -25,6 +25,7 @@ from .classical import diagonal, jacobi, sgs
 __all__ = [
     "h_of", "harmonic", "faces", "apply_A", "dense_A", "two_product", "dot", "norm2",
     "K_MODES", "mode_indices", "analysis", "synthesis", "gelu", "unpack_weights", "no_forward",
+    "cheb_basis", "analysis_cheb", "synthesis_cheb",
     "param_count", "m_schedule", "fcg", "cg", "CONVERGED", "MAXIT", "BREAKDOWN", "NONFINITE",
     "RUNNING", "a_norm", "notay_ratio", "notay_ratio_scaled", "notay_curve", "diagonal", "jacobi", "sgs",
 ]

@@ -17,6 +17,13 @@ polynomials, GeLU, processor width 32/48/85.  The paper leaves the rest open; re
       v = GELU(u) except after layer 4]; decoder out = D v + bD; returned value ||r|| * out,
       and 0 for r = 0 (SPEC.md:343, 349-357);
   R11 GELU(x) = x/2 (1 + erf(x/sqrt 2)) (exact erf form).
+Chebyshev variant ("neural operators from [fanaskov2022spectral]
+utilizes DCT-II to work with Chebyshev polynomials"), reading R25:
+  p_k(j) = cos(pi k (j + 1/2) / n), k = 0..19: T_k at the Gauss-Chebyshev nodes cos(pi (j + 1/2) / n),
+      the grid index j read as the node index; quadrature weights w = 1, so
+      h_k = p_k^T p_k = n (k = 0), n/2 (k > 0);
+  analysis  c = D^{-1} S^T f in both dimensions (P:181), S = [p_k(j)]; synthesis f = S c S^T (P:176);
+  L = mode-diagonal real channel mixing with the real part of R (the blob's imaginary parts unused).
 """
 from __future__ import annotations
 
@@ -52,6 +59,27 @@ def synthesis(g: np.ndarray, n: int) -> np.ndarray:
     G = np.zeros(g.shape[:-2] + (n, n), dtype=complex)
     G[..., idx[:, None], idx[None, :]] = g
     return np.fft.ifft2(G, axes=(-2, -1)).real
+
+
+def cheb_basis(n: int, K: int = K_MODES) -> np.ndarray:
+    """R25: S[j, k] = p_k(j) = cos(pi k (j + 1/2) / n), shape [n, K]."""
+    j = np.arange(n, dtype=np.float64)[:, None] + 0.5
+    k = np.arange(K, dtype=np.float64)[None, :]
+    return np.cos(np.pi * j * k / n)
+
+
+def analysis_cheb(v: np.ndarray, K: int = K_MODES) -> np.ndarray:
+    """R25 analysis c = D^-1 S^T v S D^-1 of v[..., n, n] -> c[..., K, K] (axis -2: k1 <-> row i)."""
+    n = v.shape[-1]
+    S = cheb_basis(n, K)
+    h = np.where(np.arange(K) == 0, float(n), n / 2.0)
+    return np.einsum("ik,...ij,jl->...kl", S, v, S) / h[:, None] / h[None, :]
+
+
+def synthesis_cheb(g: np.ndarray, n: int) -> np.ndarray:
+    """R25 synthesis f = S g S^T of g[..., K, K] -> [..., n, n]."""
+    S = cheb_basis(n, g.shape[-1])
+    return np.einsum("ik,...kl,jl->...ij", S, g, S)
 
 
 def gelu(x):
@@ -93,8 +121,8 @@ def unpack_weights(blob: np.ndarray, width: int, K: int = K_MODES) -> dict:
     return p
 
 
-def no_forward(params: dict, r: np.ndarray, k: np.ndarray, use_gelu: bool = True) -> np.ndarray:
-    """Preconditioner w = B(r) for one system, r and k of shape [n, n] (R7-R11).
+def no_forward(params: dict, r: np.ndarray, k: np.ndarray, use_gelu: bool = True, basis: str = "fourier") -> np.ndarray:
+    """Preconditioner w = B(r) for one system, r and k of shape [n, n] (R7-R11; basis 'chebyshev': R25).
 
     ``use_gelu=False`` is a test-only linear mode."""
     r = np.asarray(r, dtype=np.float64)
@@ -105,9 +133,16 @@ def no_forward(params: dict, r: np.ndarray, k: np.ndarray, use_gelu: bool = True
     x0 = np.stack([r / s, np.asarray(k, dtype=np.float64)])          # [2, n, n]
     v = np.einsum("ci,ihw->chw", params["E"], x0) + params["bE"][:, None, None]
     for l in range(N_LAYERS):
-        c_hat = analysis(v)                                            # [w, K, K]
-        g_hat = np.einsum("cokl,ckl->okl", params["R"][l], c_hat)      # L: mode-diagonal mixing
-        z = synthesis(g_hat, n)
+        if basis == "fourier":
+            c_hat = analysis(v)                                        # [w, K, K]
+            g_hat = np.einsum("cokl,ckl->okl", params["R"][l], c_hat)  # L: mode-diagonal mixing
+            z = synthesis(g_hat, n)
+        elif basis == "chebyshev":
+            c_hat = analysis_cheb(v)
+            g_hat = np.einsum("cokl,ckl->okl", params["R"][l].real, c_hat)
+            z = synthesis_cheb(g_hat, n)
+        else:
+            raise ValueError(basis)
         u = np.einsum("oc,chw->ohw", params["W"][l], v) + params["b"][l][:, None, None] + z
         v = (gelu(u) if use_gelu else u) if l < N_LAYERS - 1 else u
     out = np.einsum("c,chw->hw", params["D"], v) + params["bD"]

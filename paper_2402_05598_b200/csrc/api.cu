@@ -23,10 +23,10 @@ using namespace fcgno;
 struct fcgno_problem {
   int n, B;
   const double* k;
-  float* F32;
-  double* F64;
-  float* khat32;
-  double* khat64;
+  float* F32[2];       // [basis] twiddles [n][20] complex (fcgno_basis: Fourier, Chebyshev)
+  double* F64[2];
+  float* khat32[2];    // [basis] transform of k per system [B][400] complex
+  double* khat64[2];
   bool no_ok;
   bool kfast;   // every k in [2^-400, 2^400]: stencil faces by the branch-free division (fcg_device.cuh)
 };
@@ -75,16 +75,20 @@ int nblk_of(int n) { return part_cap(n); }   // partial-array capacity per syste
 bool no_grid_ok(int n) { return n >= kModes && n <= FCGNO_NO_NMAX; }
 
 struct ProblemWs {
-  float* F32; double* F64; float* khat32; double* khat64; double* part; int* bad;
+  float* F32[2]; double* F64[2]; float* khat32[2]; double* khat64[2]; double* part; int* bad;
 };
 ProblemWs carve_problem(Carver& c, int n, int B) {
   ProblemWs w{};
   w.bad = c.take<int>(1);
-  w.F32 = c.take<float>((size_t)n * kModes * 2);
-  w.F64 = c.take<double>((size_t)n * kModes * 2);
+  for (int bs = 0; bs < 2; ++bs) {
+    w.F32[bs] = c.take<float>((size_t)n * kModes * 2);
+    w.F64[bs] = c.take<double>((size_t)n * kModes * 2);
+  }
   if (no_grid_ok(n)) {
-    w.khat32 = c.take<float>((size_t)B * kModes2 * 2);
-    w.khat64 = c.take<double>((size_t)B * kModes2 * 2);
+    for (int bs = 0; bs < 2; ++bs) {
+      w.khat32[bs] = c.take<float>((size_t)B * kModes2 * 2);
+      w.khat64[bs] = c.take<double>((size_t)B * kModes2 * 2);
+    }
     w.part = c.take<double>((size_t)B * ngroups_of(n) * kModes2 * 2);
   }
   return w;
@@ -145,6 +149,7 @@ void carve_no_any(Carver& c, int n, int B, const fcgno_no_desc& d, NoWs<float>* 
 int check_desc(const fcgno_no_desc& d) {
   if (d.width < 1 || d.width > 1024) return fail(FCGNO_EINVAL, "NO width %d out of range", d.width);
   if (d.precision != FCGNO_FP32 && d.precision != FCGNO_FP64) return fail(FCGNO_EINVAL, "bad NO precision");
+  if (d.basis != FCGNO_BASIS_FOURIER && d.basis != FCGNO_BASIS_CHEBYSHEV) return fail(FCGNO_EINVAL, "bad NO basis");
   return FCGNO_OK;
 }
 
@@ -154,6 +159,7 @@ NoDev<T> make_nodev(const fcgno_problem* p, const fcgno_no_desc& d, const void* 
   NoDev<T> no{};
   no.n = p->n; no.B = p->B; no.N = p->n * p->n; no.w = d.width; no.use_gelu = d.use_gelu;
   no.k = p->k; no.pk = static_cast<const T*>(packed); no.L = no_layout(d.width);
+  no.k0 = d.basis == FCGNO_BASIS_CHEBYSHEV ? 0 : (kModes / 2) * kModes + kModes / 2;   // mode of a constant
   no.F = F; no.khat = khat; no.rpart = w.rpart; no.ngroups = ngroups_of(p->n);
   no.v0 = w.v0; no.v1 = w.v1; no.chat = w.chat; no.ghat = w.ghat;
   no.vb0 = w.vb0; no.vb1 = w.vb1; no.Gb = w.Gb; no.Tb = w.Tb; no.cst = w.cst; no.p3 = w.p3; no.rinv = w.rinv;
@@ -231,13 +237,16 @@ int fcgno_assemble(fcgno_grid g, const double* k, void* ws, size_t ws_bytes, voi
   CK(cudaMemcpyAsync(&bad, w.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   if (bad & 1) return fail(FCGNO_ENONPOS_K, "assemble: k has a non-positive or non-finite entry");
-  CK(launch_twiddles(w.F32, w.F64, g.n, s));
   const bool no_ok = no_grid_ok(g.n);
-  if (no_ok) {
-    CK(launch_khat<double>(k, w.F64, w.part, w.khat64, g.n, g.batch, ngroups_of(g.n), s));
-    CK(launch_khat<float>(k, w.F32, reinterpret_cast<float*>(w.part), w.khat32, g.n, g.batch, ngroups_of(g.n), s));
+  for (int bs = 0; bs < 2; ++bs) {
+    CK(launch_twiddles(w.F32[bs], w.F64[bs], g.n, bs, s));
+    if (no_ok) {
+      CK(launch_khat<double>(k, w.F64[bs], w.part, w.khat64[bs], g.n, g.batch, ngroups_of(g.n), s));
+      CK(launch_khat<float>(k, w.F32[bs], reinterpret_cast<float*>(w.part), w.khat32[bs], g.n, g.batch, ngroups_of(g.n), s));
+    }
   }
-  fcgno_problem* p = new fcgno_problem{g.n, g.batch, k, w.F32, w.F64, w.khat32, w.khat64, no_ok, (bad & 2) == 0};
+  fcgno_problem* p = new fcgno_problem{g.n, g.batch, k, {w.F32[0], w.F32[1]}, {w.F64[0], w.F64[1]},
+                                       {w.khat32[0], w.khat32[1]}, {w.khat64[0], w.khat64[1]}, no_ok, (bad & 2) == 0};
   *out = p;
   return FCGNO_OK;
 }
@@ -300,9 +309,14 @@ int fcgno_no_pack(fcgno_no_desc d, const double* blob, void* packed, void* strea
   const double bD = *take(1);
   for (size_t t = 0; t < pos; ++t)
     if (!std::isfinite(blob[t])) return fail(FCGNO_EINVAL, "no_pack: non-finite weight at %zu", t);
+  // Chebyshev basis (R25): real mixing (imaginary parts unused) and the analysis weights D^-1 folded in
+  // per mode, so the kernels' 1/n^2 synthesis scale applies to both bases
+  const bool cheb = d.basis == FCGNO_BASIS_CHEBYSHEV;
   auto Rc = [&](int l, int c, int o, int kk) {
     const double* q = R[l] + (((size_t)c * w + o) * K2 + kk) * 2;
-    return cd(q[0], q[1]);
+    if (!cheb) return cd(q[0], q[1]);
+    const double f = (kk / kModes == 0 ? 1.0 : 2.0) * (kk % kModes == 0 ? 1.0 : 2.0);
+    return cd(q[0] * f, 0.0);
   };
   const NoLayout L = no_layout(w);
   std::vector<double> P(L.total, 0.0);
@@ -319,7 +333,7 @@ int fcgno_no_pack(fcgno_no_desc d, const double* blob, void* packed, void* strea
     P[L.b1 + o] = bb;
   }
   // spectral term of layer 1: sum_c R1[c][o] DFT(E[c,0] r^ + E[c,1] k + bE[c])
-  const int k0 = (kModes / 2) * kModes + kModes / 2;
+  const int k0 = cheb ? 0 : (kModes / 2) * kModes + kModes / 2;   // mode of a constant field
   for (int kk = 0; kk < K2; ++kk)
     for (int o = 0; o < w; ++o) {
       cd a0 = 0, a1 = 0;
@@ -413,12 +427,12 @@ int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void* packed, 
   CK(launch_dot(r, r, rr, part, cnt, p->n, p->B, s));
   if (d.precision == FCGNO_FP64) {
     CK(prepare_no_kernels<double>());
-    NoDev<double> no = make_nodev<double>(p, d, packed, w64, p->F64, p->khat64);
+    NoDev<double> no = make_nodev<double>(p, d, packed, w64, p->F64[d.basis], p->khat64[d.basis]);
     CK(launch_no_forward<double>(no, r, rr, w, nullptr, nullptr, s, nullptr));
   } else {
     CK(prepare_no_kernels<float>());
     CK(prepare_px_kernels());
-    NoDev<float> no = make_nodev<float>(p, d, packed, w32, p->F32, p->khat32);
+    NoDev<float> no = make_nodev<float>(p, d, packed, w32, p->F32[d.basis], p->khat32[d.basis]);
     CK(prepare_no_constants(no, s));
     CK(launch_no_forward<float>(no, r, rr, w, nullptr, nullptr, s, nullptr));
   }
@@ -612,10 +626,10 @@ int enqueue_iteration(const FcgDev& d, const fcgno_no_desc* nd, const void* pack
     int nl = 0;
     cudaError_t e;
     if (nd->precision == FCGNO_FP64) {
-      NoDev<double> no = make_nodev<double>(p, *nd, packed, sw.n64, p->F64, p->khat64);
+      NoDev<double> no = make_nodev<double>(p, *nd, packed, sw.n64, p->F64[nd->basis], p->khat64[nd->basis]);
       e = launch_no_forward<double>(no, d.vec32 ? d.r64 : d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
     } else {
-      NoDev<float> no = make_nodev<float>(p, *nd, packed, sw.n32, p->F32, p->khat32);
+      NoDev<float> no = make_nodev<float>(p, *nd, packed, sw.n32, p->F32[nd->basis], p->khat32[nd->basis]);
       e = launch_no_forward<float>(no, d.vec32 ? d.r64 : d.r, d.rr, sw.wvec, &d, d.status, s, &nl, prof);
     }
     if (e != cudaSuccess) return -1;
@@ -776,7 +790,7 @@ struct LoopKey {
   fcgno_no_desc nd;
   int has_nd, chunk;
   const void* packed;
-  const void* pf[4];
+  const void* pf[8];
   int n, B, no_ok, kfast;   // the NO buffers are carved from the workspace after d.r (d) at
 };                          // offsets fixed by (n, B, nd, m): covered by the fields above
 struct LoopEntry { LoopKey key; DeviceLoop loop; uint64_t used; };
@@ -792,7 +806,10 @@ LoopKey loop_key(const Lane& ln, const fcgno_no_desc* nd, const void* packed, in
   if (nd) { k.nd = *nd; k.has_nd = 1; }
   k.chunk = chunk;
   k.packed = packed;
-  k.pf[0] = ln.p.F32; k.pf[1] = ln.p.F64; k.pf[2] = ln.p.khat32; k.pf[3] = ln.p.khat64;
+  for (int bs = 0; bs < 2; ++bs) {
+    k.pf[4 * bs + 0] = ln.p.F32[bs]; k.pf[4 * bs + 1] = ln.p.F64[bs];
+    k.pf[4 * bs + 2] = ln.p.khat32[bs]; k.pf[4 * bs + 3] = ln.p.khat64[bs];
+  }
   k.n = ln.p.n; k.B = ln.p.B; k.no_ok = ln.p.no_ok; k.kfast = ln.p.kfast;
   return k;
 }
@@ -915,8 +932,10 @@ int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* pack
     ln.p = *p;
     ln.p.B = nb;
     ln.p.k = p->k + b0 * N;
-    if (p->khat32) ln.p.khat32 = p->khat32 + (size_t)b0 * kModes2 * 2;
-    if (p->khat64) ln.p.khat64 = p->khat64 + (size_t)b0 * kModes2 * 2;
+    for (int bs = 0; bs < 2; ++bs) {
+      if (p->khat32[bs]) ln.p.khat32[bs] = p->khat32[bs] + (size_t)b0 * kModes2 * 2;
+      if (p->khat64[bs]) ln.p.khat64[bs] = p->khat64[bs] + (size_t)b0 * kModes2 * 2;
+    }
     ln.sw = carve_solve(c, p->n, nb, nd, o, dg != nullptr, sta != nullptr);
     FcgDev& d = ln.sw.d;
     d.n = p->n; d.B = nb; d.N = p->n * p->n; d.nblk = nblk_of(p->n);
@@ -976,7 +995,7 @@ int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* pack
       if ((e = cudaMemsetAsync(d.iter, 0, 2 * sizeof(int), s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if (d.dg_cnt && (e = cudaMemsetAsync(d.dg_cnt, 0, sizeof(unsigned) * d.B, s)) != cudaSuccess) { rc = cuda_fail(e, "memset"); break; }
       if (nd && sw.n32.Gb) {   // tensor-core constant operands (every blob byte the kernels read is written by them)
-        NoDev<float> no = make_nodev<float>(&lanes[l].p, *nd, packed, sw.n32, p->F32, lanes[l].p.khat32);
+        NoDev<float> no = make_nodev<float>(&lanes[l].p, *nd, packed, sw.n32, p->F32[nd->basis], lanes[l].p.khat32[nd->basis]);
         if ((e = prepare_no_constants(no, s)) != cudaSuccess) { rc = cuda_fail(e, "tc constants"); break; }
       }
       if ((e = launch_init_residual(d, s)) != cudaSuccess) { rc = cuda_fail(e, "init_residual"); break; }

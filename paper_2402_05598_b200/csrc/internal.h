@@ -70,6 +70,7 @@ template <typename T>
 struct NoDev {
   int n, B, N, w;
   int use_gelu;
+  int k0;                     // mode index of a constant field (Fourier kappa = 0: 210; Chebyshev k = 0: 0)
   const double* k;            // [B][N] nodal k (fp64, the problem's)
   const T* pk;                // packed weights
   NoLayout L;
@@ -147,7 +148,7 @@ cudaError_t launch_update(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_flush_x(const FcgDev& d, cudaStream_t s);
 cudaError_t launch_loop_cond(const int* active, cudaGraphConditionalHandle h, cudaStream_t s);
 
-cudaError_t launch_twiddles(float* F32, double* F64, int n, cudaStream_t s);
+cudaError_t launch_twiddles(float* F32, double* F64, int n, int basis, cudaStream_t s);
 template <typename T>
 cudaError_t launch_khat(const double* k, const T* F, T* part, T* khat, int n, int B, int ngroups,
                         cudaStream_t s);

@@ -31,21 +31,31 @@ constexpr int kMixBatch = 32;    // systems per CTA of k_mix
 constexpr int kMaxDynSmem = 227 * 1024;
 
 // ------------------------------------------------------------------ twiddles
-__global__ void k_twiddles(float2* F32, double2* F64, int n) {
+// basis 0 (Fourier, R7-R8): exp(-2 pi i kappa j / n), kappa = kx - 10;
+// basis 1 (Chebyshev, R25): (cos(pi k (j + 1/2) / n), 0), k = kx: the complex machinery then carries
+// zero imaginary parts and the synthesis Re(g F*) reduces to the cosine sum
+__global__ void k_twiddles(float2* F32, double2* F64, int n, int basis) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n * kModes) return;
   const int j = t / kModes, kx = t - j * kModes;
-  const long long kap = kx - kModes / 2;
-  const long long q = ((kap * j) % n + n) % n;       // exact phase reduction
   double sn, cs;
-  sincospi(2.0 * (double)q / (double)n, &sn, &cs);
-  F64[t] = make_double2(cs, -sn);                    // exp(-2 pi i kappa j / n)
-  F32[t] = make_float2((float)cs, (float)-sn);
+  if (basis == 0) {
+    const long long kap = kx - kModes / 2;
+    const long long q = ((kap * j) % n + n) % n;       // exact phase reduction
+    sincospi(2.0 * (double)q / (double)n, &sn, &cs);
+    sn = -sn;
+  } else {
+    const long long q = ((long long)kx * (2 * j + 1)) % (4LL * n);   // pi k (2j + 1) / (2n), reduced exactly
+    cs = cospi((double)q / (2.0 * (double)n));
+    sn = 0.0;
+  }
+  F64[t] = make_double2(cs, sn);
+  F32[t] = make_float2((float)cs, (float)sn);
 }
 
-cudaError_t launch_twiddles(float* F32, double* F64, int n, cudaStream_t s) {
+cudaError_t launch_twiddles(float* F32, double* F64, int n, int basis, cudaStream_t s) {
   const int cnt = n * kModes;
-  k_twiddles<<<(cnt + 255) / 256, 256, 0, s>>>(reinterpret_cast<float2*>(F32), reinterpret_cast<double2*>(F64), n);
+  k_twiddles<<<(cnt + 255) / 256, 256, 0, s>>>(reinterpret_cast<float2*>(F32), reinterpret_cast<double2*>(F64), n, basis);
   ++launch_counter();
   return cudaGetLastError();
 }
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
                                                   const typename Cplx<T>::type* __restrict__ A1,
                                                   const typename Cplx<T>::type* __restrict__ A2,
                                                   typename Cplx<T>::type* __restrict__ ghat, int w, T n2, T inv_n2,
-                                                  const int* __restrict__ status, int mode_major) {
+                                                  const int* __restrict__ status, int mode_major, int k0) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename Cplx<T>::type;
@@ -166,7 +176,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
     Rh[e] = T2{ar, ai};
   }
   __syncthreads();
-  const int k0 = (kModes / 2) * kModes + kModes / 2;   // kappa = (0, 0)
+  // k0: the mode of a constant field (the lift's bias bE transforms to n^2 at k0 only)
   // element e -> (o, kappa): kappa fastest for the [B][w][400] layout (FFMA path), o fastest for the
   // mode-major [400][B][w] layout of the tensor-core path, so the stores stay contiguous
   const int olo = ochunk * kLiftCh, ohi = min(w, olo + kLiftCh), no_ = ohi - olo, cnt = no_ * kModes2;
@@ -775,7 +785,7 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   launch_k(k_lift_mix<T>, dim3(B, (w + kLiftCh - 1) / kLiftCh), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
            reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
            reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2), ghat, w, n2, inv_n2,
-           status, (int)tc_layout_modes(no));
+           status, (int)tc_layout_modes(no), no.k0);
   pe(PROF_NO_INPUT);
   ++launches;
   // 3. layers 1..3, each followed by the mixing of the next layer

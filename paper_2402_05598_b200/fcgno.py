@@ -23,6 +23,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 FP32, FP64 = 0, 1
 JACOBI, SGS_RB = 1, 2   # classical preconditioners (fcgno_precond_kind)
+FOURIER, CHEBYSHEV = 0, 1  # SNO basis (fcgno_basis)
 SCHEDULE_PAPER, SCHEDULE_SLIDING = 0, 1
 RUNNING, CONVERGED, MAXIT, BREAKDOWN, NONFINITE = 0, 1, 2, 3, 4
 K_MODES = 20
@@ -40,7 +41,8 @@ class Grid(ctypes.Structure):
 
 
 class NoDesc(ctypes.Structure):
-    _fields_ = [("width", ctypes.c_int32), ("precision", ctypes.c_int32), ("use_gelu", ctypes.c_int32)]
+    _fields_ = [("width", ctypes.c_int32), ("precision", ctypes.c_int32), ("use_gelu", ctypes.c_int32),
+                ("basis", ctypes.c_int32)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -216,8 +218,8 @@ class NeuralOperator:
     """Packed SNO weights resident on the device."""
 
     def __init__(self, width: int, blob: np.ndarray, precision: int = FP32, use_gelu: bool = True,
-                 device="cuda", stream=None):
-        self.desc = NoDesc(int(width), int(precision), int(bool(use_gelu)))
+                 device="cuda", stream=None, basis: int = FOURIER):
+        self.desc = NoDesc(int(width), int(precision), int(bool(use_gelu)), int(basis))
         blob = np.ascontiguousarray(blob, dtype=np.float64)
         nbytes = _lib.fcgno_no_packed_bytes(self.desc)
         if nbytes == 0:

@@ -678,3 +678,33 @@ def test_fcg_stationary_bitwise(lib, kind, sweeps, vec32):
         it = ref["iters"]
         assert iters[b] == it and status[b] == ref["status"] == lib.CONVERGED
         assert np.array_equal(hist[b, :it + 1], ref["hist"]) and np.array_equal(u[b], ref["u"])
+
+
+# ----------------------------------------------------------------------------- Chebyshev (DCT-II) SNO basis (NEXT-4)
+@pytest.mark.parametrize("n,B,w,prec", [(32, 2, 8, "fp64"), (64, 2, 48, "fp32"), (128, 2, 85, "fp32"),
+                                        (256, 1, 85, "fp32"), (45, 2, 16, "fp32")])
+def test_no_chebyshev_matches_oracle(lib, n, B, w, prec):
+    # R25: the same layer kernels with the cosine twiddle table and D^-1 folded into the mixing
+    k, r, blob = _no_case(n, B, w, 141, 142)
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob, precision=lib.FP64 if prec == "fp64" else lib.FP32, basis=lib.CHEBYSHEV)
+    got = host(no.apply(prob, dev(r)))
+    params = orc.unpack_weights(blob, w)
+    tol = 1e-12 if prec == "fp64" else 1e-4
+    for b in range(B):
+        ref = orc.no_forward(params, r[b], k[b], basis="chebyshev")
+        assert rel_l2(got[b], ref) <= tol, rel_l2(got[b], ref)
+
+
+def test_fcg_no_chebyshev_hybrid_bitwise(lib):
+    cfg = dict(sy.CONFIGS[2], batch=4)
+    k, f, blob = sy.make_k(cfg), sy.make_f(cfg), sy.make_weights(cfg)
+    n, B, w, m = cfg["n"], cfg["batch"], cfg["width"], cfg["m"]
+    prob = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob, precision=lib.FP32, basis=lib.CHEBYSHEV)
+    res = lib.fcg_solve(prob, dev(f), m=m, tol=cfg["tol"], maxit=200, no=no)
+    for b in (0, B - 1):
+        ref = orc.fcg(lambda x: orc.apply_A(k[b], x), f[b], np.zeros_like(f[b]), m, cfg["tol"], 200,
+                      precond=_gpu_precond(lib, prob, no, B, n, b))
+        assert np.array_equal(host(res.history)[b, :ref["iters"] + 1], ref["hist"])
+        assert np.array_equal(host(res.u)[b], ref["u"])

@@ -182,3 +182,51 @@ def test_forward_matches_bruteforce_loops():
     expect = s * (sum(p["D"][c] * v[c] for c in range(w)) + p["bD"])
     out = orc.no_forward(p, r, k)
     assert np.max(np.abs(out - expect)) <= 1e-11 * np.max(np.abs(expect))
+
+
+# ----------------------------------------------------------------------------- Chebyshev / DCT-II basis (R25, NEXT-4)
+def test_cheb_analysis_is_scaled_scipy_dct2():
+    # S^T f along one axis is half of scipy's unnormalised DCT-II (y_k = 2 sum_j x_j cos(pi k (2j+1) / 2n)),
+    # the library routine the paper's Chebyshev SNO uses; analysis divides by h_k = n, n/2
+    from scipy.fft import dctn
+    n = 29
+    v = np.random.default_rng(5).standard_normal((n, n))
+    y = dctn(v, type=2)[:orc.K_MODES, :orc.K_MODES] / 4.0
+    h = np.where(np.arange(orc.K_MODES) == 0, float(n), n / 2.0)
+    assert np.allclose(orc.analysis_cheb(v), y / h[:, None] / h[None, :], rtol=1e-12, atol=1e-14)
+
+
+def test_cheb_synthesis_then_analysis_is_identity():
+    # discrete orthogonality of the cosines on the index grid: A S = identity on K x K coefficients
+    n = 33
+    g = np.random.default_rng(6).standard_normal((orc.K_MODES, orc.K_MODES))
+    assert np.allclose(orc.analysis_cheb(orc.synthesis_cheb(g, n)), g, rtol=1e-12, atol=1e-12)
+
+
+def test_cheb_brute_force_sums():
+    n, K = 21, orc.K_MODES
+    v = np.random.default_rng(7).standard_normal((n, n))
+    c = np.zeros((K, K))
+    for k1 in range(K):
+        for k2 in range(K):
+            acc = 0.0
+            for i in range(n):
+                for j in range(n):
+                    acc += v[i, j] * np.cos(np.pi * k1 * (i + 0.5) / n) * np.cos(np.pi * k2 * (j + 0.5) / n)
+            c[k1, k2] = acc / ((n if k1 == 0 else n / 2) * (n if k2 == 0 else n / 2))
+    assert np.allclose(orc.analysis_cheb(v), c, rtol=1e-12, atol=1e-13)
+
+
+def test_cheb_no_forward_linear_mode_superposition_and_constant_mode():
+    # linear mode: B is homogeneous of degree 1 in r (scale) and the k = 0 mode of a constant field
+    # is the constant itself (T_0 = 1): a constant input passes through a single-mode kernel exactly
+    n, w = 24, 3
+    k = sy.lognormal_k(n, 1, 0.1, 1.0, 8)[0]
+    r = sy.normal_field(n, 1, 9)[0]
+    p = orc.unpack_weights(sy.no_weights(w, 10), w)
+    a = orc.no_forward(p, r, k, use_gelu=False, basis="chebyshev")
+    b = orc.no_forward(p, 2.5 * r, k, use_gelu=False, basis="chebyshev")
+    assert np.allclose(b, 2.5 * a, rtol=1e-12, atol=1e-12 * np.abs(a).max())
+    const = np.full((n, n), 3.0)
+    g = np.zeros((orc.K_MODES, orc.K_MODES)); g[0, 0] = 3.0
+    assert np.allclose(orc.analysis_cheb(const), g, atol=1e-13)
