@@ -120,7 +120,7 @@ typedef enum {
   FCGNO_PROF_NO_MIX = 1,     /* k_mix: mode-diagonal channel mixing (layers 2-4) */
   FCGNO_PROF_NO_OUT = 2,     /* k_no_out: layer 4 + projection + window dots */
   FCGNO_PROF_NO_INPUT = 3,   /* k_dft_rows + k_lift_mix: DFT of r/||r|| and layer-1 mixing */
-  FCGNO_PROF_WINDOW = 4,     /* k_window_dots (identity preconditioner only) */
+  FCGNO_PROF_WINDOW = 4,     /* k_window_dots (identity / classical preconditioners, and the NO for wide batches) */
   FCGNO_PROF_PFORM = 5,      /* unused since ABI 2 (p is formed inside k_pform_stencil) */
   FCGNO_PROF_STENCIL = 6,    /* k_pform_stencil: lazy u += alpha p, p = w - sum beta p, s = A p, (p,s), (p,r); one launch
                                 per iteration */

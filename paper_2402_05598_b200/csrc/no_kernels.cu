@@ -877,7 +877,10 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   }
   // 4. layer 4 + projection (+ window dots when inside FCG)
   OutArgs<T> oa{};
-  oa.n = n; oa.N = N; oa.w = w; oa.use_dots = fcg != nullptr;
+  // wide batches: the window dots (w, s_k) run in the separate wide window kernel (16 elements per
+  // thread, w staged in shared memory) after the output kernel; small ones keep them fused in it
+  const bool split_dots = fcg != nullptr && ew_wide(n, B);
+  oa.n = n; oa.N = N; oa.w = w; oa.use_dots = fcg != nullptr && !split_dots;
   oa.vin = vbuf[0];                       // layer 3 wrote vbuf[2 & 1] = vbuf[0]
   oa.dw = pk + no.L.dw; oa.cst = pk + no.L.cst;
   oa.gh4 = ghat; oa.F = F; oa.rr = rr; oa.wout = wout; oa.status = status; oa.B = B;
@@ -903,8 +906,14 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
   }
   pe(PROF_NO_OUT);
   ++launches;
+  if (split_dots) {
+    pb(PROF_WINDOW);
+    const cudaError_t e = launch_window_dots(*fcg, s);   // adds itself to launch_counter()
+    pe(PROF_WINDOW);
+    if (e != cudaSuccess) return e;
+  }
   launch_counter() += launches;
-  if (nlaunch) *nlaunch = launches;
+  if (nlaunch) *nlaunch = launches + (split_dots ? 1 : 0);
   return cudaGetLastError();
 }
 
