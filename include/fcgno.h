@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FCGNO_ABI_VERSION 7
+#define FCGNO_ABI_VERSION 8
 #define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
 #define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
 #define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
@@ -242,6 +242,56 @@ FCGNO_API size_t fcgno_solve_stationary_workspace_bytes(fcgno_grid g, fcgno_solv
 FCGNO_API int fcgno_fcg_solve_stationary(const fcgno_problem* p, int kind, int sweeps, const double* f, double* u,
                                fcgno_solve_opts o, int32_t* iters, int32_t* status, double* history, void* ws,
                                size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------------------------------
+ * Training the SNO on the GPU (§2.5, §3.1-3.2,
+ * Table 6).  The scheme of Fig. 3: FCG with B = I on the training systems
+ * (fcgno_fcg_solve with maxit = i gives the CG iterate u_i), training pairs (r_i, e_i) with
+ * e_i = u_exact - u_i = A^{-1} r_i (fcgno_krylov_pair), then minibatch steps of
+ *   L(theta) = mean_b ||B(r_b; theta) - e_b||_A / ||e_b||_A     (Notay loss, error form)
+ *              or mean_b ||B(r_b; theta) - e_b||_2 / ||e_b||_2  (L2 form)
+ * with B(r) = ||r|| NO([r/||r||, k]) exactly as fcgno_apply_NO defines it (fp32 forward, fp64 loss), the
+ * gradient by the chain rule through projection, the four layers and the lift (oracle/train.py), and
+ * AdamW (decoupled weight decay, R26).
+ * Weights are fp32 in the canonical blob order of fcgno_no_desc (E, bE, 4 x (W, b, R), D, bD);
+ * fcgno_train_param_count(w) elements.  Samples: k, r, e [S][n][n] fp64 device; the minibatch is
+ * samples perm[0..count-1] (int32 device; NULL = 0..count-1), whose coefficient field is
+ * k[ksys[sample]] (int32 device [S]; NULL = k[sample]).  Deterministic (fixed-order reductions). */
+typedef enum { FCGNO_LOSS_NOTAY = 0, FCGNO_LOSS_L2 = 1 } fcgno_loss_kind;
+typedef struct {
+  int32_t n;      /* grid, 20 <= n <= 256 */
+  int32_t width;  /* w, 1..128 */
+  int32_t batch;  /* minibatch capacity (N_batch of Table 6), batch * n <= 65535 */
+  int32_t loss;   /* fcgno_loss_kind */
+} fcgno_train_desc;
+typedef struct {
+  double lr, beta1, beta2, eps, weight_decay;   /* Table 6: lr 1e-3 (x0.5 / 50 epochs), wd 1e-2 */
+} fcgno_adamw_opts;
+FCGNO_API size_t fcgno_train_param_count(int32_t width);
+FCGNO_API size_t fcgno_train_workspace_bytes(fcgno_train_desc d);
+/* Forward + loss of `count` <= batch samples: loss[b] (fp64 device [count], or NULL) = the sample's
+ * ratio; with grad != NULL also grad [P] fp32 device = d(mean_b loss_b)/d(theta) (overwritten).
+ * Enqueues on `stream`, no synchronisation. */
+FCGNO_API int fcgno_train_loss_grad(fcgno_train_desc d, int32_t count, const float* params, const double* k,
+                                    const double* r, const double* e, const int32_t* perm, const int32_t* ksys,
+                                    double* loss, float* grad, void* ws, size_t ws_bytes, void* stream);
+/* AdamW step t >= 1 on `count` fp32 parameters (params, m, v updated in place; m = v = 0 before t = 1):
+ * theta <- theta (1 - lr wd); m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2;
+ * theta <- theta - lr/(1-b1^t) m / (sqrt(v)/sqrt(1-b2^t) + eps). */
+FCGNO_API int fcgno_adamw_step(size_t count, float* params, const float* grad, float* m, float* v, int32_t t,
+                               fcgno_adamw_opts o, void* stream);
+/* One epoch: minibatches perm[s0 .. s0+batch-1] for s0 = 0, batch, ... < nsamples (the last one may be
+ * smaller), each a fcgno_train_loss_grad into grad [P] followed by an AdamW step with t = ++*t_host
+ * ([host] in/out).  loss [nsamples] device or NULL: loss[j] of sample perm[j] before its step. */
+FCGNO_API int fcgno_train_epoch(fcgno_train_desc d, int32_t nsamples, float* params, float* grad, float* m,
+                                float* v, int32_t* t_host, fcgno_adamw_opts o, const double* k, const double* r,
+                                const double* e, const int32_t* perm, const int32_t* ksys, double* loss, void* ws,
+                                size_t ws_bytes, void* stream);
+/* Krylov training pair (Eq. 8-9) of every system of the problem:
+ * r = f - A u (u the CG iterate u_i), e = u_star - u (u_star = u_exact, e.g. a tight FCG(I) solve);
+ * fp64 [B][n][n] device, outputs must not alias inputs.  Bitwise the oracle's arithmetic (R5). */
+FCGNO_API int fcgno_krylov_pair(const fcgno_problem* p, const double* f, const double* u_star, const double* u,
+                                double* r, double* e, void* stream);
 
 /* End-to-end convenience entry point with HOST buffers ([host], pageable or pinned): copies
  * k, f, u0 to the device, assembles, solves and copies u, iters, status (and history if

@@ -1167,3 +1167,288 @@ int fcgno_solve_host(fcgno_grid g, const double* k_host, const double* f_host, d
 }
 
 }  // extern "C"
+
+// ================================================================== SNO training
+namespace {
+
+using ll = long long;
+
+struct TrWs {
+  float *Fj, *Fi, *Gi, *Gj, *one;
+  double *kg, *rg, *eg, *d, *Ad, *Ae, *rr, *dAd, *eAe, *coef;
+  dd* part;
+  unsigned* cnt;            // [3][B] last-CTA counters of the three dots
+  float *X2, *V[5], *Z[3], *Cs[4], *T, *G, *DV, *DV2, *DG, *DC, *dout, *partials;
+};
+constexpr int kTrSplit = 256;     // split-K target of the weight-gradient GEMMs
+
+int check_train_desc(fcgno_train_desc d) {
+  if (d.n < kModes || d.n > 256) return fail(FCGNO_EUNSUPPORTED, "train: needs %d <= n <= 256 (n=%d)", kModes, d.n);
+  if (d.width < 1 || d.width > 128) return fail(FCGNO_EINVAL, "train: width %d outside 1..128", d.width);
+  if (d.batch < 1 || (size_t)d.batch * d.n > 65535) return fail(FCGNO_EINVAL, "train: batch %d", d.batch);
+  if (d.loss != FCGNO_LOSS_NOTAY && d.loss != FCGNO_LOSS_L2) return fail(FCGNO_EINVAL, "train: loss kind %d", d.loss);
+  if (tr_mix_smem(d.batch, d.width, true) > 227 * 1024)
+    return fail(FCGNO_EUNSUPPORTED, "train: batch x width too large for the per-mode mixing kernel");
+  return FCGNO_OK;
+}
+
+TrWs carve_train(Carver& c, fcgno_train_desc d) {
+  const int n = d.n, w = d.width, B = d.batch;
+  const size_t N = (size_t)n * n, BN = (size_t)B * N, act = BN * w, spec = (size_t)B * 2 * kModes2 * w;
+  TrWs t{};
+  t.Fj = c.take<float>((size_t)2 * kModes * n);
+  t.Fi = c.take<float>((size_t)2 * kModes * 2 * n);
+  t.Gi = c.take<float>((size_t)2 * n * 2 * kModes);
+  t.Gj = c.take<float>((size_t)n * 2 * kModes);
+  t.one = c.take<float>(1);
+  t.kg = c.take<double>(BN); t.rg = c.take<double>(BN); t.eg = c.take<double>(BN);
+  t.d = c.take<double>(BN); t.Ad = c.take<double>(BN); t.Ae = c.take<double>(BN);
+  t.rr = c.take<double>(B); t.dAd = c.take<double>(B); t.eAe = c.take<double>(B); t.coef = c.take<double>(B);
+  t.part = c.take<dd>((size_t)B * part_cap(n));
+  t.cnt = c.take<unsigned>((size_t)3 * B);
+  t.X2 = c.take<float>(2 * BN);
+  for (auto& v : t.V) v = c.take<float>(act);
+  for (auto& z : t.Z) z = c.take<float>(act);
+  for (auto& s : t.Cs) s = c.take<float>(spec);
+  t.T = c.take<float>((size_t)B * n * 2 * kModes * w);
+  t.G = c.take<float>(spec);
+  t.DV = c.take<float>(act); t.DV2 = c.take<float>(act);
+  t.DG = c.take<float>(spec); t.DC = c.take<float>(spec);
+  t.dout = c.take<float>(BN);
+  t.partials = c.take<float>((size_t)kTrSplit * 2 * std::max(w * w, 2 * w));
+  return t;
+}
+
+// Blocks of the canonical weight blob (include/fcgno.h), as element offsets.
+struct TrOff {
+  size_t E, bE, W[4], b[4], R[4], D, bD, total;
+};
+TrOff tr_offsets(int w) {
+  TrOff o{};
+  size_t pos = 0;
+  o.E = pos; pos += 2 * (size_t)w;
+  o.bE = pos; pos += w;
+  for (int l = 0; l < 4; ++l) {
+    o.W[l] = pos; pos += (size_t)w * w;
+    o.b[l] = pos; pos += w;
+    o.R[l] = pos; pos += (size_t)w * w * kModes2 * 2;
+  }
+  o.D = pos; pos += w;
+  o.bD = pos; pos += 1;
+  o.total = pos;
+  return o;
+}
+
+// Smallest divisor of K that is >= K / target (the split-K chunk; every chunk has the same length).
+int split_chunk(int K, int target) {
+  int c = std::max(1, (K + target - 1) / target);
+  while (K % c) ++c;
+  return c;
+}
+
+TrGemm gemm0() {
+  TrGemm g{};
+  g.nb0 = g.nb1 = 1;
+  g.alpha = 1.f;
+  return g;
+}
+
+// Truncated analysis X[b][i][j][c] -> C[b][part][kappa1][kappa2][c], times alpha (two GEMMs).
+cudaError_t tr_analysis(const TrWs& t, const float* X, float* Cout, int n, int B, int w, float alpha, cudaStream_t s) {
+  TrGemm g = gemm0();
+  g.M = 2 * kModes; g.N = w; g.K = n; g.nb0 = B; g.nb1 = n;
+  g.A = t.Fj; g.sAm = n; g.sAk = 1;
+  g.B = X; g.sBk = w; g.sBn = 1; g.sB0 = (ll)n * n * w; g.sB1 = (ll)n * w;
+  g.C = t.T; g.sCm = w; g.sCn = 1; g.sC0 = (ll)n * 2 * kModes * w; g.sC1 = (ll)2 * kModes * w;
+  cudaError_t e = launch_tr_gemm(g, s);
+  if (e != cudaSuccess) return e;
+  TrGemm h = gemm0();
+  h.M = 2 * kModes; h.N = kModes * w; h.K = 2 * n; h.nb0 = B;
+  h.A = t.Fi; h.sAm = 2 * n; h.sAk = 1;
+  h.B = t.T; h.sBk = (ll)kModes * w; h.sBn = 1; h.sB0 = (ll)n * 2 * kModes * w;
+  h.C = Cout; h.sCm = (ll)kModes * w; h.sCn = 1; h.sC0 = (ll)2 * kModes2 * w;
+  h.alpha = alpha;
+  return launch_tr_gemm(h, s);
+}
+
+// Truncated synthesis x = alpha Re sum_M G e^{+i theta} (+ beta x), G[b][part][kappa1][kappa2][o] -> x[b][i][j][o].
+cudaError_t tr_synthesis(const TrWs& t, const float* G, float* X, int n, int B, int w, float alpha, float beta,
+                         cudaStream_t s) {
+  TrGemm g = gemm0();
+  g.M = 2 * n; g.N = kModes * w; g.K = 2 * kModes; g.nb0 = B;
+  g.A = t.Gi; g.sAm = 2 * kModes; g.sAk = 1;
+  g.B = G; g.sBk = (ll)kModes * w; g.sBn = 1; g.sB0 = (ll)2 * kModes2 * w;
+  g.C = t.T; g.sCm = (ll)kModes * w; g.sCn = 1; g.sC0 = (ll)n * 2 * kModes * w;
+  cudaError_t e = launch_tr_gemm(g, s);
+  if (e != cudaSuccess) return e;
+  TrGemm h = gemm0();
+  h.M = n; h.N = w; h.K = 2 * kModes; h.nb0 = B; h.nb1 = n;
+  h.A = t.Gj; h.sAm = 2 * kModes; h.sAk = 1;
+  h.B = t.T; h.sBk = w; h.sBn = 1; h.sB0 = (ll)n * 2 * kModes * w; h.sB1 = (ll)2 * kModes * w;
+  h.C = X; h.sCm = w; h.sCn = 1; h.sC0 = (ll)n * n * w; h.sC1 = (ll)n * w;
+  h.alpha = alpha; h.beta = beta;
+  return launch_tr_gemm(h, s);
+}
+
+// out(m, n) = sum_p A(m, p) B(p, n) over p < K, as kTrSplit-way split-K partials reduced in order.
+cudaError_t tr_wgrad(const TrWs& t, int M, int N, int K, const float* A, ll sAm, ll sAk, const float* Bm, ll sBk, ll sBn,
+                     float* out, ll sOm, ll sOn, cudaStream_t s) {
+  const int chunk = split_chunk(K, kTrSplit), S = K / chunk;
+  TrGemm g = gemm0();
+  g.M = M; g.N = N; g.K = chunk; g.nb0 = S;
+  g.A = A; g.sAm = sAm; g.sAk = sAk; g.sA0 = chunk * sAk;
+  g.B = Bm; g.sBk = sBk; g.sBn = sBn; g.sB0 = chunk * sBk;
+  g.C = t.partials; g.sCm = N; g.sCn = 1; g.sC0 = (ll)M * N;
+  cudaError_t e = launch_tr_gemm(g, s);
+  if (e != cudaSuccess) return e;
+  return launch_tr_reduce(t.partials, S, M, N, out, sOm, sOn, s);
+}
+
+#define CKE(call)                                  \
+  do {                                             \
+    cudaError_t e_ = (call);                       \
+    if (e_ != cudaSuccess) return e_;              \
+  } while (0)
+
+// One minibatch: forward, loss, and (grad != nullptr) the full gradient of the mean loss.
+cudaError_t tr_loss_grad(const TrWs& t, fcgno_train_desc d, int B, const float* P, const double* k, const double* r,
+                         const double* e, const int* perm, const int* ksys, double* loss, float* grad, cudaStream_t s) {
+  const int n = d.n, w = d.width, N = n * n, BP = B * N;
+  const TrOff o = tr_offsets(w);
+  const size_t act = (size_t)BP * w;
+  CKE(launch_tr_twiddles(n, t.Fj, t.Fi, t.Gi, t.Gj, t.one, s));
+  CKE(launch_tr_gather(k, r, e, perm, ksys, N, B, t.kg, t.rg, t.eg, s));
+  CKE(cudaMemsetAsync(t.cnt, 0, sizeof(unsigned) * 3 * B, s));
+  CKE(launch_dot(t.rg, t.rg, t.rr, t.part, t.cnt, n, B, s));
+  // ---- forward (R10): lift, 4 layers, projection
+  CKE(launch_tr_lift(t.rg, t.kg, t.rr, P + o.E, P + o.bE, N, B, w, t.X2, t.V[0], s));
+  for (int l = 0; l < 4; ++l) {
+    float* zout = l < 3 ? t.Z[l] : t.V[4];
+    CKE(tr_analysis(t, t.V[l], t.Cs[l], n, B, w, 1.f, s));
+    CKE(launch_tr_mix_fwd(t.Cs[l], P + o.R[l], B, w, t.G, s));
+    CKE(tr_synthesis(t, t.G, zout, n, B, w, 1.f / float(N), 0.f, s));
+    TrGemm g = gemm0();          // z = v W^T + b + S L A v;  v' = GELU(z) (layers 1-3)
+    g.M = BP; g.N = w; g.K = w;
+    g.A = t.V[l]; g.sAm = w; g.sAk = 1;
+    g.B = P + o.W[l]; g.sBk = 1; g.sBn = w;
+    g.C = zout; g.sCm = w; g.sCn = 1;
+    g.beta = 1.f;
+    g.epi = l < 3 ? TR_EPI_BIAS_GELU : TR_EPI_BIAS;
+    g.bias = P + o.b[l];
+    g.aux = l < 3 ? t.V[l + 1] : nullptr;
+    CKE(launch_tr_gemm(g, s));
+  }
+  CKE(launch_tr_proj(t.V[4], P + o.D, P + o.bD, t.rr, t.eg, N, B, w, nullptr, t.d, s));
+  // ---- loss
+  const double* gvec = t.d;
+  if (d.loss == FCGNO_LOSS_NOTAY) {
+    CKE(launch_apply_A(t.kg, t.d, t.Ad, n, B, false, s));
+    CKE(launch_apply_A(t.kg, t.eg, t.Ae, n, B, false, s));
+    CKE(launch_dot(t.d, t.Ad, t.dAd, t.part, t.cnt + B, n, B, s));
+    CKE(launch_dot(t.eg, t.Ae, t.eAe, t.part, t.cnt + 2 * B, n, B, s));
+    gvec = t.Ad;
+  } else {
+    CKE(launch_dot(t.d, t.d, t.dAd, t.part, t.cnt + B, n, B, s));
+    CKE(launch_dot(t.eg, t.eg, t.eAe, t.part, t.cnt + 2 * B, n, B, s));
+  }
+  CKE(launch_tr_loss(t.dAd, t.eAe, t.rr, B, B, loss, t.coef, s));
+  if (!grad) return cudaSuccess;
+  // ---- backward (oracle/train.py no_backward)
+  CKE(launch_tr_dout(gvec, t.coef, P + o.D, N, B, w, t.dout, t.DV, s));
+  CKE(tr_wgrad(t, 1, w, BP, t.dout, 0, 1, t.V[4], w, 1, grad + o.D, 0, 1, s));          // dD
+  CKE(tr_wgrad(t, 1, 1, BP, t.dout, 0, 1, t.one, 0, 0, grad + o.bD, 0, 0, s));           // dbD
+  float *DV = t.DV, *DV2 = t.DV2;
+  for (int l = 3; l >= 0; --l) {
+    if (l < 3) CKE(launch_tr_gelu_bwd(DV, t.Z[l], act, s));                              // dz (in place)
+    CKE(tr_wgrad(t, w, w, BP, DV, 1, w, t.V[l], w, 1, grad + o.W[l], w, 1, s));          // dW[o][c]
+    CKE(tr_wgrad(t, 1, w, BP, t.one, 0, 0, DV, w, 1, grad + o.b[l], 0, 1, s));           // db
+    CKE(tr_analysis(t, DV, t.DG, n, B, w, 1.f / float(N), s));                           // dg = A(dz)/n^2
+    CKE(launch_tr_mix_bwd(t.Cs[l], t.DG, P + o.R[l], B, w, grad + o.R[l], t.DC, s));     // dR, dc
+    CKE(tr_synthesis(t, t.DC, DV2, n, B, w, 1.f, 0.f, s));                               // dv = n^2 S(dc)
+    TrGemm g = gemm0();                                                                   // dv += dz W
+    g.M = BP; g.N = w; g.K = w;
+    g.A = DV; g.sAm = w; g.sAk = 1;
+    g.B = P + o.W[l]; g.sBk = w; g.sBn = 1;
+    g.C = DV2; g.sCm = w; g.sCn = 1;
+    g.beta = 1.f;
+    CKE(launch_tr_gemm(g, s));
+    std::swap(DV, DV2);
+  }
+  CKE(tr_wgrad(t, 2, w, BP, t.X2, 1, 2, DV, w, 1, grad + o.E, 1, 2, s));                // dE[c][i]
+  CKE(tr_wgrad(t, 1, w, BP, t.one, 0, 0, DV, w, 1, grad + o.bE, 0, 1, s));              // dbE
+  return cudaSuccess;
+}
+#undef CKE
+
+}  // namespace
+
+extern "C" {
+
+size_t fcgno_train_param_count(int32_t width) { return width >= 1 ? tr_offsets(width).total : 0; }
+
+size_t fcgno_train_workspace_bytes(fcgno_train_desc d) {
+  if (check_train_desc(d) != FCGNO_OK) return 0;
+  Carver c(nullptr);
+  carve_train(c, d);
+  return c.bytes();
+}
+
+int fcgno_train_loss_grad(fcgno_train_desc d, int32_t count, const float* params, const double* k, const double* r,
+                          const double* e, const int32_t* perm, const int32_t* ksys, double* loss, float* grad,
+                          void* ws, size_t ws_bytes, void* stream) {
+  if (int rc = check_train_desc(d)) return rc;
+  if (!params || !k || !r || !e || !ws) return fail(FCGNO_EINVAL, "train_loss_grad: NULL argument");
+  if (count < 1 || count > d.batch) return fail(FCGNO_EINVAL, "train_loss_grad: count %d outside 1..%d", count, d.batch);
+  if (!aligned(ws) || ws_bytes < fcgno_train_workspace_bytes(d)) return fail(FCGNO_EWORKSPACE, "train_loss_grad: workspace");
+  CK(prepare_tr_kernels());
+  Carver c(ws);
+  const TrWs t = carve_train(c, d);
+  CK(tr_loss_grad(t, d, count, params, k, r, e, perm, ksys, loss, grad, static_cast<cudaStream_t>(stream)));
+  return FCGNO_OK;
+}
+
+int fcgno_adamw_step(size_t count, float* params, const float* grad, float* m, float* v, int32_t t, fcgno_adamw_opts o,
+                     void* stream) {
+  if (!params || !grad || !m || !v) return fail(FCGNO_EINVAL, "adamw_step: NULL argument");
+  if (t < 1 || !(o.lr >= 0) || !(o.beta1 >= 0 && o.beta1 < 1) || !(o.beta2 >= 0 && o.beta2 < 1) || !(o.eps > 0))
+    return fail(FCGNO_EINVAL, "adamw_step: bad step or hyperparameters");
+  if (count == 0) return FCGNO_OK;
+  CK(launch_tr_adamw(count, params, grad, m, v, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay, t,
+                     static_cast<cudaStream_t>(stream)));
+  return FCGNO_OK;
+}
+
+int fcgno_train_epoch(fcgno_train_desc d, int32_t nsamples, float* params, float* grad, float* m, float* v,
+                      int32_t* t_host, fcgno_adamw_opts o, const double* k, const double* r, const double* e,
+                      const int32_t* perm, const int32_t* ksys, double* loss, void* ws, size_t ws_bytes,
+                      void* stream) {
+  if (int rc = check_train_desc(d)) return rc;
+  if (!params || !grad || !m || !v || !t_host || !k || !r || !e || !perm || !ws)
+    return fail(FCGNO_EINVAL, "train_epoch: NULL argument");
+  if (nsamples < 1) return fail(FCGNO_EINVAL, "train_epoch: nsamples %d", nsamples);
+  if (!aligned(ws) || ws_bytes < fcgno_train_workspace_bytes(d)) return fail(FCGNO_EWORKSPACE, "train_epoch: workspace");
+  CK(prepare_tr_kernels());
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Carver c(ws);
+  const TrWs t = carve_train(c, d);
+  const size_t P = tr_offsets(d.width).total;
+  for (int s0 = 0; s0 < nsamples; s0 += d.batch) {
+    const int cnt = std::min(d.batch, nsamples - s0);
+    CK(tr_loss_grad(t, d, cnt, params, k, r, e, perm + s0, ksys, loss ? loss + s0 : nullptr, grad, s));
+    const int step = ++*t_host;
+    CK(launch_tr_adamw(P, params, grad, m, v, o.lr, o.beta1, o.beta2, o.eps, o.weight_decay, step, s));
+  }
+  return FCGNO_OK;
+}
+
+int fcgno_krylov_pair(const fcgno_problem* p, const double* f, const double* u_star, const double* u, double* r,
+                      double* e, void* stream) {
+  if (!p || !f || !u_star || !u || !r || !e) return fail(FCGNO_EINVAL, "krylov_pair: NULL argument");
+  if (r == u || r == f || e == u || e == u_star || r == e) return fail(FCGNO_EINVAL, "krylov_pair: outputs alias inputs");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CK(launch_apply_A(p->k, u, r, p->n, p->B, p->kfast, s));
+  CK(launch_tr_pair(f, r, u_star, u, (size_t)p->B * p->n * p->n, r, e, s));
+  return FCGNO_OK;
+}
+
+}  // extern "C"

@@ -164,6 +164,42 @@ cudaError_t prepare_no_constants(const NoDev<float>& no, cudaStream_t s);
 template <typename T>
 size_t no_max_smem(int n, int w);   // largest dynamic smem any NO kernel needs for (n, w)
 
+// SNO training (train_kernels.cu).  Batched strided fp32 GEMM:
+// C[z](m,n) = alpha sum_k A[z](m,k) B[z](k,n) + beta C[z](m,n) (+ bias[n]; GELU copy to aux), z = b0 nb1 + b1.
+enum : int { TR_EPI_STORE = 0, TR_EPI_BIAS = 1, TR_EPI_BIAS_GELU = 2 };
+struct TrGemm {
+  int M, N, K, nb0, nb1;
+  const float* A; long long sAm, sAk, sA0, sA1;
+  const float* B; long long sBk, sBn, sB0, sB1;
+  float* C; long long sCm, sCn, sC0, sC1;
+  float alpha, beta;
+  int epi; const float* bias; float* aux;
+};
+cudaError_t launch_tr_gemm(const TrGemm& g, cudaStream_t s);
+cudaError_t launch_tr_reduce(const float* part, int S, int M, int N, float* out, long long sOm, long long sOn,
+                             cudaStream_t s);
+cudaError_t launch_tr_twiddles(int n, float* Fj, float* Fi, float* Gi, float* Gj, float* one, cudaStream_t s);
+cudaError_t launch_tr_gather(const double* k, const double* r, const double* e, const int* perm, const int* ksys, int N,
+                             int B, double* kg, double* rg, double* eg, cudaStream_t s);
+cudaError_t launch_tr_lift(const double* rg, const double* kg, const double* rr, const float* E, const float* bE, int N,
+                           int B, int w, float* X2, float* v0, cudaStream_t s);
+cudaError_t launch_tr_proj(const float* v4, const float* D, const float* bD, const double* rr, const double* eg, int N,
+                           int B, int w, double* wout, double* d, cudaStream_t s);
+cudaError_t launch_tr_loss(const double* dd, const double* ee, const double* rr, int B, int Bmean, double* loss,
+                           double* coef, cudaStream_t s);
+cudaError_t launch_tr_dout(const double* gvec, const double* coef, const float* D, int N, int B, int w, float* dout,
+                           float* dv, cudaStream_t s);
+cudaError_t launch_tr_gelu_bwd(float* dv, const float* z, size_t count, cudaStream_t s);
+size_t tr_mix_smem(int B, int w, bool bwd);
+cudaError_t prepare_tr_kernels();
+cudaError_t launch_tr_mix_fwd(const float* C, const float* R, int B, int w, float* G, cudaStream_t s);
+cudaError_t launch_tr_mix_bwd(const float* C, const float* dG, const float* R, int B, int w, float* dR, float* dC,
+                              cudaStream_t s);
+cudaError_t launch_tr_adamw(size_t count, float* th, const float* g, float* m, float* v, double lr, double b1, double b2,
+                            double eps, double wd, int t, cudaStream_t s);
+cudaError_t launch_tr_pair(const double* f, const double* Au, const double* ustar, const double* u, size_t count,
+                           double* r, double* e, cudaStream_t s);
+
 uint64_t& launch_counter();
 
 // Theorem-1 / Notay diagnostics (diag_kernels.cu)

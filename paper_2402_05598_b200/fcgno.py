@@ -27,6 +27,7 @@ FOURIER, CHEBYSHEV = 0, 1  # SNO basis (fcgno_basis)
 SCHEDULE_PAPER, SCHEDULE_SLIDING = 0, 1
 RUNNING, CONVERGED, MAXIT, BREAKDOWN, NONFINITE = 0, 1, 2, 3, 4
 K_MODES = 20
+LOSS_NOTAY, LOSS_L2 = 0, 1
 ERRORS = {1: "EINVAL", 2: "ENONPOS_K", 3: "ECUDA", 4: "EWORKSPACE", 5: "EUNSUPPORTED"}
 
 
@@ -43,6 +44,16 @@ class Grid(ctypes.Structure):
 class NoDesc(ctypes.Structure):
     _fields_ = [("width", ctypes.c_int32), ("precision", ctypes.c_int32), ("use_gelu", ctypes.c_int32),
                 ("basis", ctypes.c_int32)]
+
+
+class TrainDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("width", ctypes.c_int32), ("batch", ctypes.c_int32),
+                ("loss", ctypes.c_int32)]
+
+
+class AdamWOpts(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -83,6 +94,13 @@ EXPORTS = {
     "fcgno_profile_name": (ctypes.c_char_p, [_i]),
     "fcgno_kernel_launches": (ctypes.c_uint64, []),
     "fcgno_debug_px_trace": (_i, [_vp, _i]),
+    "fcgno_train_param_count": (_sz, [ctypes.c_int32]),
+    "fcgno_train_workspace_bytes": (_sz, [TrainDesc]),
+    "fcgno_train_loss_grad": (_i, [TrainDesc, ctypes.c_int32, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_adamw_step": (_i, [_sz, _vp, _vp, _vp, _vp, ctypes.c_int32, AdamWOpts, _vp]),
+    "fcgno_train_epoch": (_i, [TrainDesc, ctypes.c_int32, _vp, _vp, _vp, _vp, _P(ctypes.c_int32), AdamWOpts, _vp,
+                               _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "fcgno_krylov_pair": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "fcgno_last_error": (ctypes.c_char_p, []),
     "fcgno_abi_version": (_i, []),
 }
@@ -381,3 +399,75 @@ def fcg_solve_stationary(problem: Problem, f: torch.Tensor, u0: torch.Tensor | N
     _check(_lib.fcgno_fcg_solve_stationary(problem._h, int(kind), int(sweeps), _ptr(f), _ptr(u), opts, _ptr(iters),
                                            _ptr(status), _ptr(hist), _ptr(ws), ws.numel(), _stream()))
     return SolveResult(u, iters, status, hist)
+
+
+# ------------------------------------------------------------------ training
+def krylov_pair(problem: Problem, f: torch.Tensor, u_star: torch.Tensor, u: torch.Tensor, stream=None):
+    """Training pair of every system (Eq. 8-9; fcgno_krylov_pair): r = f - A u, e = u_star - u."""
+    for name, t in (("f", f), ("u_star", u_star), ("u", u)):
+        _require(t, problem.shape, name)
+    r = _on(stream, lambda: torch.empty_like(f))
+    e = _on(stream, lambda: torch.empty_like(f))
+    _check(_lib.fcgno_krylov_pair(problem._h, _ptr(f), _ptr(u_star), _ptr(u), _ptr(r), _ptr(e), _stream(stream)))
+    return r, e
+
+
+def train_param_count(width: int) -> int:
+    return int(_lib.fcgno_train_param_count(int(width)))
+
+
+class Trainer:
+    """fp32 SNO weights, AdamW state and the training workspace (fcgno_train_*).  The weights use the
+    canonical blob order (include/fcgno.h), so `blob()` feeds NeuralOperator directly."""
+
+    def __init__(self, n: int, width: int, batch: int, blob: np.ndarray, loss: int = LOSS_NOTAY, device="cuda",
+                 lr: float = 1e-3, weight_decay: float = 1e-2, betas=(0.9, 0.999), eps: float = 1e-8):
+        self.desc = TrainDesc(int(n), int(width), int(batch), int(loss))
+        nbytes = _lib.fcgno_train_workspace_bytes(self.desc)
+        if nbytes == 0:
+            raise FcgnoError(1, _lib.fcgno_last_error().decode())
+        self.P = train_param_count(width)
+        blob = np.ascontiguousarray(blob, dtype=np.float64)
+        if blob.size != self.P:
+            raise ValueError("weight blob size mismatch")
+        self.width, self.n, self.batch = int(width), int(n), int(batch)
+        self.params = torch.tensor(blob, dtype=torch.float32, device=device)
+        self.grad = torch.zeros_like(self.params)
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.t = ctypes.c_int32(0)
+        self.opts = AdamWOpts(float(lr), float(betas[0]), float(betas[1]), float(eps), float(weight_decay))
+        self.ws = _workspace(nbytes, device)
+        self.device = device
+
+    def blob(self) -> np.ndarray:
+        """Canonical fp64 blob of the current weights (for NeuralOperator / the oracle)."""
+        return self.params.double().cpu().numpy()
+
+    def loss_grad(self, k, r, e, perm=None, ksys=None, count=None, grad=True, stream=None):
+        """Per-sample losses [count] (and self.grad = d mean loss / d theta) of samples perm[:count]."""
+        count = int(perm.numel() if perm is not None else (count or r.shape[0]))
+        loss = _on(stream, lambda: torch.empty(count, dtype=torch.float64, device=self.device))
+        _check(_lib.fcgno_train_loss_grad(self.desc, count, _ptr(self.params), _ptr(k), _ptr(r), _ptr(e), _ptr(perm),
+                                          _ptr(ksys), _ptr(loss), _ptr(self.grad) if grad else None, _ptr(self.ws),
+                                          self.ws.numel(), _stream(stream)))
+        return loss
+
+    def adamw_step(self, lr: float | None = None, stream=None):
+        if lr is not None:
+            self.opts.lr = float(lr)
+        self.t.value += 1
+        _check(_lib.fcgno_adamw_step(self.P, _ptr(self.params), _ptr(self.grad), _ptr(self.m), _ptr(self.v),
+                                     self.t.value, self.opts, _stream(stream)))
+
+    def epoch(self, k, r, e, perm, ksys=None, lr: float | None = None, stream=None) -> torch.Tensor:
+        """One pass over the samples in the order perm (int32 device): minibatch loss/grad + AdamW steps.
+        Returns the per-sample losses (before each minibatch's step), in perm order."""
+        if lr is not None:
+            self.opts.lr = float(lr)
+        ns = int(perm.numel())
+        loss = _on(stream, lambda: torch.empty(ns, dtype=torch.float64, device=self.device))
+        _check(_lib.fcgno_train_epoch(self.desc, ns, _ptr(self.params), _ptr(self.grad), _ptr(self.m), _ptr(self.v),
+                                      ctypes.byref(self.t), self.opts, _ptr(k), _ptr(r), _ptr(e), _ptr(perm),
+                                      _ptr(ksys), _ptr(loss), _ptr(self.ws), self.ws.numel(), _stream(stream)))
+        return loss

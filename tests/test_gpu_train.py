@@ -1,0 +1,180 @@
+"""GPU parity of SNO training through the C-ABI against oracle/train.py.
+
+Tolerances: the training forward runs in fp32 (R18), the loss and its A-norms in fp64, so
+  per-sample loss                 <= 1e-5 relative
+  gradient, every weight block    <= 1e-4 relative L2 (fp32 GEMM accumulation over B n^2 pixels)
+  AdamW                           <= 1e-6 relative (fp32 state vs the fp64 oracle)
+  Krylov pairs                    bitwise (the identity FCG iterate is bitwise, R5/R6)
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as orc
+import synthetic as sy
+from oracle import train as otr
+
+pytestmark = pytest.mark.gpu
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def blocks(w):
+    """Canonical blob blocks (include/fcgno.h)."""
+    out, pos = {}, 0
+    def take(name, size):
+        nonlocal pos
+        out[name] = (pos, pos + size)
+        pos += size
+    take("E", 2 * w); take("bE", w)
+    for l in range(4):
+        take(f"W{l}", w * w); take(f"b{l}", w); take(f"R{l}", 2 * w * w * 400)
+    take("D", w); take("bD", 1)
+    return out
+
+
+def samples(n, B, seed, kind="lognormal"):
+    k = sy.lognormal_k(n, B, 0.1, 1.0, seed) if kind == "lognormal" else sy.rectangles_k(n, B, seed)
+    r = sy.normal_field(n, B, seed + 1)
+    if n <= 32:
+        e = np.stack([np.linalg.solve(orc.dense_A(k[b]), r[b].ravel()).reshape(n, n) for b in range(B)])
+    else:   # any e works for the loss parity; use a smooth stand-in of A^-1 r's scale
+        e = r / (8.0 * (n + 1) ** 2) + 1e-3 * sy.normal_field(n, B, seed + 2)
+    return k, r, e
+
+
+@pytest.mark.parametrize("n,w,B,loss", [(20, 4, 3, "notay"), (32, 8, 5, "l2"), (33, 5, 2, "notay"),
+                                        (64, 48, 4, "notay")])
+def test_loss_and_gradient_match_oracle(lib, n, w, B, loss):
+    k, r, e = samples(n, B, 11 + n)
+    blob = sy.no_weights(w, 3)
+    kind = lib.LOSS_NOTAY if loss == "notay" else lib.LOSS_L2
+    tr = lib.Trainer(n, w, B, blob, loss=kind)
+    lg = host(tr.loss_grad(dev(k), dev(r), dev(e)))
+    g = host(tr.grad).astype(np.float64)
+    ref_l, ref_g = otr.loss_and_grad(blob, w, r, e, k, loss)
+    assert np.max(np.abs(lg - ref_l) / ref_l) <= 1e-5, (lg, ref_l)
+    for name, (a, b) in blocks(w).items():
+        num = np.linalg.norm(g[a:b] - ref_g[a:b])
+        den = np.linalg.norm(ref_g[a:b])
+        assert num <= 1e-4 * den + 1e-12, (name, num / den)
+
+
+def test_gradient_permuted_minibatch_and_shared_k(lib):
+    """perm / ksys gather: samples 4, 1 with the coefficient fields of systems ksys = [0, 0, 1, 1, 0]."""
+    n, w = 24, 6
+    k, r, e = samples(n, 5, 7)
+    ks = np.array([0, 0, 1, 1, 0], dtype=np.int32)
+    perm = np.array([4, 1], dtype=np.int32)
+    blob = sy.no_weights(w, 9)
+    tr = lib.Trainer(n, w, 4, blob)
+    lg = host(tr.loss_grad(dev(k[:2]), dev(r), dev(e), perm=torch.from_numpy(perm).cuda(),
+                           ksys=torch.from_numpy(ks).cuda()))
+    kk = k[ks[perm]]
+    ref_l, ref_g = otr.loss_and_grad(blob, w, r[perm], e[perm], kk, "notay")
+    assert np.max(np.abs(lg - ref_l) / ref_l) <= 1e-5
+    g = host(tr.grad).astype(np.float64)
+    assert np.linalg.norm(g - ref_g) <= 1e-4 * np.linalg.norm(ref_g)
+
+
+def test_training_step_is_deterministic(lib):
+    n, w, B = 32, 16, 8
+    k, r, e = samples(n, B, 21)
+    tr = lib.Trainer(n, w, B, sy.no_weights(w, 2))
+    tr.loss_grad(dev(k), dev(r), dev(e))
+    g1 = tr.grad.clone()
+    tr.loss_grad(dev(k), dev(r), dev(e))
+    assert torch.equal(g1, tr.grad)
+
+
+def test_training_forward_matches_production_no(lib):
+    """The training forward is the production NO (fcgno_apply_NO): the loss of the production output,
+    evaluated by the oracle, equals the training loss."""
+    n, w, B = 64, 48, 4
+    k, r, e = samples(n, B, 31)
+    blob = sy.no_weights(w, 5)
+    tr = lib.Trainer(n, w, B, blob)
+    lg = host(tr.loss_grad(dev(k), dev(r), dev(e), grad=False))
+    p = lib.Problem(dev(k))
+    no = lib.NeuralOperator(w, blob)
+    wp = host(no.apply(p, dev(r)))
+    ref = np.array([otr.notay_loss(k[b], wp[b], e[b])[0] for b in range(B)])
+    assert np.max(np.abs(lg - ref) / ref) <= 1e-4
+
+
+def test_adamw_matches_oracle(lib):
+    rng = np.random.default_rng(4)
+    P = 1000
+    th = rng.normal(size=P)
+    grads = [rng.normal(size=P) * 10.0 ** rng.uniform(-3, 1) for _ in range(5)]
+    tr = lib.Trainer(20, 1, 1, np.zeros(lib.train_param_count(1)))
+    params = torch.tensor(th, dtype=torch.float32, device="cuda")
+    m = torch.zeros_like(params); v = torch.zeros_like(params)
+    mo, vo, cur = np.zeros(P), np.zeros(P), th.astype(np.float32).astype(np.float64)
+    for t, g in enumerate(grads, start=1):
+        gd = torch.tensor(g, dtype=torch.float32, device="cuda")
+        opts = lib.AdamWOpts(1e-3, 0.9, 0.999, 1e-8, 1e-2)
+        lib._check(lib._lib.fcgno_adamw_step(P, lib._ptr(params), lib._ptr(gd), lib._ptr(m), lib._ptr(v), t, opts,
+                                             lib._stream()))
+        cur, mo, vo = otr.adamw_step(cur, g.astype(np.float32).astype(np.float64), mo, vo, t, 1e-3)
+        got = host(params).astype(np.float64)
+        assert np.max(np.abs(got - cur) / np.maximum(np.abs(cur), 1e-3)) <= 1e-6, t
+    del tr
+
+
+def test_krylov_pairs_bitwise(lib):
+    """Fig. 3 (a)-(b) on the GPU: u_i from fcgno_fcg_solve(B = I, maxit = i), r_i = f - A u_i and
+    e_i = u* - u_i from fcgno_krylov_pair, bitwise equal to oracle.train.krylov_samples given the same u*."""
+    from paper_2402_05598_b200 import train as ptr
+    n, B = 24, 3
+    k = sy.lognormal_k(n, B, 0.1, 1.0, 41)
+    f = sy.normal_field(n, B, 42)
+    u0 = sy.normal_field(n, B, 43)
+    p = lib.Problem(dev(k))
+    iters = [0, 1, 7, 20]
+    r, e, ksys, it_exact = ptr.krylov_dataset(p, dev(f), dev(u0), iters, m=5, tol_exact=1e-12)
+    assert np.array_equal(host(ksys), np.arange(len(iters) * B) % B)
+    r, e = host(r), host(e)
+    ustar = host(lib.fcg_solve(p, dev(f), dev(u0), m=5, tol=1e-12, maxit=20000, history=False).u)
+    for b in range(B):
+        ro, eo, _ = otr.krylov_samples(k[b], f[b], u0[b], iters, m_max=5, u_exact=ustar[b])
+        for s in range(len(iters)):
+            assert np.array_equal(r[s * B + b], ro[s]), (b, iters[s])
+            assert np.array_equal(e[s * B + b], eo[s]), (b, iters[s])
+
+
+def test_training_reduces_loss_and_preconditions(lib):
+    """Fig. 3 end to end at config 1's geometry (n = 32) with a narrow SNO: the Notay loss on held-out
+    Krylov samples falls well below the random-init value, and FCG with the trained NO converges on
+    held-out systems in fewer iterations than FCG(I) (where the random-init NO stagnates)."""
+    from paper_2402_05598_b200 import train as ptr
+    n, w, Bs = 32, 16, 48
+    k = sy.lognormal_k(n, Bs, 0.1, 1.0, 100)
+    f = sy.normal_field(n, Bs, 101)
+    u0 = np.zeros((Bs, n, n))
+    p = lib.Problem(dev(k))
+    r, e, ksys, _ = ptr.krylov_dataset(p, dev(f), dev(u0), [0, 2, 5, 10, 20, 40, 80], m=5)
+    tr = lib.Trainer(n, w, 16, sy.no_weights(w, 7))
+    kt = dev(k)
+    # held-out systems
+    kh = sy.lognormal_k(n, 8, 0.1, 1.0, 200)
+    fh = sy.normal_field(n, 8, 201)
+    ph = lib.Problem(dev(kh))
+    rh, eh, ksh, _ = ptr.krylov_dataset(ph, dev(fh), dev(np.zeros((8, n, n))), [0, 5, 20], m=5)
+    l0 = float(tr.loss_grad(dev(kh), rh[:16], eh[:16], ksys=ksh, count=16, grad=False).mean())
+    curve = ptr.train(tr, kt, r, e, ksys, epochs=60, seed=0)
+    l1 = float(tr.loss_grad(dev(kh), rh[:16], eh[:16], ksys=ksh, count=16, grad=False).mean())
+    assert curve[-1] < 0.5 * curve[0]
+    assert l1 < 0.6 * l0, (l0, l1)
+    no = ptr.trained_operator(tr)
+    res = lib.fcg_solve(ph, dev(fh), m=5, tol=1e-6, maxit=500, no=no, history=False)
+    ide = lib.fcg_solve(ph, dev(fh), m=5, tol=1e-6, maxit=500, history=False)
+    st, it, it_id = host(res.status), host(res.iters), host(ide.iters)
+    assert np.all(st == lib.CONVERGED), st
+    assert np.mean(it) < np.mean(it_id), (it, it_id)
