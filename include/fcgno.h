@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define FCGNO_ABI_VERSION 8
+#define FCGNO_ABI_VERSION 9
 #define FCGNO_K_MODES 20   /* modes per dimension, "number of orthogonal polynomials is 20" */
 #define FCGNO_LAYERS 4     /* PAPER.md:530 "Number of SNO layers is 4" */
 #define FCGNO_MMAX 64      /* largest truncation parameter m accepted by fcgno_fcg_solve */
@@ -288,10 +288,13 @@ FCGNO_API int fcgno_train_epoch(fcgno_train_desc d, int32_t nsamples, float* par
                                 const double* e, const int32_t* perm, const int32_t* ksys, double* loss, void* ws,
                                 size_t ws_bytes, void* stream);
 /* Krylov training pair (Eq. 8-9) of every system of the problem:
- * r = f - A u (u the CG iterate u_i), e = u_star - u (u_star = u_exact, e.g. a tight FCG(I) solve);
- * fp64 [B][n][n] device, outputs must not alias inputs.  Bitwise the oracle's arithmetic (R5). */
+ * r = f - A u (u the CG iterate u_i), e = e_scale (u_star - u) (u_star = u_exact, e.g. a tight FCG(I)
+ * solve); fp64 [B][n][n] device, outputs must not alias inputs.  e_scale > 0 is the unit of the target
+ * (R27: 1 = A^{-1} r as printed; (n+1)^2 = the error in units of the unscaled stencil
+ * h^2 A, which keeps the trained output weights O(1); FCG is invariant to a positive scaling of B).
+ * Bitwise the oracle's arithmetic (R5).  FCGNO_EINVAL for e_scale <= 0 or non-finite. */
 FCGNO_API int fcgno_krylov_pair(const fcgno_problem* p, const double* f, const double* u_star, const double* u,
-                                double* r, double* e, void* stream);
+                                double e_scale, double* r, double* e, void* stream);
 
 /* End-to-end convenience entry point with HOST buffers ([host], pageable or pinned): copies
  * k, f, u0 to the device, assembles, solves and copies u, iters, status (and history if

@@ -142,10 +142,10 @@ def lr_at_epoch(epoch: int, lr0: float = 1e-3, decay: float = 0.5, every: int = 
     return lr0 * decay ** (epoch // every)
 
 
-def krylov_samples(k, f, u0, iters, m_max=5, u_exact=None, tol_exact=1e-13, maxit_exact=100000):
+def krylov_samples(k, f, u0, iters, m_max=5, u_exact=None, tol_exact=1e-13, maxit_exact=100000, e_scale=1.0):
     """Training pairs of one system (Eq. 8-9; Fig. 3): for each i in `iters`, the CG
     iterate u_i (FCG with B = I stopped after i iterations, Algorithm 1), r_i = f - A u_i and
-    e_i = u_exact - u_i.  u_exact: a tight FCG(I) solve unless given.  Returns (r [S][n][n],
+    e_i = e_scale (u_exact - u_i) (e_scale: the unit of the target, R27; 1 as printed).  u_exact: a tight FCG(I) solve unless given.  Returns (r [S][n][n],
     e [S][n][n], u_exact)."""
     A = lambda x: apply_A(k, x)
     if u_exact is None:
@@ -154,5 +154,5 @@ def krylov_samples(k, f, u0, iters, m_max=5, u_exact=None, tol_exact=1e-13, maxi
     for i in iters:
         u_i = fcg(A, f, u0, m_max, 0.0, int(i))["u"]
         rs.append(f - A(u_i))
-        es.append(u_exact - u_i)
+        es.append(e_scale * (u_exact - u_i))
     return np.array(rs), np.array(es), u_exact

@@ -1441,13 +1441,14 @@ int fcgno_train_epoch(fcgno_train_desc d, int32_t nsamples, float* params, float
   return FCGNO_OK;
 }
 
-int fcgno_krylov_pair(const fcgno_problem* p, const double* f, const double* u_star, const double* u, double* r,
-                      double* e, void* stream) {
+int fcgno_krylov_pair(const fcgno_problem* p, const double* f, const double* u_star, const double* u, double e_scale,
+                      double* r, double* e, void* stream) {
   if (!p || !f || !u_star || !u || !r || !e) return fail(FCGNO_EINVAL, "krylov_pair: NULL argument");
+  if (!(e_scale > 0.0) || !std::isfinite(e_scale)) return fail(FCGNO_EINVAL, "krylov_pair: e_scale must be positive and finite");
   if (r == u || r == f || e == u || e == u_star || r == e) return fail(FCGNO_EINVAL, "krylov_pair: outputs alias inputs");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CK(launch_apply_A(p->k, u, r, p->n, p->B, p->kfast, s));
-  CK(launch_tr_pair(f, r, u_star, u, (size_t)p->B * p->n * p->n, r, e, s));
+  CK(launch_tr_pair(f, r, u_star, u, (size_t)p->B * p->n * p->n, e_scale, r, e, s));
   return FCGNO_OK;
 }
 

@@ -198,7 +198,7 @@ cudaError_t launch_tr_mix_bwd(const float* C, const float* dG, const float* R, i
 cudaError_t launch_tr_adamw(size_t count, float* th, const float* g, float* m, float* v, double lr, double b1, double b2,
                             double eps, double wd, int t, cudaStream_t s);
 cudaError_t launch_tr_pair(const double* f, const double* Au, const double* ustar, const double* u, size_t count,
-                           double* r, double* e, cudaStream_t s);
+                           double e_scale, double* r, double* e, cudaStream_t s);
 
 uint64_t& launch_counter();
 

@@ -48,17 +48,52 @@ __device__ __forceinline__ float ex2_approx(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// GELU(x) = x/2 (1 + erf(x / sqrt 2)) (reading R11), erf by Abramowitz & Stegun 7.1.26 (|error| <=
-// 1.5e-7, two orders below the 3xBF16 operand rounding) evaluated branch-free through erfc.
-__device__ __forceinline__ float gelu_px(float x) {
-  const float t = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x), 1.0f));
-  float p = fmaf(1.061405429f, t, -1.453152027f);
-  p = fmaf(p, t, 1.421413741f);
-  p = fmaf(p, t, -0.284496736f);
-  p = fmaf(p, t, 0.254829592f);
-  p *= t;
-  const float pe = p * ex2_approx((x * x) * -0.72134752044448170f);
-  return 0.5f * x * (x >= 0.f ? 2.0f - pe : pe);
+// packed fp32 pairs (FFMA2 / FMUL2 / FADD2 on sm_100a: one issue slot for two lanes of arithmetic)
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t r, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); }
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// GELU(x) = x/2 (1 + erf(x / sqrt 2)) (reading R11) of two values, erf by Abramowitz & Stegun 7.1.26
+// (|error| <= 1.5e-7, two orders below the 3xBF16 operand rounding) through erfc: with h = x/2 and
+// pe = poly(t) exp(-x^2/2), t = 1/(1 + p|x|/sqrt 2),  GELU = h + |h| - |h| pe  (x >= 0: h (2 - pe);
+// x < 0: h pe, the sum h + |h| being exactly 0).  Branch-free; the polynomial, the squares and the
+// scalings run as packed pairs, the two MUFU operations (rcp, ex2) per value as scalars.
+__device__ __forceinline__ void gelu_px2(float& x0, float& x1) {
+  const float t0 = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x0), 1.0f));
+  const float t1 = rcp_approx(fmaf(0.3275911f * 0.70710678118654752f, fabsf(x1), 1.0f));
+  const uint64_t X = pk2(x0, x1), T = pk2(t0, t1);
+  uint64_t P = fma2(pk2(1.061405429f, 1.061405429f), T, pk2(-1.453152027f, -1.453152027f));
+  P = fma2(P, T, pk2(1.421413741f, 1.421413741f));
+  P = fma2(P, T, pk2(-0.284496736f, -0.284496736f));
+  P = fma2(P, T, pk2(0.254829592f, 0.254829592f));
+  P = mul2(P, T);
+  const uint64_t Z = mul2(mul2(X, X), pk2(-0.72134752044448170f, -0.72134752044448170f));
+  float z0, z1;
+  upk2(Z, z0, z1);
+  const uint64_t PE = mul2(P, pk2(ex2_approx(z0), ex2_approx(z1)));
+  const uint64_t H = mul2(X, pk2(0.5f, 0.5f));
+  float h0, h1, pe0, pe1;
+  upk2(H, h0, h1);
+  upk2(PE, pe0, pe1);
+  x0 = fmaf(-fabsf(h0), pe0, h0 + fabsf(h0));
+  x1 = fmaf(-fabsf(h1), pe1, h1 + fabsf(h1));
 }
 
 // bulk copy shared -> global (async proxy), completion tracked by bulk groups
@@ -476,6 +511,7 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
     const uint32_t poff = (uint32_t)(p >> 3) * 128u + (uint32_t)(p & 7) * 16u;
     int t = 0;
     int u = next_unit(blockIdx.x);
+    const bool use_gelu = a.use_gelu != 0;
     double inv_next = (FIRST && u < nunits) ? __ldg(a.rr + u / g.units) : 0.0;   // 1/||r|| of the next unit, in flight
     for (int un; u < nunits; u = un) {
       const int b = u / g.units, ul = u % g.units;
@@ -507,10 +543,16 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const int o = c0 + q;
-            float x = __uint_as_float(uu[q]) + sbias[o];
-            if (FIRST) x = fmaf(sw1e[2 * o], rh, fmaf(sw1e[2 * o + 1], kf, x));
-            v[q] = a.use_gelu ? gelu_px(x) : x;
-            if (PROJ) pacc = fmaf(sdw[o], v[q], pacc);
+            v[q] = __uint_as_float(uu[q]) + sbias[o];
+            if (FIRST) v[q] = fmaf(sw1e[2 * o], rh, fmaf(sw1e[2 * o + 1], kf, v[q]));
+          }
+          if (use_gelu) {   // one uniform branch around 8 independent pairs
+#pragma unroll
+            for (int q = 0; q < 16; q += 2) gelu_px2(v[q], v[q + 1]);
+          }
+          if (PROJ) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) pacc = fmaf(sdw[c0 + q], v[q], pacc);
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {

@@ -341,13 +341,14 @@ __global__ void k_tr_adamw(size_t count, float* __restrict__ th, const float* __
   }
 }
 
-// Krylov training pair (Eq. 8-9): r = f - A u_i (given Au), e = u* - u_i.
-// Au may alias r (element-wise, read before write).
+// Krylov training pair (Eq. 8-9): r = f - A u_i (given Au), e = e_scale (u* - u_i)
+// (e_scale: the unit of the target, R27).  Au may alias r (element-wise, read before write).
 __global__ void k_tr_pair(const double* __restrict__ f, const double* Au, const double* __restrict__ ustar,
-                          const double* __restrict__ u, size_t count, double* r, double* __restrict__ e) {
+                          const double* __restrict__ u, size_t count, double e_scale, double* r,
+                          double* __restrict__ e) {
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < count; t += (size_t)gridDim.x * blockDim.x) {
     r[t] = __dsub_rn(f[t], Au[t]);
-    e[t] = __dsub_rn(ustar[t], u[t]);
+    e[t] = __dmul_rn(e_scale, __dsub_rn(ustar[t], u[t]));
   }
 }
 
@@ -423,8 +424,8 @@ cudaError_t launch_tr_adamw(size_t count, float* th, const float* g, float* m, f
   return cudaGetLastError();
 }
 cudaError_t launch_tr_pair(const double* f, const double* Au, const double* ustar, const double* u, size_t count,
-                           double* r, double* e, cudaStream_t s) {
-  k_tr_pair<<<ew_grid(count), 256, 0, s>>>(f, Au, ustar, u, count, r, e);
+                           double e_scale, double* r, double* e, cudaStream_t s) {
+  k_tr_pair<<<ew_grid(count), 256, 0, s>>>(f, Au, ustar, u, count, e_scale, r, e);
   ++launch_counter();
   return cudaGetLastError();
 }

@@ -100,7 +100,7 @@ EXPORTS = {
     "fcgno_adamw_step": (_i, [_sz, _vp, _vp, _vp, _vp, ctypes.c_int32, AdamWOpts, _vp]),
     "fcgno_train_epoch": (_i, [TrainDesc, ctypes.c_int32, _vp, _vp, _vp, _vp, _P(ctypes.c_int32), AdamWOpts, _vp,
                                _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
-    "fcgno_krylov_pair": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp]),
+    "fcgno_krylov_pair": (_i, [_vp, _vp, _vp, _vp, ctypes.c_double, _vp, _vp, _vp]),
     "fcgno_last_error": (ctypes.c_char_p, []),
     "fcgno_abi_version": (_i, []),
 }
@@ -402,13 +402,16 @@ def fcg_solve_stationary(problem: Problem, f: torch.Tensor, u0: torch.Tensor | N
 
 
 # ------------------------------------------------------------------ training
-def krylov_pair(problem: Problem, f: torch.Tensor, u_star: torch.Tensor, u: torch.Tensor, stream=None):
-    """Training pair of every system (Eq. 8-9; fcgno_krylov_pair): r = f - A u, e = u_star - u."""
+def krylov_pair(problem: Problem, f: torch.Tensor, u_star: torch.Tensor, u: torch.Tensor, e_scale: float = 1.0,
+                stream=None):
+    """Training pair of every system (Eq. 8-9; fcgno_krylov_pair): r = f - A u,
+    e = e_scale (u_star - u)."""
     for name, t in (("f", f), ("u_star", u_star), ("u", u)):
         _require(t, problem.shape, name)
     r = _on(stream, lambda: torch.empty_like(f))
     e = _on(stream, lambda: torch.empty_like(f))
-    _check(_lib.fcgno_krylov_pair(problem._h, _ptr(f), _ptr(u_star), _ptr(u), _ptr(r), _ptr(e), _stream(stream)))
+    _check(_lib.fcgno_krylov_pair(problem._h, _ptr(f), _ptr(u_star), _ptr(u), float(e_scale), _ptr(r), _ptr(e),
+                                  _stream(stream)))
     return r, e
 
 

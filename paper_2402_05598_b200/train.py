@@ -25,7 +25,7 @@ def lr_at_epoch(epoch: int, lr0: float = 1e-3, decay: float = 0.5, every: int = 
 
 
 def krylov_dataset(problem: fcgno.Problem, f: torch.Tensor, u0: torch.Tensor, sample_iters, m: int = 5,
-                   tol_exact: float = 1e-12, maxit_exact: int = 20000):
+                   tol_exact: float = 1e-12, maxit_exact: int = 20000, e_scale: float = 1.0):
     """Training pairs of every system of `problem` at the CG iterations `sample_iters` (Fig. 3 (a)-(b)).
     Returns (r, e, ksys): r, e [S][n][n] fp64 with S = len(sample_iters) * B (sample s belongs to system
     s % B), ksys [S] int32, and the per-system iteration count of the tight solve."""
@@ -34,7 +34,7 @@ def krylov_dataset(problem: fcgno.Problem, f: torch.Tensor, u0: torch.Tensor, sa
     rs, es = [], []
     for i in sample_iters:
         u_i = fcgno.fcg_solve(problem, f, u0, m=m, tol=0.0, maxit=int(i), history=False).u
-        r, e = fcgno.krylov_pair(problem, f, u_star, u_i)
+        r, e = fcgno.krylov_pair(problem, f, u_star, u_i, e_scale=e_scale)
         rs.append(r)
         es.append(e)
     B = problem.B

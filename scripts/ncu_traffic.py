@@ -37,7 +37,7 @@ def main():
     d["src_sha16"] = bench.src_hash()
     d["source"] = (f"ncu --set full --clock-control none, {len(per)} {kname} launches (layers 1-3 of one NO apply), "
                    "dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged")
-    d.setdefault(f"config{config}", {})["k_tc_layer"] = sum(per) / len(per)
+    d.setdefault(f"config{config}", {})["k_px_layer"] = sum(per) / len(per)
     d[f"config{config}"]["per_launch_bytes"] = per
     json.dump(d, open(path, "w"), indent=1)
     print(json.dumps(d, indent=1))

@@ -3,9 +3,13 @@ and evaluate FCG-NO on held-out systems against FCG(I) (the shape of the paper's
 
   python scripts/train_sno.py --config 1 --epochs 150 > profiles/r02/train_c1.json
 
-Data (synthetic, seeded; DESIGN.md R27): the BASELINE config's k field and N(0,1) right-hand sides;
-training residuals are CG iterates from u0 = 0 at log-spaced iterations (Eq. 8-9).  Every step runs
-in libfcgno.so (paper_2402_05598_b200/train.py sequences the calls)."""
+Data (synthetic, seeded; R27), --dataset:
+  diffusion  the paper's Diffusion set: a ~ P(5,5,2) + 10, f ~ P(5,5,2), u0 ~ N(0, I)
+  poisson    the paper's Poisson set: a = 1, f ~ P(5,5,2), u0 ~ N(0, I)
+  lognormal  the BASELINE config's k field (exp of a Gaussian random field) and N(0,1) f, u0 = 0
+Training residuals are CG iterates at the iterations --iters (Eq. 8-9); the target is the error in
+units of the unscaled stencil, e_scale = (n+1)^2 (R27; --e-scale 1 gives A^{-1} r as printed).  Every
+step runs in libfcgno.so (paper_2402_05598_b200/train.py sequences the calls)."""
 import argparse
 import json
 import os
@@ -44,25 +48,37 @@ def main():
     ap.add_argument("--tol", type=float, default=1e-6)
     ap.add_argument("--maxit", type=int, default=1000)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--dataset", choices=["diffusion", "poisson", "lognormal"], default="diffusion")
+    ap.add_argument("--e-scale", type=float, default=None, help="unit of the target (default (n+1)^2)")
+    ap.add_argument("--lr", type=float, default=1e-3)
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
     n, w, m = c["n"], args.width or c["width"], c["m"]
     batch = args.batch or c["batch"]
     torch.cuda.init()
 
-    def system_set(count, seed):
-        k = sy.lognormal_k(n, count, c["length"], c["variance"], seed)
-        f = sy.normal_field(n, count, seed + 1)
-        return k, f
+    e_scale = args.e_scale if args.e_scale is not None else float((n + 1) ** 2)
 
-    k_tr, f_tr = system_set(args.train_systems, 1000 + args.seed)
-    k_te, f_te = system_set(args.test_systems, 5000 + args.seed)
+    def system_set(count, seed):
+        if args.dataset == "lognormal":
+            k = sy.lognormal_k(n, count, c["length"], c["variance"], seed)
+            f = sy.normal_field(n, count, seed + 1)
+            u0 = np.zeros_like(f)
+        else:
+            k = (np.ones((count, n, n)) if args.dataset == "poisson"
+                 else sy.trig_poly(n, count, seed, offset=10.0, stream=0))
+            f = sy.trig_poly(n, count, seed)
+            u0 = sy.normal_field(n, count, seed + 2)
+        return k, f, u0
+
+    k_tr, f_tr, u0_tr = system_set(args.train_systems, 1000 + args.seed)
+    k_te, f_te, u0_te = system_set(args.test_systems, 5000 + args.seed)
     p_tr, p_te = fcgno.Problem(dev(k_tr)), fcgno.Problem(dev(k_te))
     t0 = time.time()
-    r, e, ksys, it_exact = ptr.krylov_dataset(p_tr, dev(f_tr), dev(np.zeros_like(f_tr)), args.iters, m=m)
+    r, e, ksys, it_exact = ptr.krylov_dataset(p_tr, dev(f_tr), dev(u0_tr), args.iters, m=m, e_scale=e_scale)
     torch.cuda.synchronize()
     t_data = time.time() - t0
-    rh, eh, ksh, _ = ptr.krylov_dataset(p_te, dev(f_te), dev(np.zeros_like(f_te)), args.iters, m=m)
+    rh, eh, ksh, _ = ptr.krylov_dataset(p_te, dev(f_te), dev(u0_te), args.iters, m=m, e_scale=e_scale)
     tr = fcgno.Trainer(n, w, batch, sy.no_weights(w, 7 + args.seed),
                        loss=fcgno.LOSS_NOTAY if args.loss == "notay" else fcgno.LOSS_L2)
     kte = dev(k_te)
@@ -75,7 +91,7 @@ def main():
         return float(torch.cat(ls).mean())
 
     def fcg_counts(no):
-        res = fcgno.fcg_solve(p_te, dev(f_te), m=m, tol=args.tol, maxit=args.maxit, no=no, history=False)
+        res = fcgno.fcg_solve(p_te, dev(f_te), dev(u0_te), m=m, tol=args.tol, maxit=args.maxit, no=no, history=False)
         it = res.iters.cpu().numpy()
         st = res.status.cpu().numpy()
         return dict(mean=float(it.mean()), min=int(it.min()), max=int(it.max()),
@@ -87,7 +103,7 @@ def main():
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     start.record()
-    curve = ptr.train(tr, dev(k_tr), r, e, ksys, epochs=args.epochs, seed=args.seed,
+    curve = ptr.train(tr, dev(k_tr), r, e, ksys, epochs=args.epochs, seed=args.seed, lr0=args.lr,
                       log=lambda ep, l: print(f"epoch {ep} loss {l:.4f}", file=sys.stderr) if ep % 10 == 0 else None)
     end.record()
     torch.cuda.synchronize()
@@ -97,7 +113,8 @@ def main():
     samples = int(r.shape[0])
     out = dict(
         what="SNO trained on the GPU (Fig. 3 scheme), FCG-NO on held-out systems vs FCG(I)",
-        config=args.config, n=n, width=w, m=m, tol=args.tol, maxit=args.maxit, loss=args.loss,
+        config=args.config, dataset=args.dataset, e_scale=e_scale, lr0=args.lr,
+        n=n, width=w, m=m, tol=args.tol, maxit=args.maxit, loss=args.loss,
         train_systems=args.train_systems, test_systems=args.test_systems, sample_iters=args.iters,
         samples=samples, batch=batch, epochs=args.epochs, steps=int(tr.t.value),
         table6=dict(lr0=1e-3, decay="x0.5 / 50 epochs", weight_decay=1e-2),
@@ -106,7 +123,7 @@ def main():
         loss_curve=[round(x, 5) for x in curve],
         before=before, after=after, fcg_identity=ident,
         exact_solve_iters_mean=float(it_exact.float().mean()),
-        data="synthetic (seeded lognormal k, N(0,1) f; CG residuals from u0 = 0)",
+        data="synthetic, seeded (see --dataset in the header)",
     )
     print(json.dumps(out))
 

@@ -37,7 +37,7 @@ def test_library_exports_every_declared_symbol(built):
 def test_binding_covers_every_declared_symbol(built):
     from paper_2402_05598_b200 import fcgno
     assert set(declared_functions()) <= set(fcgno.EXPORTS)
-    assert fcgno.abi_version() == 8
+    assert fcgno.abi_version() == 9
 
 
 def test_sizes_and_validation(built):
