@@ -65,11 +65,6 @@ __device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
   asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
   return r;
 }
-__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
-  uint64_t r;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-  return r;
-}
 // GELU(x) = x/2 (1 + erf(x / sqrt 2)) (reading R11) of two values, erf by Abramowitz & Stegun 7.1.26
 // (|error| <= 1.5e-7, two orders below the 3xBF16 operand rounding) through erfc: with h = x/2 and
 // pe = poly(t) exp(-x^2/2), t = 1/(1 + p|x|/sqrt 2),  GELU = h + |h| - |h| pe  (x >= 0: h (2 - pe);
@@ -95,16 +90,6 @@ __device__ __forceinline__ void gelu_px2(float& x0, float& x1) {
   x0 = fmaf(-fabsf(h0), pe0, h0 + fabsf(h0));
   x1 = fmaf(-fabsf(h1), pe1, h1 + fabsf(h1));
 }
-
-// bulk copy shared -> global (async proxy), completion tracked by bulk groups
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(tc::smem_u32(src)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 
 __device__ __forceinline__ void st_split8(unsigned char* hi, unsigned char* lo, const float* v) {
   uint4 h, l;
@@ -212,7 +197,7 @@ __global__ void __launch_bounds__(256) k_px_prep(const PxPrepArgs a) {
 // ------------------------------------------------------------------ k_px_layer
 // Diagnostics (FCGNO_PX_TRACE=<layer 1..3>): clock64 stamps of the pipeline events of CTA 0's first
 // kPxTraceTiles tiles, read back with fcgno_debug_px_trace (scripts/px_trace.py).
-constexpr int kPxTraceTiles = 64, kPxTraceEv = 10;
+constexpr int kPxTraceTiles = 64, kPxTraceEv = 34;   // 10 pipeline events + (start, done) of the 12 epilogue-1 warps
 __device__ unsigned long long g_px_trace[kPxTraceTiles * kPxTraceEv];
 #define PX_TRACE(t, ev)                                                                  \
   do {                                                                                   \
@@ -413,7 +398,7 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
     }
   } else if (warp == 1) {
     // ================= D1 MMAs (one thread): bypass + x-synthesis
-    if (lane == 0) {
+    if (tc::elect_one()) {
       tc::mbar_wait(cstb, 0);
       const uint32_t id1 = tc::make_idesc_bf16(128, NP, false, false);   // V (K-major) . W (K-major)
       const uint32_t id2 = tc::make_idesc_bf16(128, NP, false, true);    // F (K-major) . G (MN-major)
@@ -462,7 +447,7 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
     }
   } else if (warp == 3) {
     // ================= x-analysis MMAs (one thread): D2[o][k'] += sum_p v'[p][o] F[p][k']
-    if (lane == 0) {
+    if (tc::elect_one()) {
       tc::mbar_wait(cstb, 0);
       const uint32_t id3 = tc::make_idesc_bf16(128, 48, true, true);     // v'^T (MN-major) . F (MN-major)
       int t = 0, ui = 0;
@@ -471,7 +456,9 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
         for (int cb = 0; cb < g.CB; ++cb, ++t) {
           const int s = t % NST;
           tc::mbar_wait(&vfull[s], (uint32_t)(t / NST) & 1u);
+          PX_TRACE(t, 8);
           if (cb == 0) tc::mbar_wait(&d2empty[b2], ((uint32_t)(ui >> 1) & 1u) ^ 1u);
+          PX_TRACE(t, 9);
           tc::fence_after_sync();
           const uint32_t sth = sth0 + (uint32_t)s * L.stage_bytes, stl = sth + sh;
           const uint32_t d2 = tmem + 2u * NP + (uint32_t)b2 * g.D2W;
@@ -524,6 +511,7 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
         if (lane == 0 && q4 == 0 && eg == 0) PX_TRACE(t, 6);
         tc::mbar_wait(&d1full[d], (uint32_t)(t >> 1) & 1u);
         if (lane == 0 && q4 == 0 && eg == 0) PX_TRACE(t, 3);
+        if (lane == 0) PX_TRACE(t, 10 + 2 * (warp - kPxE1First));
         tc::fence_after_sync();
         if (FIRST) {   // the lift's 2-channel bypass W1 (E [r/||r||, k] + bE) on the CUDA cores
           tc::mbar_wait(&full[s], (uint32_t)(t / NST) & 1u);
@@ -574,7 +562,8 @@ __global__ void __launch_bounds__(kPxThreads, 1) k_px_layer(const PxLayerArgs a,
         tc::mbar_arrive(&d1empty[d]);
         tc::fence_proxy_async_smem();
         tc::mbar_arrive(&vfull[s]);
-        if (lane == 0 && q4 == 0) PX_TRACE(t, eg == 0 ? 4 : (eg == 1 ? 9 : 8));
+        if (lane == 0 && q4 == 0 && eg == 0) PX_TRACE(t, 4);
+        if (lane == 0) PX_TRACE(t, 11 + 2 * (warp - kPxE1First));
         if (PROJ) {   // sum_o (D W4)[o] v3[o]: the groups' partials added in a fixed order
           pj[((size_t)d * kPxE1Groups + eg) * 128 + p] = pacc;
           tc::named_sync(1, 32u * kPxE1Warps);
@@ -734,7 +723,7 @@ __global__ void __launch_bounds__(kYsynThreads, 1) k_px_ysyn(const float2* __res
     }
   } else if (warp == kYsynBuild) {
     // ================= MMA issuer
-    if (lane == 0) {
+    if (tc::elect_one()) {
       tc::mbar_wait(abar, 0);
       const uint32_t id = tc::make_idesc_bf16(128, N2, false, false);
       const uint32_t base = tc::smem_u32(sm);
@@ -901,7 +890,7 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
       tc::fence_before_sync();
       __syncthreads();
       tc::fence_after_sync();
-      if (tid == 0) {
+      if (warp == 0 && tc::elect_one()) {
         const uint32_t aah = base + L.A + (c & 1u) * 2u * a_half, aal = aah + a_half;
         const uint32_t bh = base + L.Bf, bl = bh + C.fy_half;
         for (int ks = 0; ks < kYanKC / 16; ++ks)
@@ -1038,7 +1027,7 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
     tc::fence_proxy_async_smem();
     tc::fence_before_sync();
     __syncthreads();
-    if (tid == 0) {
+    if (warp == 0 && tc::elect_one()) {
       tc::mbar_wait(&bar[0], ph);
       tc::fence_after_sync();
       uint32_t acc = 0;

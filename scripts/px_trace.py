@@ -28,15 +28,20 @@ r = torch.from_numpy(f).cuda()
 for _ in range(3):
     no.apply(prob, r)
 torch.cuda.synchronize()
-buf = np.zeros(640, dtype=np.uint64)
-F._check(F._lib.fcgno_debug_px_trace(buf.ctypes.data_as(ctypes.c_void_p), 640))
-t = buf.reshape(64, 10).astype(np.float64)
+EV = 34
+buf = np.zeros(64 * EV, dtype=np.uint64)
+F._check(F._lib.fcgno_debug_px_trace(buf.ctypes.data_as(ctypes.c_void_p), 64 * EV))
+full = buf.reshape(64, EV).astype(np.float64)
+t = full[:, :10]
 t0 = t[0, 0]
 mhz = 1965.0
-names = ["ld_issue", "mma_full", "d1_commit", "e1_start", "e1g0_done", "mma3", "e1_pre", "e2_done", "e1g2_done",
-         "e1g1_done"]
+names = ["ld_issue", "mma_full", "d1_commit", "e1_start", "e1g0_done", "mma3", "e1_pre", "e2_done", "xa_vfull",
+         "xa_d2empty"]
 print("tile " + " ".join(f"{n:>10s}" for n in names))
 for i in range(24):
     print(f"{i:4d} " + " ".join(f"{(v - t0) / mhz:10.2f}" if v else f"{'-':>10s}" for v in t[i]))
+print("epilogue-1 warps (warp 4 + w): start / done per tile, us")
+for i in range(16, 24):
+    print(f"{i:4d} " + " ".join(f"{(full[i, 10 + 2 * w] - t0) / mhz:6.2f}/{(full[i, 11 + 2 * w] - t0) / mhz:6.2f}" for w in range(12)))
 d = np.diff(t[4:40, 2]) / mhz
 print("per-tile period (d1_commit), us: median", float(np.median(d)))
