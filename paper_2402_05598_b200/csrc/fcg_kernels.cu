@@ -370,27 +370,35 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   pdl_wait();
   pdl_trigger();
   ST_SMEM;
-  __shared__ dd sm[16];
+  __shared__ dd sm[2 * (kStThreads / 32)];
   __shared__ double sbeta[kMmax];
   __shared__ const V* sptr[kMmax];
   const int b = blockIdx.y;
-  if (d.status[b] != SYS_RUNNING) return;
+  const int n = d.n;
+  const size_t N = (size_t)d.N;
+  const StGeo g = st_geo(n);
+  st_copy<PAIRS>(g, n, d.k + b * N, sk);   // independent of the iteration state: in flight first
+  if (d.status[b] != SYS_RUNNING) {
+    cp_async_wait_all();
+    return;
+  }
   const int i = *d.iter;
   const int mi = m_schedule(i, d.m, d.schedule);
-  const int n = d.n, slot = ring_slot(i, d.m);
-  const size_t N = (size_t)d.N;
+  const int slot = ring_slot(i, d.m);
   for (int q = threadIdx.x; q < mi; q += blockDim.x) {
     sbeta[q] = d.beta[(size_t)b * kMmax + q];
     sptr[q] = reinterpret_cast<const V*>(d.ring_p) + ((size_t)ring_slot(i - mi + q, d.m) * d.B + b) * N;
   }
   __syncthreads();
-  const StGeo g = st_geo(n);
   V* pout = reinterpret_cast<V*>(d.ring_p) + ((size_t)slot * d.B + b) * N;
   const V* wb = reinterpret_cast<const V*>(d.w) + b * N;
   const bool fast = d.kfast != 0;
-  st_copy<PAIRS>(g, n, d.k + b * N, sk);
-  const int bad = st_pform<PAIRS, V>(g, n, wb, sptr, sbeta, mi, sx, pout);
-  st_fill_end();
+  // lazy x update of the previous iteration, u += alpha_{i-1} p_{i-1}, inside
+  // the p-form's first batch of loads (p_{i-1} is the newest window vector): the same single rounding
+  // as in k_update's place, one sweep of u fewer.  alpha[b] still holds alpha_{i-1}: this launch's
+  // last CTA overwrites it only after every CTA has passed here.
+  const int bad = st_pform<PAIRS, V>(g, n, wb, sptr, sbeta, mi, sx, pout, d.u + b * N, i > 0 ? d.alpha[b] : 0.0, i > 0);
+  cp_async_wait_all();
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(d.flags + b, FLAG_NONFINITE);
   const StWalk<RG> w(g);
   double rx[RG];
@@ -404,49 +412,66 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
     dot2_acc(p, q, s0, c0);
     dot2_acc(p, rv, s1, c1);
   });
-  if (i > 0) {
-    // lazy x update of the previous iteration, u += alpha_{i-1} p_{i-1}:
-    // the same single rounding as in k_update's place, one sweep of u fewer.  alpha[b] still holds
-    // alpha_{i-1}: this launch's last CTA overwrites it only after every CTA has passed here.
-    const V* pprev = sptr[mi - 1];        // newest window vector = p_{i-1}
-    double* ub = d.u + b * N;
-    const double al = d.alpha[b];
-    double uv[RG], pv[RG];
-#pragma unroll
-    for (int s = 0; s < RG; ++s) {
-      const int e = (g.i0 + w.r0 + s) * n + g.j0 + w.c;
-      const bool ok = w.valid(g, s);
-      uv[s] = ok ? ub[e] : 0.0;
-      pv[s] = ok ? (double)__ldg(pprev + e) : 0.0;
-    }
-#pragma unroll
-    for (int s = 0; s < RG; ++s)
-      if (w.valid(g, s)) ub[(g.i0 + w.r0 + s) * n + g.j0 + w.c] = __dadd_rn(uv[s], __dmul_rn(al, pv[s]));
-  }
+  // (p,s), (p,r): warp sums, then warp 0 alone finishes (the other warps retire: no block-wide wait on
+  // the arrival's fence + atomic round trip)
   dd v[2] = {dot2_finish(s0, c0), dot2_finish(s1, c1)};
-  block_reduce_dd<2>(v, sm);
-  if (threadIdx.x == 0) {
-    d.part_step[((size_t)b * d.nblk + blockIdx.x) * 2 + 0] = v[0];
-    d.part_step[((size_t)b * d.nblk + blockIdx.x) * 2 + 1] = v[1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    v[0] = dd_add(v[0], shfl_down_dd(v[0], off));
+    v[1] = dd_add(v[1], shfl_down_dd(v[1], off));
   }
+  if (lane == 0) {
+    sm[warp * 2 + 0] = v[0];
+    sm[warp * 2 + 1] = v[1];
+  }
+  __syncthreads();
+  if (warp != 0) return;
   const int nb = gridDim.x;
-  if (arrive_last(d.cnt + d.B + b, nb)) {
-    dd gsum, psum;
-    if (nb <= kSerialPartials) {
-      if (threadIdx.x == 0) {
-        gsum = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, nb, 2);
-        psum = serial_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, nb, 2);
-      }
-    } else {
-      gsum = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 0, nb, 2, sm);
-      psum = block_reduce_partials(d.part_step + (size_t)b * d.nblk * 2 + 1, nb, 2, sm);
+  int last = 0;
+  if (lane == 0) {
+    dd a0 = sm[0], a1 = sm[1];
+    for (int q = 1; q < kStThreads / 32; ++q) {   // fixed order over the warps
+      a0 = dd_add(a0, sm[q * 2 + 0]);
+      a1 = dd_add(a1, sm[q * 2 + 1]);
     }
-    if (threadIdx.x == 0) {
-      const double gamma = dd_round(gsum);
-      d.gamma[(size_t)slot * d.B + b] = gamma;
-      if (!(gamma > 0.0) || !isfinite(gamma)) atomicOr(d.flags + b, FLAG_BREAKDOWN);
-      d.alpha[b] = __ddiv_rn(dd_round(psum), gamma);
+    d.part_step[((size_t)b * d.nblk + blockIdx.x) * 2 + 0] = a0;
+    d.part_step[((size_t)b * d.nblk + blockIdx.x) * 2 + 1] = a1;
+    __threadfence();
+    unsigned* counter = d.cnt + d.B + b;
+    const unsigned prev = atomicAdd(counter, 1u);
+    last = prev == (unsigned)(nb - 1);
+    if (last) *counter = 0u;   // every CTA of this launch has arrived; safe to re-arm
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  // the system's last CTA: gamma = (p,s), alpha = (p,r)/gamma, breakdown flag
+  dd gsum = {0.0, 0.0}, psum = {0.0, 0.0};
+  const dd* part = d.part_step + (size_t)b * d.nblk * 2;
+  if (nb <= kSerialPartials) {
+    if (lane == 0) {
+      gsum = serial_partials(part + 0, nb, 2);
+      psum = serial_partials(part + 1, nb, 2);
     }
+  } else {   // lanes stride over the CTAs' partials, then a shuffle tree (fixed order)
+    for (int t = lane; t < nb; t += 32) {
+      const double2 ga = __ldcg(reinterpret_cast<const double2*>(part + (size_t)t * 2 + 0));
+      const double2 pa = __ldcg(reinterpret_cast<const double2*>(part + (size_t)t * 2 + 1));
+      gsum = dd_add(gsum, dd{ga.x, ga.y});
+      psum = dd_add(psum, dd{pa.x, pa.y});
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      gsum = dd_add(gsum, shfl_down_dd(gsum, off));
+      psum = dd_add(psum, shfl_down_dd(psum, off));
+    }
+  }
+  if (lane == 0) {
+    const double gamma = dd_round(gsum);
+    d.gamma[(size_t)slot * d.B + b] = gamma;
+    if (!(gamma > 0.0) || !isfinite(gamma)) atomicOr(d.flags + b, FLAG_BREAKDOWN);
+    d.alpha[b] = __ddiv_rn(dd_round(psum), gamma);
   }
 }
 
