@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libfcgno.so")
-SOURCES = ["api.cu", "fcg_kernels.cu", "no_kernels.cu", "no_px_kernels.cu", "diag_kernels.cu", "train_kernels.cu"]
+SOURCES = ["api.cu", "fcg_kernels.cu", "no_kernels.cu", "no_px_kernels.cu", "diag_kernels.cu", "train_kernels.cu",
+           "fcg_small.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

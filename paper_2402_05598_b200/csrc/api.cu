@@ -916,6 +916,17 @@ int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* pack
   }
   fcgno_grid g{p->n, p->B};
   if (!aligned(ws) || ws_bytes < solve_ws_bytes(g, nd, o, dg != nullptr, sta != nullptr)) return fail(FCGNO_EWORKSPACE, "fcg_solve: workspace");
+  if (!nd && !sta && !dg && !o.vec_fp32 && !o.profile_mask && fcg_small_applies(p->n, o.m)) {
+    // small systems, identity preconditioner: the whole solve in one persistent kernel (fcg_small.cu), one
+    // CTA per system, on the caller's stream; same arithmetic as the launch-per-step path below
+    FcgDev d{};
+    d.n = p->n; d.B = p->B; d.N = p->n * p->n;
+    d.m = o.m; d.maxit = o.maxit; d.schedule = o.schedule; d.tol = o.tol;
+    d.scale = double(p->n + 1) * double(p->n + 1);
+    d.k = p->k; d.f = f; d.u = u; d.status = status; d.iters = iters; d.hist = history;
+    CK(launch_fcg_small(d, static_cast<cudaStream_t>(stream)));
+    return FCGNO_OK;
+  }
   if (nd) {
     if (nd->precision == FCGNO_FP64) CK(prepare_no_kernels<double>());
     else { CK(prepare_no_kernels<float>()); CK(prepare_px_kernels()); }

@@ -202,6 +202,10 @@ cudaError_t launch_tr_pair(const double* f, const double* Au, const double* usta
 
 uint64_t& launch_counter();
 
+// Persistent single-kernel solve of small identity-preconditioned systems (fcg_small.cu).
+bool fcg_small_applies(int n, int m);
+cudaError_t launch_fcg_small(const FcgDev& d, cudaStream_t s);
+
 // Theorem-1 / Notay diagnostics (diag_kernels.cu)
 cudaError_t launch_notay_form(const double* w, const double* e, const double* c, double* d, int n, int B, cudaStream_t s);
 cudaError_t launch_notay_coef(const double* wAe, const double* wAw, double* c, int B, cudaStream_t s);

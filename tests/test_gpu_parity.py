@@ -536,6 +536,43 @@ def test_opt_in_paths_match_default(lib):
     assert np.array_equal(u0, u1) and np.array_equal(h0, h1, equal_nan=True)
 
 
+def _identity_in_subprocess(env_extra, tag, n, B, m, maxit, schedule=0):
+    """fp64 identity FCG solve of a small lognormal system in a fresh process (env flags are read once per
+    process); returns (u, history, iters, status)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import sys,numpy as np,torch; sys.path.insert(0,'.'); import synthetic as sy;"
+            "from paper_2402_05598_b200 import fcgno as F;"
+            f"k=sy.lognormal_k({n},{B},0.1,1.0,31); f=sy.normal_field({n},{B},32); u0=sy.normal_field({n},{B},33);"
+            "f[-1]=0.0; u0[-1]=0.0;"   # the last system has r0 = 0
+            "p=F.Problem(torch.from_numpy(k).cuda());"
+            f"res=F.fcg_solve(p, torch.from_numpy(f).cuda(), torch.from_numpy(u0).cuda(), m={m}, tol=1e-9, maxit={maxit},"
+            f" schedule={schedule});"
+            "np.savez(sys.argv[1], u=res.u.cpu().numpy(), h=res.history.cpu().numpy(), it=res.iters.cpu().numpy(),"
+            " st=res.status.cpu().numpy())")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    path = f"/tmp/fcgno_small_{tag}.npz"
+    subprocess.run([sys.executable, "-c", code, path], cwd=root, env=dict(os.environ, **env_extra), check=True)
+    z = np.load(path)
+    return z["u"], z["h"], z["it"], z["st"]
+
+
+@pytest.mark.parametrize("n,B,m,maxit,schedule", [(32, 3, 5, 500, 0), (32, 2, 10, 60, 1), (19, 4, 7, 25, 0), (8, 2, 64, 200, 1)])
+def test_persistent_small_solve_matches_launch_per_step_path(lib, n, B, m, maxit, schedule):
+    """The single-kernel solve of small identity systems (fcg_small.cu) against the general
+    path (FCGNO_PERSISTENT=0) on the same inputs: iterates, histories, counts and statuses bitwise, with
+    converging, maxit-capped and r0 = 0 systems in the batch."""
+    a = _identity_in_subprocess({}, "on", n, B, m, maxit, schedule)
+    b = _identity_in_subprocess({"FCGNO_PERSISTENT": "0"}, "off", n, B, m, maxit, schedule)
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[3], b[3]), (a[2], b[2], a[3], b[3])
+    assert a[2][-1] == 0 and a[3][-1] == lib.CONVERGED
+    for s in range(B):
+        it = int(a[2][s])
+        assert np.array_equal(a[1][s, :it + 1], b[1][s, :it + 1]), s
+        assert np.array_equal(a[0][s], b[0][s]), s
+
+
 # ----------------------------------------------------------------------------- Notay ratio (NEXT-2)
 @pytest.mark.parametrize("kind", ["identity", "no64", "no32"])
 def test_notay_ratio_matches_oracle(lib, kind):
