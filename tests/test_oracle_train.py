@@ -161,3 +161,28 @@ def test_krylov_samples_lie_in_the_krylov_subspace():
                 assert np.linalg.norm(ri - Qs @ (Qs.T @ ri)) > 1e-6 * np.linalg.norm(ri)
         assert np.max(np.abs(Ad @ es[s].ravel() - ri)) < 1e-9 * np.max(np.abs(f))
     assert np.array_equal(rs[0], f - orc.apply_A(k, u0))
+
+
+def test_krylov_target_unit_and_scale_invariance_of_fcg():
+    """R27: e_scale only rescales the target (A e_i = e_scale r_i), and FCG is invariant to a positive
+    scaling of the preconditioner (alpha is a line search), which is why weights trained against
+    the scaled target precondition as they are."""
+    n = 6
+    k = sy.lognormal_k(n, 1, 0.2, 1.0, 3)[0]
+    f = sy.normal_field(n, 1, 3)[0]
+    u0 = np.zeros((n, n))
+    Ad = orc.dense_A(k)
+    c = float((n + 1) ** 2)
+    r1, e1, ue = otr.krylov_samples(k, f, u0, [0, 2], m_max=5, tol_exact=1e-14, maxit_exact=500)
+    rc, ec, _ = otr.krylov_samples(k, f, u0, [0, 2], m_max=5, u_exact=ue, e_scale=c)
+    assert np.array_equal(r1, rc) and np.array_equal(ec, c * e1)
+    assert np.max(np.abs(Ad @ ec[1].ravel() - c * r1[1].ravel())) < 1e-9 * c * np.max(np.abs(f))
+    A = lambda x: orc.apply_A(k, x)
+    Minv = np.linalg.inv(Ad + 3.0 * np.diag(np.diag(Ad)))      # some SPD preconditioner
+    B1 = lambda r: (Minv @ r.ravel()).reshape(n, n)
+    Bc = lambda r: c * B1(r)
+    o1 = orc.fcg(A, f, u0, 5, 1e-10, 200, precond=B1)
+    oc = orc.fcg(A, f, u0, 5, 1e-10, 200, precond=Bc)
+    assert o1["iters"] == oc["iters"]
+    assert np.max(np.abs(o1["u"] - oc["u"])) <= 1e-12 * np.max(np.abs(o1["u"]))
+    assert np.allclose(o1["hist"], oc["hist"], rtol=1e-9, atol=0)
