@@ -86,15 +86,39 @@ __global__ void __launch_bounds__(256) k_dft_rows(const double* __restrict__ x, 
   const double* xb = x + (size_t)b * N + (size_t)i0 * n;
   for (int t = threadIdx.x; t < rows * n; t += blockDim.x) X[t] = (T)(xb[t] * inv);
   __syncthreads();
-  for (int e = threadIdx.x; e < rows * kModes; e += blockDim.x) {
-    const int r = e / kModes, k2 = e - r * kModes;
-    T ar = 0, ai = 0;
-    for (int j = 0; j < n; ++j) {
-      const T v = X[r * n + j];
-      const T2 f = __ldg(F + j * kModes + k2);
-      ar += v * f.x; ai += v * f.y;
+  // x-direction: thread = (column slice js, mode k2); a twiddle is loaded once for every row of the group,
+  // and a slice's chain is n / kDftSlices steps long; the slices' partial sums are added in a fixed order
+  {
+    constexpr int kDftSlices = 12;                                   // 12 x 20 modes = 240 of the 256 threads
+    T2* Tp = reinterpret_cast<T2*>(Tx + DR * kModes);                // [kDftSlices][DR][20]
+    const int js = threadIdx.x / kModes, k2 = threadIdx.x - js * kModes;
+    if (js < kDftSlices) {
+      const int per = (n + kDftSlices - 1) / kDftSlices, j0 = js * per, j1 = min(n, j0 + per);
+      T ar[8], ai[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) { ar[r] = 0; ai[r] = 0; }
+      for (int j = j0; j < j1; ++j) {
+        const T2 f = __ldg(F + j * kModes + k2);
+#pragma unroll
+        for (int r = 0; r < 8; ++r)
+          if (r < rows) {
+            const T v = X[r * n + j];
+            ar[r] += v * f.x; ai[r] += v * f.y;
+          }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < rows) Tp[(js * DR + r) * kModes + k2] = T2{ar[r], ai[r]};
     }
-    Tx[e] = T2{ar, ai};
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * kModes; e += blockDim.x) {
+      T sr = 0, si = 0;
+      for (int q = 0; q < kDftSlices; ++q) {
+        const T2 v = Tp[q * DR * kModes + e];
+        sr += v.x; si += v.y;
+      }
+      Tx[e] = T2{sr, si};
+    }
   }
   __syncthreads();
   for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
@@ -127,8 +151,8 @@ __global__ void k_reduce_groups(const typename Cplx<T>::type* __restrict__ part,
   }
 }
 
-static size_t dft_smem(int n, size_t tsz) {
-  return ((size_t)((dft_rows(n) * n + 3) & ~3)) * tsz + (size_t)dft_rows(n) * kModes * 2 * tsz;
+static size_t dft_smem(int n, size_t tsz) {   // X [DR][n], Tx [DR][20] complex, slice partials [12][DR][20] complex
+  return ((size_t)((dft_rows(n) * n + 3) & ~3)) * tsz + (size_t)13 * dft_rows(n) * kModes * 2 * tsz;
 }
 
 template <typename T>
@@ -144,7 +168,12 @@ template cudaError_t launch_khat<float>(const double*, const float*, float*, flo
 template cudaError_t launch_khat<double>(const double*, const double*, double*, double*, int, int, int, cudaStream_t);
 
 // ------------------------------------------------------------------ layer-1 mixing with the lift folded in
-constexpr int kLiftCh = 4;      // output channels per CTA of k_lift_mix
+// Output channels per CTA of k_lift_mix: every CTA of a system repeats the sum over the input DFT's row
+// groups, so the channel chunk grows with the batch once the grid exceeds about eight CTAs per SM.
+static int lift_channels(int w, int B) {
+  const int ch = (w * B + 8 * 148 - 1) / (8 * 148);
+  return ch < 4 ? 4 : (ch > w ? w : ch);
+}
 template <typename T>
 __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* __restrict__ rpart, int ngroups,
                                                   const typename Cplx<T>::type* __restrict__ khat,
@@ -152,11 +181,11 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
                                                   const typename Cplx<T>::type* __restrict__ A1,
                                                   const typename Cplx<T>::type* __restrict__ A2,
                                                   typename Cplx<T>::type* __restrict__ ghat, int w, T n2, T inv_n2,
-                                                  const int* __restrict__ status, int mode_major, int k0) {
+                                                  const int* __restrict__ status, int mode_major, int k0, int och) {
   pdl_wait();
   pdl_trigger();
   using T2 = typename Cplx<T>::type;
-  const int b = blockIdx.x, ochunk = blockIdx.y;   // kLiftCh output channels per CTA
+  const int b = blockIdx.x, ochunk = blockIdx.y;   // och output channels per CTA
   if (status && status[b] != SYS_RUNNING) return;
   __shared__ T2 Rh[kModes2];
   for (int e = threadIdx.x; e < kModes2; e += blockDim.x) {
@@ -179,7 +208,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
   // k0: the mode of a constant field (the lift's bias bE transforms to n^2 at k0 only)
   // element e -> (o, kappa): kappa fastest for the [B][w][400] layout (FFMA path), o fastest for the
   // mode-major [400][B][w] layout of the tensor-core path, so the stores stay contiguous
-  const int olo = ochunk * kLiftCh, ohi = min(w, olo + kLiftCh), no_ = ohi - olo, cnt = no_ * kModes2;
+  const int olo = ochunk * och, ohi = min(w, olo + och), no_ = ohi - olo, cnt = no_ * kModes2;
   auto decode = [&](int e, int& o, int& kk) {
     if (mode_major) { kk = e / no_; o = olo + (e - kk * no_); }
     else { o = olo + e / kModes2; kk = e % kModes2; }
@@ -782,10 +811,11 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
            reinterpret_cast<T2*>(no.rpart), n, no.ngroups, status, no.rinv);
   ++launches;
   // 2. layer-1 mixing with the lift folded in
-  launch_k(k_lift_mix<T>, dim3(B, (w + kLiftCh - 1) / kLiftCh), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
+  const int och = lift_channels(w, B);
+  launch_k(k_lift_mix<T>, dim3(B, (w + och - 1) / och), dim3(256), 0, s, reinterpret_cast<const T2*>(no.rpart), no.ngroups,
            reinterpret_cast<const T2*>(no.khat), reinterpret_cast<const T2*>(pk + no.L.A0),
            reinterpret_cast<const T2*>(pk + no.L.A1), reinterpret_cast<const T2*>(pk + no.L.A2), ghat, w, n2, inv_n2,
-           status, (int)tc_layout_modes(no), no.k0);
+           status, (int)tc_layout_modes(no), no.k0, och);
   pe(PROF_NO_INPUT);
   ++launches;
   // 3. layers 1..3, each followed by the mixing of the next layer
