@@ -158,6 +158,14 @@ static size_t dft_smem(int n, size_t tsz) {   // X [DR][n], Tx [DR][20] complex,
 template <typename T>
 cudaError_t launch_khat(const double* k, const T* F, T* part, T* khat, int n, int B, int ngroups, cudaStream_t s) {
   using T2 = typename Cplx<T>::type;
+  static bool attr = false;   // assemble runs before any NO call; sized for the largest NO grid (n = 512): the
+                              // slice partials exceed 48 KB at n >= 256 in fp64
+  if (!attr) {
+    const cudaError_t e = cudaFuncSetAttribute((const void*)k_dft_rows<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)dft_smem(512, sizeof(T)));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
   k_dft_rows<T, false><<<dim3(ngroups, B), 256, dft_smem(n, sizeof(T)), s>>>(
       k, nullptr, reinterpret_cast<const T2*>(F), reinterpret_cast<T2*>(part), n, ngroups, nullptr, nullptr);
   k_reduce_groups<T><<<B, 256, 0, s>>>(reinterpret_cast<const T2*>(part), reinterpret_cast<T2*>(khat), ngroups);
