@@ -414,17 +414,10 @@ __global__ void __launch_bounds__(kStThreads, 3) k_pform_stencil(FcgDev d) {
   });
   // (p,s), (p,r): warp sums, then warp 0 alone finishes (the other warps retire: no block-wide wait on
   // the arrival's fence + atomic round trip)
-  dd v[2] = {dot2_finish(s0, c0), dot2_finish(s1, c1)};
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    v[0] = dd_add(v[0], shfl_down_dd(v[0], off));
-    v[1] = dd_add(v[1], shfl_down_dd(v[1], off));
-  }
-  if (lane == 0) {
-    sm[warp * 2 + 0] = v[0];
-    sm[warp * 2 + 1] = v[1];
-  }
+  const dd vs = warp_sum2_dd(dot2_finish(s0, c0), dot2_finish(s1, c1), lane);   // lane 0: (p,s), lane 16: (p,r)
+  if (lane == 0) sm[warp * 2 + 0] = vs;
+  if (lane == 16) sm[warp * 2 + 1] = vs;
   __syncthreads();
   if (warp != 0) return;
   const int nb = gridDim.x;
