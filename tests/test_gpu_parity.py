@@ -536,7 +536,7 @@ def test_opt_in_paths_match_default(lib):
     assert np.array_equal(u0, u1) and np.array_equal(h0, h1, equal_nan=True)
 
 
-def _identity_in_subprocess(env_extra, tag, n, B, m, maxit, schedule=0):
+def _identity_in_subprocess(env_extra, tag, n, B, m, maxit, schedule=0, nan_first=False):
     """fp64 identity FCG solve of a small lognormal system in a fresh process (env flags are read once per
     process); returns (u, history, iters, status)."""
     import os
@@ -546,6 +546,7 @@ def _identity_in_subprocess(env_extra, tag, n, B, m, maxit, schedule=0):
             "from paper_2402_05598_b200 import fcgno as F;"
             f"k=sy.lognormal_k({n},{B},0.1,1.0,31); f=sy.normal_field({n},{B},32); u0=sy.normal_field({n},{B},33);"
             "f[-1]=0.0; u0[-1]=0.0;"   # the last system has r0 = 0
+            f"f[0,0,0]=float('nan') if {int(nan_first)} else f[0,0,0];"   # optionally a non-finite system (R14)
             "p=F.Problem(torch.from_numpy(k).cuda());"
             f"res=F.fcg_solve(p, torch.from_numpy(f).cuda(), torch.from_numpy(u0).cuda(), m={m}, tol=1e-9, maxit={maxit},"
             f" schedule={schedule});"
@@ -571,6 +572,16 @@ def test_persistent_small_solve_matches_launch_per_step_path(lib, n, B, m, maxit
         it = int(a[2][s])
         assert np.array_equal(a[1][s, :it + 1], b[1][s, :it + 1]), s
         assert np.array_equal(a[0][s], b[0][s]), s
+
+
+def test_persistent_small_solve_nonfinite_system(lib):
+    """A system whose right-hand side holds a NaN is reported NONFINITE at iteration 0 by both paths
+    (R14), its iterate untouched, and does not disturb the other systems of the batch."""
+    a = _identity_in_subprocess({}, "on_nan", 16, 3, 5, 300, 0, nan_first=True)
+    b = _identity_in_subprocess({"FCGNO_PERSISTENT": "0"}, "off_nan", 16, 3, 5, 300, 0, nan_first=True)
+    assert a[3][0] == lib.NONFINITE == b[3][0] and a[2][0] == 0 == b[2][0]
+    assert a[3][1] == lib.CONVERGED == b[3][1] and a[2][1] == b[2][1]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1][1, :a[2][1] + 1], b[1][1, :b[2][1] + 1])
 
 
 # ----------------------------------------------------------------------------- Notay ratio (NEXT-2)
