@@ -103,6 +103,19 @@ __device__ __forceinline__ void store_split8(unsigned char* hi, unsigned char* l
 }
 using tc::tmem_ld8;
 
+// 256-bit read-only global load (sm_100: LDG.256), 32-byte aligned
+__device__ __forceinline__ void ld_global_256(const float* p, float4& a, float4& b) {
+  asm volatile("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+               : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+               : "l"(p));
+}
+// 256-bit global store (sm_100: STG.256), 32-byte aligned
+__device__ __forceinline__ void st_global_256(void* p, const uint4& a, const uint4& b) {
+  asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w),
+               "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+               : "memory");
+}
+
 __host__ __device__ inline uint32_t pow2_cols(uint32_t c) { return c <= 32 ? 32u : c <= 64 ? 64u : c <= 128 ? 128u : c <= 256 ? 256u : 512u; }
 
 }  // namespace
@@ -784,10 +797,9 @@ __global__ void __launch_bounds__(kYsynThreads, 1) k_px_ysyn(const float2* __res
               uint4 hr, lr, hi, li;
               tc::split8(vr, hr, lr);
               tc::split8(vi, hi, li);
-              uint4* dh = reinterpret_cast<uint4*>(Gb + g.g_off(b, 0, kgi, og, pair, i));
-              uint4* dl = reinterpret_cast<uint4*>(Gb + g.g_off(b, 1, kgi, og, pair, i));
-              dh[0] = hr; dh[1] = hi;
-              dl[0] = lr; dl[1] = li;
+              // one 32-byte store per (row, o-group) piece: a warp writes 1 KB contiguous per instruction
+              st_global_256(Gb + g.g_off(b, 0, kgi, og, pair, i), hr, hi);
+              st_global_256(Gb + g.g_off(b, 1, kgi, og, pair, i), lr, li);
             }
           }
         }
@@ -864,9 +876,7 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
 #pragma unroll
       for (int z = 0; z < kYanTasks; ++z) {   // task t = (row il, 8-float group mg): lanes cover 8 rows x 4 groups
         const int t = tid + z * 256, il = (t >> 7) * 8 + (t & 7), mg = (t >> 3) & 15;
-        const float4* p = reinterpret_cast<const float4*>(src + (size_t)il * M + mg * 8);
-        x[z][0] = __ldg(p);
-        x[z][1] = __ldg(p + 1);
+        ld_global_256(src + (size_t)il * M + mg * 8, x[z][0], x[z][1]);   // 32 contiguous bytes, one load
       }
       if (++lkc == nK) { lkc = 0; lit = next_item(lit + gridDim.x); }
     }
