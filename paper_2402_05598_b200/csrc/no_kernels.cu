@@ -712,6 +712,66 @@ __global__ void __launch_bounds__(kThreads, 2) k_no_out_blob(const OutArgs<float
   if (mi > 0) window_dots_beta<true, kPerThread, V>(d, b, blk, it, mi, wv, rv);
 }
 
+
+// Wide-batch variant (B n^2 >= 2^21, no fused window dots): a CTA owns kOutRows rows of one system.  The
+// twiddles F[j][.] of a thread's column stay in registers over its rows, the y-synthesised rows are
+// built once per CTA, and a pixel costs 20 shared broadcasts and 40 FMAs (the tile variant above
+// reloads the whole twiddle table and re-derives its rows per 1,024 pixels).
+constexpr int kOutRows = 16;
+template <typename V>
+__global__ void __launch_bounds__(256) k_no_out_wide(const OutArgs<float> a) {
+  pdl_wait();
+  pdl_trigger();
+  const int b = blockIdx.y, n = a.n, N = a.N;
+  if (a.status && a.status[b] != SYS_RUNNING) return;
+  __shared__ float2 gh[kModes2];                 // g4 of this system
+  __shared__ __align__(16) float2 Gs[kOutRows][kModes];   // y-synthesised rows
+  const int rlo = blockIdx.x * kOutRows, nr = min(kOutRows, n - rlo);
+  for (int t = threadIdx.x; t < kModes2; t += blockDim.x) gh[t] = a.gh4[(size_t)t * a.B + b];   // mode-major
+  __syncthreads();
+  for (int e = threadIdx.x; e < nr * kModes; e += blockDim.x) {
+    const int r = e / kModes, k2 = e - r * kModes;
+    const float2* Fi = a.F + (size_t)(rlo + r) * kModes;
+    float gr = 0, gi = 0;
+#pragma unroll 4
+    for (int k1 = 0; k1 < kModes; ++k1) {
+      const float2 gg = gh[k1 * kModes + k2];
+      const float2 f = __ldg(Fi + k1);
+      gr += gg.x * f.x + gg.y * f.y;
+      gi += gg.y * f.x - gg.x * f.y;
+    }
+    Gs[r][k2] = make_float2(gr, gi);
+  }
+  __syncthreads();
+  const double s = sqrt(a.rr[b]);
+  const float cst = a.cst[0];
+  const int cols = n < 256 ? n : 256, rsub = 256 / cols;   // n = 64: 4 row sets, 128: 2, >= 256: 1
+  const int jl = threadIdx.x % cols, r0 = threadIdx.x / cols;
+  for (int jb = 0; jb < n; jb += cols) {
+    const int j = jb + jl;
+    float2 fj[kModes];
+    const float4* Fp = reinterpret_cast<const float4*>(a.F + (size_t)j * kModes);   // 160 bytes, 16-byte aligned
+#pragma unroll
+    for (int q = 0; q < kModes / 2; ++q) {
+      const float4 v = __ldg(Fp + q);
+      fj[2 * q] = make_float2(v.x, v.y);
+      fj[2 * q + 1] = make_float2(v.z, v.w);
+    }
+    for (int r = r0; r < nr; r += rsub) {
+      const size_t e = (size_t)b * N + (size_t)(rlo + r) * n + j;
+      float z = cst + __ldg(a.p3 + e);
+      const float4* Gr = reinterpret_cast<const float4*>(&Gs[r][0]);
+#pragma unroll
+      for (int q = 0; q < kModes / 2; ++q) {
+        const float4 g2 = Gr[q];
+        z += g2.x * fj[2 * q].x + g2.y * fj[2 * q].y;
+        z += g2.z * fj[2 * q + 1].x + g2.w * fj[2 * q + 1].y;
+      }
+      reinterpret_cast<V*>(a.wout)[e] = (V)(s * (double)z);   // w as stored (R21)
+    }
+  }
+}
+
 // ------------------------------------------------------------------ launcher
 // Largest dynamic shared memory a CTA may request on this device (opt-in limit).
 static int optin_smem() {
@@ -932,7 +992,11 @@ cudaError_t launch_no_forward(const NoDev<T>& no, const double* r, const double*
     if (tc_path) {
       oa.p3 = no.p3;
       const size_t bsmem = (size_t)(kModes2 + (size_t)nr_max * kModes + (size_t)kModes * n) * sizeof(float2) + kTile * sizeof(float);
-      if (v32) launch_k(k_no_out_blob<float>, dim3(nblk, B), dim3(kThreads), bsmem, s, oa, *fcg);
+      if (ew_wide(n, B) && !oa.use_dots) {   // wide batches (also the standalone apply on them: same kernel, same bits)
+        const dim3 wg((unsigned)((n + kOutRows - 1) / kOutRows), (unsigned)B);
+        if (v32) launch_k(k_no_out_wide<float>, wg, dim3(256), 0, s, oa);
+        else launch_k(k_no_out_wide<double>, wg, dim3(256), 0, s, oa);
+      } else if (v32) launch_k(k_no_out_blob<float>, dim3(nblk, B), dim3(kThreads), bsmem, s, oa, *fcg);
       else launch_k(k_no_out_blob<double>, dim3(nblk, B), dim3(kThreads), bsmem, s, oa, fcg ? *fcg : dummy);
     } else {
       if (v32) launch_k(k_no_out<T, float>, dim3(nblk, B), dim3(kThreads), osmem, s, oa, *fcg);
