@@ -24,7 +24,7 @@ constexpr int kDotChunk = 6;           // window dots reduced together
 constexpr int kRowSplitMax = 8;        // row parts per system of the FFMA NO layer (partial analyses)
 // rows per CTA of k_dft_rows (= row groups of the input DFT partials): 4 up to n = 128 (more CTAs
 // for the small grids), 8 above (fewer partials for k_lift_mix to sum); same-box A/B, DESIGN §5.7
-__host__ __device__ __forceinline__ int dft_rows(int n) { return n <= 128 ? 4 : 8; }
+__host__ __device__ __forceinline__ int dft_rows(int n) { return n <= 64 ? 4 : 8; }
 constexpr int kStR = 16;               // rows of a 2-D stencil tile
 constexpr int kStC = 128;              // columns of a 2-D stencil tile
 constexpr int kStThreads = 256;        // block size of the stencil-tile kernels
