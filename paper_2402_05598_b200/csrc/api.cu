@@ -121,10 +121,11 @@ NoWs<T> carve_no(Carver& c, int n, int B, int w) {
   NoWs<T> r{};
   const size_t N = (size_t)n * n;
   r.rpart = c.take<T>((size_t)B * ngroups_of(n) * kModes2 * 2);
-  r.ghat = c.take<T>((size_t)B * w * kModes2 * 2);
+  const size_t wp = (size_t)((w + 3) & ~3);   // tensor-core path: mode-major spectra rows padded to 32 bytes
+  r.ghat = c.take<T>((size_t)B * wp * kModes2 * 2);
   if (use_px(n, w, sizeof(T) == sizeof(float))) {
     r.rinv = c.take<double>(B);
-    r.chat = c.take<T>((size_t)kModes2 * B * w * 2);
+    r.chat = c.take<T>((size_t)kModes2 * B * wp * 2);
     r.vb_bytes = px_v_bytes(n, w, B);
     r.gb_bytes = px_g_bytes(n, w, B);
     r.vb0 = c.take<unsigned char>(r.vb_bytes);

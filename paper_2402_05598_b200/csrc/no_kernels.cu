@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) k_lift_mix(const typename Cplx<T>::type* 
       T gr = a0[q].x * rh.x - a0[q].y * rh.y + a1[q].x * kh[q].x - a1[q].y * kh[q].y;
       T gi = a0[q].x * rh.y + a0[q].y * rh.x + a1[q].x * kh[q].y + a1[q].y * kh[q].x;
       if (kk == k0) { gr += n2 * A2[o].x; gi += n2 * A2[o].y; }
-      const size_t at = mode_major ? ((size_t)kk * gridDim.x + b) * w + o : ((size_t)b * w + o) * kModes2 + kk;
+      const size_t at = mode_major ? ((size_t)kk * gridDim.x + b) * ((w + 3) & ~3) + o : ((size_t)b * w + o) * kModes2 + kk;
       ghat[at] = T2{gr * inv_n2, gi * inv_n2};
     }
   }

@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(kYsynThreads, 1) k_px_ysyn(const float2* __res
   const PxConst C(g);
   const PxYsynSmem L(g);
   extern __shared__ __align__(1024) unsigned char sm[];
-  const int NP = g.NP, N2 = 2 * NP, nkg = kModes / kg;
+  const int NP = g.NP, N2 = 2 * NP, nkg = kModes / kg, wp = (w + 3) & ~3;   // wp: row pitch of the spectra
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + L.bar);
   uint64_t *bfull = bar, *bfree = bar + 2, *dfull = bar + 4, *dfree = bar + 6, *abar = bar + 8;
@@ -710,7 +710,7 @@ __global__ void __launch_bounds__(kYsynThreads, 1) k_px_ysyn(const float2* __res
 #pragma unroll
           for (int e = 0; e < 12; ++e) {
             const int k1 = hh * 12 + e;
-            gg[e] = (k1 < kModes && o < w) ? __ldg(ghat + ((size_t)(k1 * kModes + k2) * B + b) * w + o) : make_float2(0.f, 0.f);
+            gg[e] = (k1 < kModes && o < w) ? __ldg(ghat + ((size_t)(k1 * kModes + k2) * B + b) * wp + o) : make_float2(0.f, 0.f);
           }
 #pragma unroll
           for (int kq = 0; kq < 3; ++kq) {
@@ -927,8 +927,9 @@ __global__ void __launch_bounds__(256) k_px_yan(const float* __restrict__ T, con
       tc::tmem_wait_ld();
       const int m = m0 + warp * 32 + lane, pr = m >> 1, k2 = pr / w, o = pr - k2 * w;
       const bool re = (lane & 1) == 0;
-      float2* dst = chat + ((size_t)k2 * B + b) * w + o;            // mode (k1, k2) at dst + k1 * 20 B w
-      const size_t kstride = (size_t)kModes * B * w;
+      const int wp = (w + 3) & ~3;                                    // row pitch of the mode-major spectra
+      float2* dst = chat + ((size_t)k2 * B + b) * wp + o;           // mode (k1, k2) at dst + k1 * 20 B wp
+      const size_t kstride = (size_t)kModes * B * wp;
 #pragma unroll
       for (int k1 = 0; k1 < kModes; ++k1) {
         const float xv = __uint_as_float(v[2 * k1]), yv = __uint_as_float(v[2 * k1 + 1]);
@@ -970,7 +971,7 @@ constexpr int kMixSys = 64;   // systems per work item (2 A rows each)
 __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat, const unsigned char* __restrict__ mx,
                                                float2* __restrict__ ghat, int w, int B, int cout, float inv_n2,
                                                const int* status) {
-  const int KM = (2 * w + 15) & ~15, NM = (cout + 15) & ~15;
+  const int KM = (2 * w + 15) & ~15, NM = (cout + 15) & ~15, wp = (w + 3) & ~3;   // wp: row pitch of the spectra
   const MixSmem L(KM, NM);
   extern __shared__ __align__(1024) unsigned char sm[];
   const uint32_t SBO = (KM / 8) * 128, a_half = 128u * KM * 2, b_half = (uint32_t)NM * KM * 2;
@@ -1002,31 +1003,34 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
   uint32_t ph = 0;
   for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     const int kk = it / nbc, b0 = (it % nbc) * kMixSys, nb = min(kMixSys, B - b0);
-    // A: rows (b, re|im), K = (c, re|im); all loads of a batch first
+    // A: rows (b, re|im), K = (c, re|im); all loads of a batch first.  A task's four channels are 32
+    // contiguous, 32-byte aligned bytes (spectra rows are padded to wp = 4-channel multiples): one 256-bit
+    // load per task instead of four 8-byte loads that each cost the load unit a pass over 32 scattered lines
     {
       constexpr int kBatch = 8;
       const int ntask = kMixSys * (KM / 8);
       for (int t0 = tid; t0 < ntask; t0 += kBatch * blockDim.x) {
-        float2 x[kBatch][4];
+        float4 x[kBatch][2];
 #pragma unroll
         for (int z = 0; z < kBatch; ++z) {
           const int t = t0 + z * blockDim.x, bl = t % kMixSys, kc = t / kMixSys;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int c = kc * 4 + q;
-            x[z][q] = (t < ntask && bl < nb && c < w) ? __ldg(chat + ((size_t)kk * B + b0 + bl) * w + c)
-                                                      : make_float2(0.f, 0.f);
-          }
+          if (t < ntask && bl < nb && kc * 4 < wp)
+            ld_global_256(reinterpret_cast<const float*>(chat + ((size_t)kk * B + b0 + bl) * wp + kc * 4), x[z][0], x[z][1]);
+          else
+            x[z][0] = x[z][1] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int z = 0; z < kBatch; ++z) {
           const int t = t0 + z * blockDim.x, bl = t % kMixSys, kc = t / kMixSys;
           if (t >= ntask) break;
+          const float cr[4] = {x[z][0].x, x[z][0].z, x[z][1].x, x[z][1].z}, ci[4] = {x[z][0].y, x[z][0].w, x[z][1].y, x[z][1].w};
           float vr[8], vi[8];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            vr[2 * q] = x[z][q].x;  vr[2 * q + 1] = -x[z][q].y;
-            vi[2 * q] = x[z][q].y;  vi[2 * q + 1] = x[z][q].x;
+            const bool in = kc * 4 + q < w;          // the row's padding holds no data
+            const float re = in ? cr[q] : 0.f, im = in ? ci[q] : 0.f;
+            vr[2 * q] = re;  vr[2 * q + 1] = -im;
+            vi[2 * q] = im;  vi[2 * q + 1] = re;
           }
           const uint32_t offr = tc::kmajor_off(2 * bl, kc * 8, SBO, 128), offi = tc::kmajor_off(2 * bl + 1, kc * 8, SBO, 128);
           store_split8(sm + L.A + offr, sm + L.A + a_half + offr, vr);
@@ -1058,6 +1062,7 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
       // even lane writes o in [c0, c0+4) and the odd lane o in [c0+4, c0+8) as float2 runs
       const int row = warp * 32 + lane, bl = row >> 1, p = row & 1, b = b0 + bl;
       const bool ok = bl < nb && (!status || status[b] == SYS_RUNNING);
+      const int coutp = cout == 1 ? 1 : wp;          // output row pitch (padded like the input's)
       for (int c0 = 0; c0 < cout; c0 += 8) {
         uint32_t u[8];
         tmem_ld8(tmem + ((uint32_t)(warp * 32) << 16) + c0, u);
@@ -1071,13 +1076,19 @@ __global__ void __launch_bounds__(128) k_mix_tc(const float2* __restrict__ chat,
           other[q] = __shfl_xor_sync(0xffffffffu, give, 1);
         }
         if (ok) {
+          float2 o4[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const int o = c0 + 4 * p + q;
-            if (o < cout) {
-              const float gr = p ? other[q] : mine[q], gi = p ? mine[q] : other[q];
-              ghat[((size_t)kk * B + b) * cout + o] = make_float2(gr * inv_n2, gi * inv_n2);
-            }
+            const float gr = p ? other[q] : mine[q], gi = p ? mine[q] : other[q];
+            o4[q] = make_float2(gr * inv_n2, gi * inv_n2);
+          }
+          float2* dst = ghat + ((size_t)kk * B + b) * coutp + c0 + 4 * p;
+          if (cout > 1) {   // 4 channels = 32 aligned bytes (columns >= cout of the padded row receive zeros)
+            if (c0 + 4 * p < coutp)
+              st_global_256(dst, make_uint4(__float_as_uint(o4[0].x), __float_as_uint(o4[0].y), __float_as_uint(o4[1].x), __float_as_uint(o4[1].y)),
+                            make_uint4(__float_as_uint(o4[2].x), __float_as_uint(o4[2].y), __float_as_uint(o4[3].x), __float_as_uint(o4[3].y)));
+          } else if (p == 0) {
+            dst[0] = o4[0];
           }
         }
       }
