@@ -51,6 +51,8 @@ def main():
     ap.add_argument("--dataset", choices=["diffusion", "poisson", "lognormal"], default="diffusion")
     ap.add_argument("--e-scale", type=float, default=None, help="unit of the target (default (n+1)^2)")
     ap.add_argument("--lr", type=float, default=1e-3)
+    ap.add_argument("--m-test", type=int, nargs="*", default=[], help="extra FCG windows m for the held-out solves (P:406 uses m_max = 20)")
+    ap.add_argument("--save", default=None, help="write the trained weight blob (.npy)")
     args = ap.parse_args()
     c = dict(CONFIGS[args.config])
     n, w, m = c["n"], args.width or c["width"], c["m"]
@@ -90,11 +92,11 @@ def main():
             ls.append(tr.loss_grad(kte, rh, eh, perm=perm, ksys=ksh, grad=False))
         return float(torch.cat(ls).mean())
 
-    def fcg_counts(no):
-        res = fcgno.fcg_solve(p_te, dev(f_te), dev(u0_te), m=m, tol=args.tol, maxit=args.maxit, no=no, history=False)
+    def fcg_counts(no, mm=None):
+        res = fcgno.fcg_solve(p_te, dev(f_te), dev(u0_te), m=mm or m, tol=args.tol, maxit=args.maxit, no=no, history=False)
         it = res.iters.cpu().numpy()
         st = res.status.cpu().numpy()
-        return dict(mean=float(it.mean()), min=int(it.min()), max=int(it.max()),
+        return dict(mean=float(it.mean()), median=float(np.median(it)), min=int(it.min()), max=int(it.max()),
                     converged=int((st == fcgno.CONVERGED).sum()), systems=int(st.size))
 
     random_no = fcgno.NeuralOperator(w, sy.no_weights(w, 7 + args.seed))
@@ -110,6 +112,11 @@ def main():
     train_ms = start.elapsed_time(end)
     no = ptr.trained_operator(tr)
     after = dict(held_out_loss=held_out_loss(), fcg_no=fcg_counts(no))
+    for mm in args.m_test:
+        after[f"fcg_no_m{mm}"] = fcg_counts(no, mm)
+        after[f"fcg_identity_m{mm}"] = fcg_counts(None, mm)
+    if args.save:
+        np.save(args.save, np.ascontiguousarray(tr.blob()))
     samples = int(r.shape[0])
     out = dict(
         what="SNO trained on the GPU (Fig. 3 scheme), FCG-NO on held-out systems vs FCG(I)",
