@@ -189,8 +189,9 @@ FCGNO_API int fcgno_apply_NO(const fcgno_problem* p, fcgno_no_desc d, const void
  *   ws       fcgno_solve_workspace_bytes(g, d_or_null, o) bytes.
  * Converged systems are frozen (no further writes).  The iteration loop runs on the device (a
  * CUDA-graph WHILE node on an on-device "systems running" counter); instantiated graphs are reused
- * by later solves with identical arguments.  Synchronises `stream` before returning (iteration
- * count, final lazy x update). */
+ * by later solves with identical arguments.  Identity solves of small systems (n^2 <= 1024, fp64
+ * vectors, ring fitting shared memory) run as one persistent kernel, one CTA per system, with the same
+ * arithmetic.  Synchronises `stream` before returning (iteration count, final lazy x update). */
 FCGNO_API size_t fcgno_solve_workspace_bytes(fcgno_grid g, const fcgno_no_desc* d_or_null, fcgno_solve_opts o);
 FCGNO_API int fcgno_fcg_solve(const fcgno_problem* p, const fcgno_no_desc* d_or_null, const void* packed,
                     const double* f, double* u, fcgno_solve_opts o, int32_t* iters,

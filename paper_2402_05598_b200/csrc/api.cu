@@ -926,6 +926,7 @@ int solve_impl(const fcgno_problem* p, const fcgno_no_desc* nd, const void* pack
     d.scale = double(p->n + 1) * double(p->n + 1);
     d.k = p->k; d.f = f; d.u = u; d.status = status; d.iters = iters; d.hist = history;
     CK(launch_fcg_small(d, static_cast<cudaStream_t>(stream)));
+    CK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));   // the entry's contract: complete on return
     return FCGNO_OK;
   }
   if (nd) {
