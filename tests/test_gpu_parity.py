@@ -157,7 +157,10 @@ def test_no_fp64_matches_oracle(lib, n, B, w):
         assert rel_l2(got[b], ref) <= 1e-12
 
 
-@pytest.mark.parametrize("n,B,w", [(20, 2, 4), (32, 2, 32), (45, 3, 48), (64, 8, 48), (128, 2, 85)])
+# tensor-core shapes (n = 64 or 128 k) include widths with every remainder modulo 4 (padded spectra rows) and
+# the largest width
+@pytest.mark.parametrize("n,B,w", [(20, 2, 4), (32, 2, 32), (45, 3, 48), (64, 8, 48), (128, 2, 85), (64, 3, 5),
+                                   (128, 1, 23), (64, 2, 126), (64, 2, 128)])
 def test_no_fp32_matches_oracle(lib, n, B, w):
     k, r, blob = _no_case(n, B, w, 21, 22)
     prob = lib.Problem(dev(k))
