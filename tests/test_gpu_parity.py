@@ -562,7 +562,8 @@ def _identity_in_subprocess(env_extra, tag, n, B, m, maxit, schedule=0, nan_firs
     return z["u"], z["h"], z["it"], z["st"]
 
 
-@pytest.mark.parametrize("n,B,m,maxit,schedule", [(32, 3, 5, 500, 0), (32, 2, 10, 60, 1), (19, 4, 7, 25, 0), (8, 2, 64, 200, 1)])
+@pytest.mark.parametrize("n,B,m,maxit,schedule", [(32, 3, 5, 500, 0), (32, 2, 10, 60, 1), (19, 4, 7, 25, 0), (8, 2, 64, 200, 1),
+                                                    (12, 400, 4, 80, 0)])   # the last: more systems than CTA slots
 def test_persistent_small_solve_matches_launch_per_step_path(lib, n, B, m, maxit, schedule):
     """The single-kernel solve of small identity systems (fcg_small.cu) against the general
     path (FCGNO_PERSISTENT=0) on the same inputs: iterates, histories, counts and statuses bitwise, with
